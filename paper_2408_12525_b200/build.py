@@ -1,0 +1,73 @@
+"""Build recipe for the in-tree CUDA library (sm_100a only).
+
+``python -m paper_2408_12525_b200.build`` compiles ``csrc/pcgrl_b200.cu`` into
+``paper_2408_12525_b200/libpcgrl_b200.so`` with nvcc. The shared object is
+git-ignored but travels with the repo snapshot to the GPU box.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+SRC = os.path.join(PKG, "csrc", "pcgrl_b200.cu")
+DEPS = [os.path.join(PKG, "csrc", f) for f in ("pcgrl_b200.cu", "env_kernels.cuh", "team.cuh", "rng.cuh")] + [
+    os.path.join(ROOT, "include", "pcgrl_b200.h")]
+LIB = os.path.join(PKG, "libpcgrl_b200.so")
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-fmad=false", "-prec-div=true", "-prec-sqrt=true",
+    "-Xcompiler", "-fPIC", "-shared",
+    "-Xptxas", "-v",
+]
+
+
+def nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def source_hash() -> str:
+    import hashlib
+    h = hashlib.sha256(" ".join(NVCC_FLAGS).encode())
+    for d in DEPS:
+        with open(d, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()
+
+
+def stale() -> bool:
+    """True when the .so is missing or was built from other sources/flags."""
+    if not os.path.exists(LIB) or not os.path.exists(LIB + ".hash"):
+        return True
+    with open(LIB + ".hash") as f:
+        return f.read().strip() != source_hash()
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not stale():
+        return LIB
+    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), SRC, "-o", LIB + ".tmp"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("nvcc failed building libpcgrl_b200.so")
+    os.replace(LIB + ".tmp", LIB)
+    with open(LIB + ".hash", "w") as f:
+        f.write(source_hash())
+    with open(os.path.join(PKG, "build_ptxas.log"), "w") as f:
+        f.write(res.stdout + res.stderr)
+    if verbose:
+        sys.stdout.write(res.stdout + res.stderr)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose=True)

@@ -1,0 +1,856 @@
+// env_kernels.cuh -- the fused batched env step for sm_100a.
+//
+// One launch of env_kernel<G, DOM> advances a block of E = blockDim/TEAM
+// environments (reference _Core.step, levelgen/env.py:355-393) and then
+// streams their observations (build_observation, env.py:186-233) to HBM:
+//
+//   phase 1 (team per env, registers + shared memory)
+//     load state -> apply action (narrow/turtle/wide) -> recompute metrics on
+//     a real change (problems.py:105-243) -> loss delta reward (251-279) ->
+//     advance scan position -> done / info -> in-kernel auto-reset
+//     (reset_rows, env.py:284-305, numpy-exact draws) -> store state ->
+//     render the env's 0/1 observation planes as a bit image in shared memory
+//   phase 2 (whole block)
+//     expand the bit images of the block's envs (contiguous in the output) to
+//     float32 with coalesced 128-bit streaming stores (st.global.cs.v4).
+//
+// The observation write is the HBM roofline of the path (15,376 B per env-step
+// for binary 16x16 / obs 31 against ~330 B of state traffic).
+#pragma once
+#include <stdint.h>
+
+#include "rng.cuh"
+#include "team.cuh"
+
+namespace lg {
+
+enum { MODE_STEP = 0, MODE_RESET = 1, MODE_OBSERVE = 2 };
+enum { REP_NARROW = 0, REP_TURTLE = 1, REP_WIDE = 2 };
+enum { FLAG_BAD_ACTION = 1, FLAG_NO_EDITABLE = 2, FLAG_PINPOINTS = 4 };
+
+// Domain tables (tiles.py:126-171). Stored bit-planes are tile ids 1..N-1
+// (plane p <-> tile p+1); AIR is "active and in no plane", BORDER is "inactive".
+template <int DOM>
+struct Dom;
+template <>
+struct Dom<0> {  // binary: AIR 0, WALL 1
+    static constexpr int N = 2, M = 2, NPL = 1;
+};
+template <>
+struct Dom<1> {  // maze: AIR 0, WALL 1, PLAYER 2, DOOR 3
+    static constexpr int N = 4, M = 4, NPL = 3;
+};
+template <>
+struct Dom<2> {  // dungeon: AIR 0, WALL 1, ENEMY 2, KEY 3, DOOR 4, PLAYER 5
+    static constexpr int N = 6, M = 7, NPL = 5;
+};
+
+struct FastDiv {  // n / d for n, d < 2^31 (mul-hi + shift)
+    uint32_t d, mul, shr;
+};
+__device__ __forceinline__ uint32_t fdiv(const FastDiv &f, uint32_t n) {
+    return f.d == 1 ? n : (__umulhi(n, f.mul) >> f.shr);
+}
+
+// Per-env hot scalars, 32 bytes.
+struct __align__(16) Hot {
+    uint32_t geo;     // h | w << 8 | pos_r << 16 | pos_c << 24
+    int32_t pos_idx;  // narrow scan index
+    int32_t order_len;
+    int32_t changes;
+    int64_t t;
+    int64_t max_steps;
+};
+
+struct Params {
+    // config
+    int B, H, W, rep, OH, OW, half;
+    int randomize, weighted, n_pins, n_ctrl, det;
+    long long max_steps, budget;
+    long long n_actions, goffset;
+    int pins[16];
+    int ctrl[8];
+    double cdf[8];
+    double w[8];
+    // state (library owned)
+    void *rows;          // Row [B][NPL+1][ROWS]; plane NPL = frozen
+    Hot *hot;            // [B]
+    int *mv;             // [B][24]: values 0..6, unreach mask at 7, lo 8..14, hi 16..22
+    double *lossv;       // [B][4]: prev_loss, ep_reward, ep_start_loss, -
+    ulonglong2 *rs;      // [B] PCG state (hi, lo)
+    ulonglong2 *ri;      // [B] PCG inc (hi, lo)
+    uint2 *rb;           // [B] (has_uint32, uinteger)
+    long long *mseed;    // [B]
+    unsigned *err;       // error flags
+    // io
+    const long long *actions;
+    float *obs;
+    double *reward;
+    unsigned char *done, *terminal;
+    double *ep_rew;
+    long long *ep_len;
+    double *ep_start, *fin_loss;
+    double *stats;  // [5]
+    const unsigned char *reset_mask;
+    // observation writer
+    uint32_t PE, PB, OO;  // floats per env, bit-plane elements per env, OH*OW
+    FastDiv divPE, divOO;
+    int img_words;  // u32 words of one env's bit image (incl. 1 pad word)
+    int env_smem;   // bytes of shared memory per env
+    int off_ctrl;   // byte offset of the control floats within an env's smem
+};
+
+template <class G, int DOM>
+struct EnvRegs {
+    using Row = typename G::Row;
+    Bd<G> pl[Dom<DOM>::NPL];  // tile planes
+    Bd<G> frz;                // frozen plane
+    int h, w, pr, pc, pos_idx, order_len, changes;
+    long long t, max_steps;
+    int val[8], lo[8], hi[8];
+    int unr;
+    double prev_loss, ep_reward, ep_start_loss;
+    Pcg g;
+    long long mseed;
+};
+
+template <class G>
+__device__ __forceinline__ Bd<G> rect_board(const Team<G> &t, int h, int w) {
+    Bd<G> a;
+#pragma unroll
+    for (int k = 0; k < G::RPL; k++) a.r[k] = t.row(k) < h ? low_mask<typename G::Row>(w) : 0;
+    return a;
+}
+
+// ---------------------------------------------------------------------------
+// metrics (problems.py:105-243) -- values, unreachable mask
+// ---------------------------------------------------------------------------
+
+template <class G>
+__device__ int kth_cell(const Team<G> &t, const Bd<G> &m, int k) {
+    // flat index (row * 64 + col) of the k-th set cell in row-major order
+    int c = m.count();
+    int inc = t.scan(c);
+    int exc = inc - c;
+    unsigned own = t.ballot(exc <= k && k < inc);
+    int src = __ffs((int)own) - 1;
+    int res = 0;
+    if (t.lane == src) {
+        int kk = k - exc;
+#pragma unroll
+        for (int j = 0; j < G::RPL; j++) {
+            int cj = popc(m.r[j]);
+            if (kk >= 0 && kk < cj) {
+                auto x = m.r[j];
+                for (int i = 0; i < kk; i++) x &= x - 1;
+                res = t.row(j) * 64 + ctz(x);
+            }
+            kk -= cj;
+        }
+    }
+    return t.from(res, src);
+}
+
+template <class G>
+__device__ int lowest_cell(const Team<G> &t, const Bd<G> &m) {
+    unsigned own = t.ballot(m.nz());
+    int src = __ffs((int)own) - 1;
+    int res = 0;
+    if (t.lane == src) {
+        bool found = false;
+#pragma unroll
+        for (int j = 0; j < G::RPL; j++)
+            if (!found && m.r[j]) {
+                res = t.row(j) * 64 + ctz(m.r[j]);
+                found = true;
+            }
+    }
+    return t.from(res, src);
+}
+
+template <class G>
+__device__ __forceinline__ Bd<G> cell_board(const Team<G> &t, int flat) {
+    Bd<G> b;
+#pragma unroll
+    for (int k = 0; k < G::RPL; k++)
+        b.r[k] = t.row(k) == (flat >> 6) ? (typename G::Row(1) << (flat & 63)) : 0;
+    return b;
+}
+
+template <class G>
+__device__ __forceinline__ int team_count(const Team<G> &t, const Bd<G> &b) {
+    return t.sum(b.count());
+}
+
+// pl: tile planes, act: active board. g: the metric generator (binary only).
+template <class G, int DOM>
+__device__ void compute_metrics(const Team<G> &t, const Bd<G> *pl, const Bd<G> &act,
+                                typename G::Row wm, Pcg &g, uint16_t *uf, int *val, int &unr) {
+    unr = 0;
+    if constexpr (DOM == 0) {
+        // _binary_metrics (problems.py:136-173)
+        Bd<G> pass = andnot(act, pl[0]);
+        val[1] = count_regions(t, pass, uf);
+        int cnt = team_count(t, pass);
+        val[0] = 0;
+        if (cnt > 0) {
+            int k = (int)pcg_integers(g, 0, cnt);  // problems.py:152-154
+            Bd<G> f = cell_board(t, kth_cell(t, pass, k));
+            bfs_last_layer(t, f, pass, wm);
+            int y = lowest_cell(t, f);  // np.argmax: lowest flat index at max d1
+            Bd<G> f2 = cell_board(t, y);
+            val[0] = bfs_last_layer(t, f2, pass, wm);
+        }
+    } else if constexpr (DOM == 1) {
+        // _maze_metrics (problems.py:176-198)
+        Bd<G> pass = andnot(act, pl[0]);  // AIR | PLAYER | DOOR
+        const Bd<G> &players = pl[1], &doors = pl[2];
+        int np = team_count(t, players), nd = team_count(t, doors);
+        val[2] = np;
+        val[3] = nd;
+        val[1] = count_regions(t, pass, uf);
+        int d = -1, dummy;
+        if (np > 0 && nd > 0) bfs_touch<G, false>(t, players, pass, wm, doors, doors, false, d, dummy);
+        bool bad = d < 0;
+        val[0] = bad ? 0 : d;
+        unr = bad ? 1 : 0;
+    } else {
+        // _dungeon_metrics (problems.py:201-243); planes WALL ENEMY KEY DOOR PLAYER
+        const Bd<G> &enemy = pl[1], &key = pl[2], &door = pl[3], &player = pl[4];
+        Bd<G> trav = andnot(andnot(andnot(andnot(act, pl[0]), enemy), key), door);  // AIR|PLAYER
+        int cp = team_count(t, player), ck = team_count(t, key), cd = team_count(t, door),
+            ce = team_count(t, enemy);
+        val[2] = cp;
+        val[3] = ck;
+        val[4] = cd;
+        val[5] = ce;
+        int leg1 = -1, nearv = -1, leg2 = -1, dummy;
+        if (cp > 0) bfs_touch<G, true>(t, player, trav, wm, key, enemy, true, leg1, nearv);
+        bool missing = cp == 0 || ck == 0 || cd == 0;
+        if (!missing && leg1 >= 0) bfs_touch<G, true>(t, key, trav, wm, door, door, false, leg2, dummy);
+        bool bad = missing || leg1 < 0 || leg2 < 0;
+        val[0] = bad ? 0 : leg1 + leg2;
+        bool badn = cp == 0 || ce == 0 || nearv < 0;
+        val[6] = badn ? 0 : nearv;
+        unr = (bad ? 1 : 0) | (badn ? 64 : 0);
+        Bd<G> open = andnot(andnot(act, pl[0]), enemy);  // AIR|PLAYER|KEY|DOOR
+        val[1] = count_regions(t, open, uf);
+    }
+}
+
+// loss_batch (problems.py:251-279): canonical order, explicit IEEE ops (no FMA).
+template <int DOM>
+__device__ double loss_of(const Params &p, const int *val, int unr, const int *lo, const int *hi) {
+    constexpr int M = Dom<DOM>::M;
+    double wreg = p.w[1];
+    double total = 0.0;
+#pragma unroll
+    for (int m = 0; m < M; m++) {
+        double wm = p.w[m];
+        double x = (double)val[m], l = (double)lo[m], h = (double)hi[m];
+        double a = __dsub_rn(l, x), b = __dsub_rn(x, h);
+        a = a > 0.0 ? a : 0.0;
+        b = b > 0.0 ? b : 0.0;
+        double term = __dmul_rn(wm, __dadd_rn(a, b));
+        bool path = (DOM == 1 && m == 0) || (DOM == 2 && (m == 0 || m == 6));
+        if (path && ((unr >> m) & 1)) term = __dadd_rn(__dmul_rn(wm, h), wreg);
+        total = m == 0 ? term : __dadd_rn(total, term);
+    }
+    return total;
+}
+
+// _recompute (env.py:332-347)
+template <class G, int DOM>
+__device__ void recompute(const Params &p, const Team<G> &t, EnvRegs<G, DOM> &e, uint16_t *uf,
+                          bool reset) {
+    using Row = typename G::Row;
+    Row wm = low_mask<Row>(p.W);
+    Bd<G> act = rect_board(t, e.h, e.w);
+    if (p.det) {  // _metric_rngs: fresh default_rng(metric_seed) (env.py:327-330)
+        Pcg mg;
+        seedseq_pcg((uint64_t)e.mseed, false, 0, mg);
+        compute_metrics<G, DOM>(t, e.pl, act, wm, mg, uf, e.val, e.unr);
+    } else {
+        compute_metrics<G, DOM>(t, e.pl, act, wm, e.g, uf, e.val, e.unr);
+    }
+    double l = loss_of<DOM>(p, e.val, e.unr, e.lo, e.hi);
+    e.prev_loss = l;
+    if (reset) {
+        e.ep_reward = 0.0;
+        e.ep_start_loss = l;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// scan order (env.py:155-178) without materialising the order array
+// ---------------------------------------------------------------------------
+
+// first editable cell in boustrophedon order from row `r0` on (inclusive);
+// returns flat row*64+col or -1.
+template <class G>
+__device__ int serp_first_from(const Team<G> &t, const Bd<G> &ed, int r0) {
+    int best = 0x7fffffff;
+#pragma unroll
+    for (int k = 0; k < G::RPL; k++) {
+        int r = t.row(k);
+        if (r >= r0 && ed.r[k]) best = min(best, r);
+    }
+    // team min over rows
+    unsigned own = t.ballot(best != 0x7fffffff);
+    if (!own) return -1;
+    int cand = best;
+#pragma unroll
+    for (int o = G::TEAM / 2; o > 0; o >>= 1) cand = min(cand, __shfl_xor_sync(t.mask, cand, o, G::TEAM));
+    int row = cand;
+    int src = row / G::RPL;
+    int res = 0;
+    if (t.lane == src) {
+#pragma unroll
+        for (int k = 0; k < G::RPL; k++)
+            if (t.row(k) == row) res = row * 64 + ((row & 1) ? msb(ed.r[k]) : ctz(ed.r[k]));
+    }
+    return t.from(res, src);
+}
+
+// next editable cell strictly after (r, c) in scan order; -1 if none.
+template <class G>
+__device__ int serp_next(const Team<G> &t, const Bd<G> &ed, int r, int c) {
+    using Row = typename G::Row;
+    int src = r / G::RPL;
+    int res = -1;
+    if (t.lane == src) {
+#pragma unroll
+        for (int k = 0; k < G::RPL; k++)
+            if (t.row(k) == r) {
+                Row x = ed.r[k];
+                if (r & 1) {
+                    Row below = c == 0 ? Row(0) : low_mask<Row>(c);
+                    x &= below;
+                    if (x) res = r * 64 + msb(x);
+                } else {
+                    Row above = c >= G::BITS - 1 ? Row(0) : ~low_mask<Row>(c + 1);
+                    x &= above;
+                    if (x) res = r * 64 + ctz(x);
+                }
+            }
+    }
+    res = t.from(res, src);
+    if (res >= 0) return res;
+    return serp_first_from(t, ed, r + 1);
+}
+
+// ---------------------------------------------------------------------------
+// reset_rows for one env (env.py:284-325; grid.py:116-225; problems.py:48-90)
+// ---------------------------------------------------------------------------
+
+template <class G, int DOM>
+__device__ void reset_env(const Params &p, const Team<G> &t, EnvRegs<G, DOM> &e, uint16_t *uf) {
+    using Row = typename G::Row;
+    constexpr int N = Dom<DOM>::N, NPL = Dom<DOM>::NPL, M = Dom<DOM>::M;
+    Pcg &g = e.g;
+    int h = p.H, w = p.W;
+    if (p.randomize) {  // sample_shape: width then height (grid.py:124-125)
+        w = (int)pcg_integers(g, 3, p.W + 1);
+        h = (int)pcg_integers(g, 3, p.H + 1);
+    }
+    e.h = h;
+    e.w = w;
+    Bd<G> act = rect_board(t, h, w);
+#pragma unroll
+    for (int q = 0; q < NPL; q++) e.pl[q] = Bd<G>::zero();
+    e.frz = andnot(rect_board(t, p.H, p.W), act);  // apply_shape: inactive cells frozen
+    if (p.weighted) {
+        // init_random: one choice(n_tiles, (h, w), p) block, row-major doubles
+        // (grid.py:169-191); each row-lane jumps to its slice of the stream.
+#pragma unroll
+        for (int k = 0; k < G::RPL; k++) {
+            int r = t.row(k);
+            if (r < h) {
+                Pcg g2 = g;
+                pcg_advance(g2, (uint64_t)r * (uint64_t)w);
+                for (int c = 0; c < w; c++) {
+                    double u = pcg_double(g2);
+                    int idx = 0;
+#pragma unroll
+                    for (int q = 0; q < N; q++) idx += (p.cdf[q] <= u) ? 1 : 0;  // searchsorted right
+                    idx = idx < N - 1 ? idx : N - 1;
+                    if (idx > 0) {
+#pragma unroll
+                        for (int q = 0; q < NPL; q++)
+                            if (q == idx - 1) e.pl[q].r[k] |= Row(1) << c;
+                    }
+                }
+            }
+        }
+        pcg_advance(g, (uint64_t)h * (uint64_t)w);
+    }
+    if (p.n_pins > 0) {
+        // place_pinpoints: choice(h*w, k, replace=False) over the free cells,
+        // which are exactly the h x w rectangle in row-major order here.
+        int pop = h * w;
+        if (pop < p.n_pins) {
+            if (t.lane == 0) atomicOr(p.err, (unsigned)FLAG_PINPOINTS);
+        } else {
+            int picks[16];
+            int k = p.n_pins;
+            for (int j = pop - k; j < pop; j++) {  // Floyd
+                int val = (int)pcg_bounded(g, (uint64_t)j);
+                bool seen = false;
+                for (int i = 0; i < j - (pop - k); i++) seen |= picks[i] == val;
+                picks[j - (pop - k)] = seen ? j : val;
+            }
+            for (int i = k - 1; i > 0; i--) {  // bounded Fisher-Yates
+                int j = (int)pcg_bounded(g, (uint64_t)i);
+                int tmp = picks[i];
+                picks[i] = picks[j];
+                picks[j] = tmp;
+            }
+            for (int i = 0; i < k; i++) {
+                int r = picks[i] / w, c = picks[i] % w, tile = p.pins[i];
+#pragma unroll
+                for (int kk = 0; kk < G::RPL; kk++)
+                    if (t.row(kk) == r) {
+                        Row bit = Row(1) << c;
+#pragma unroll
+                        for (int q = 0; q < NPL; q++) {
+                            e.pl[q].r[kk] &= ~bit;
+                            if (q == tile - 1) e.pl[q].r[kk] |= bit;
+                        }
+                        e.frz.r[kk] |= bit;
+                    }
+            }
+        }
+    }
+    // default_targets + sample_control_targets (problems.py:48-90)
+    int cap = h * w;
+#pragma unroll
+    for (int m = 0; m < M; m++) {
+        int lo = 1, hi = 1;
+        if (m == 0) lo = hi = cap;  // maximize: diameter / path_length / pkd_path
+        if (DOM == 2 && m == 5) {
+            lo = 2;
+            hi = 5;
+        }
+        if (DOM == 2 && m == 6) {
+            lo = 4;
+            hi = cap;
+        }
+        for (int j = 0; j < p.n_ctrl; j++)
+            if (p.ctrl[j] == m) lo = hi = (int)pcg_integers(g, 0, (int64_t)cap + 1);
+        e.lo[m] = lo;
+        e.hi[m] = hi;
+    }
+    if (p.det) e.mseed = (long long)pcg_bounded(g, 0x7FFFFFFFFFFFFFFFULL);  // env.py:302-303
+    // _install_row (env.py:307-325)
+    Bd<G> ed = andnot(act, e.frz);
+    e.order_len = team_count(t, ed);
+    int first = serp_first_from(t, ed, 0);
+    if (first < 0) {
+        if (t.lane == 0) atomicOr(p.err, (unsigned)FLAG_NO_EDITABLE);
+        first = 0;
+    }
+    e.pr = first >> 6;
+    e.pc = first & 63;
+    e.pos_idx = 0;
+    e.t = 0;
+    e.changes = 0;
+    e.max_steps = p.max_steps > 0 ? p.max_steps : 3LL * cap;
+    recompute<G, DOM>(p, t, e, uf, true);
+}
+
+// ---------------------------------------------------------------------------
+// state load / store
+// ---------------------------------------------------------------------------
+
+template <class G, int DOM>
+__device__ __forceinline__ typename G::Row *rows_of(const Params &p, long long env) {
+    return reinterpret_cast<typename G::Row *>(p.rows) +
+           (size_t)env * (Dom<DOM>::NPL + 1) * G::ROWS;
+}
+
+template <class G, int DOM>
+__device__ void load_env(const Params &p, const Team<G> &t, long long env, EnvRegs<G, DOM> &e) {
+    constexpr int NPL = Dom<DOM>::NPL;
+    const typename G::Row *rw = rows_of<G, DOM>(p, env);
+#pragma unroll
+    for (int q = 0; q <= NPL; q++) {
+#pragma unroll
+        for (int k = 0; k < G::RPL; k++) {
+            auto v = rw[q * G::ROWS + t.row(k)];
+            if (q < NPL) e.pl[q].r[k] = v;
+            else e.frz.r[k] = v;
+        }
+    }
+    Hot hv = p.hot[env];
+    e.h = hv.geo & 255;
+    e.w = (hv.geo >> 8) & 255;
+    e.pr = (hv.geo >> 16) & 255;
+    e.pc = hv.geo >> 24;
+    e.pos_idx = hv.pos_idx;
+    e.order_len = hv.order_len;
+    e.changes = hv.changes;
+    e.t = hv.t;
+    e.max_steps = hv.max_steps;
+    const int4 *mv = reinterpret_cast<const int4 *>(p.mv + env * 24);
+    int4 a = mv[0], b = mv[1], c = mv[2], d = mv[3], f = mv[4], h2 = mv[5];
+    e.val[0] = a.x; e.val[1] = a.y; e.val[2] = a.z; e.val[3] = a.w;
+    e.val[4] = b.x; e.val[5] = b.y; e.val[6] = b.z; e.unr = b.w;
+    e.lo[0] = c.x; e.lo[1] = c.y; e.lo[2] = c.z; e.lo[3] = c.w;
+    e.lo[4] = d.x; e.lo[5] = d.y; e.lo[6] = d.z; e.lo[7] = d.w;
+    e.hi[0] = f.x; e.hi[1] = f.y; e.hi[2] = f.z; e.hi[3] = f.w;
+    e.hi[4] = h2.x; e.hi[5] = h2.y; e.hi[6] = h2.z; e.hi[7] = h2.w;
+    const double2 *lv = reinterpret_cast<const double2 *>(p.lossv + env * 4);
+    double2 l0 = lv[0], l1 = lv[1];
+    e.prev_loss = l0.x;
+    e.ep_reward = l0.y;
+    e.ep_start_loss = l1.x;
+    ulonglong2 s = p.rs[env], inc = p.ri[env];
+    uint2 bf = p.rb[env];
+    e.g.s = ((u128)s.x << 64) | s.y;
+    e.g.inc = ((u128)inc.x << 64) | inc.y;
+    e.g.has = bf.x;
+    e.g.u = bf.y;
+    e.mseed = p.det ? p.mseed[env] : 0;
+}
+
+template <class G, int DOM>
+__device__ void store_env(const Params &p, const Team<G> &t, long long env, const EnvRegs<G, DOM> &e,
+                          bool rows_dirty, int dirty_row, bool metrics_dirty, bool rng_dirty) {
+    constexpr int NPL = Dom<DOM>::NPL;
+    if (rows_dirty || dirty_row >= 0) {
+        typename G::Row *rw = rows_of<G, DOM>(p, env);
+#pragma unroll
+        for (int k = 0; k < G::RPL; k++) {
+            int r = t.row(k);
+            if (rows_dirty || r == dirty_row) {
+#pragma unroll
+                for (int q = 0; q < NPL; q++) rw[q * G::ROWS + r] = e.pl[q].r[k];
+                if (rows_dirty) rw[NPL * G::ROWS + r] = e.frz.r[k];
+            }
+        }
+    }
+    if (t.lane != 0) return;
+    Hot hv;
+    hv.geo = (uint32_t)e.h | ((uint32_t)e.w << 8) | ((uint32_t)e.pr << 16) | ((uint32_t)e.pc << 24);
+    hv.pos_idx = e.pos_idx;
+    hv.order_len = e.order_len;
+    hv.changes = e.changes;
+    hv.t = e.t;
+    hv.max_steps = e.max_steps;
+    p.hot[env] = hv;
+    if (metrics_dirty) {
+        int4 *mv = reinterpret_cast<int4 *>(p.mv + env * 24);
+        mv[0] = make_int4(e.val[0], e.val[1], e.val[2], e.val[3]);
+        mv[1] = make_int4(e.val[4], e.val[5], e.val[6], e.unr);
+        mv[2] = make_int4(e.lo[0], e.lo[1], e.lo[2], e.lo[3]);
+        mv[3] = make_int4(e.lo[4], e.lo[5], e.lo[6], e.lo[7]);
+        mv[4] = make_int4(e.hi[0], e.hi[1], e.hi[2], e.hi[3]);
+        mv[5] = make_int4(e.hi[4], e.hi[5], e.hi[6], e.hi[7]);
+    }
+    double2 *lv = reinterpret_cast<double2 *>(p.lossv + env * 4);
+    lv[0] = make_double2(e.prev_loss, e.ep_reward);
+    if (metrics_dirty) lv[1] = make_double2(e.ep_start_loss, 0.0);
+    if (rng_dirty) {
+        p.rs[env] = make_ulonglong2((unsigned long long)(e.g.s >> 64), (unsigned long long)e.g.s);
+        p.rb[env] = make_uint2(e.g.has, e.g.u);
+        if (p.det) p.mseed[env] = e.mseed;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// observation bit image (env.py:186-233)
+// ---------------------------------------------------------------------------
+
+// OR a row of `nbits` (<=128) window bits into the image at bit offset `off`.
+__device__ __forceinline__ void img_or(uint32_t *img, uint32_t off, u128 v) {
+    if (v == 0) return;
+    uint32_t w0 = off >> 5, sh = off & 31;
+    u128 lo = v << sh;
+    uint32_t hi = sh ? (uint32_t)(v >> (128 - sh)) : 0u;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        uint32_t x = (uint32_t)(lo >> (32 * j));
+        if (x) atomicOr(&img[w0 + j], x);
+    }
+    if (hi) atomicOr(&img[w0 + 4], hi);
+}
+
+// Window row bits of one grid row word: column c0+j -> bit j; columns
+// outside the max grid read `fill`.
+__device__ __forceinline__ u128 window_bits(uint64_t gridrow, int c0, int OW, int W, bool fill) {
+    u128 x = (u128)gridrow;
+    u128 win = c0 >= 0 ? (x >> c0) : (x << (-c0));
+    int jlo = c0 < 0 ? -c0 : 0;
+    int jhi = W - c0;
+    if (jhi > OW) jhi = OW;
+    u128 inside = 0;
+    if (jhi > jlo) {
+        u128 upto = jhi >= 128 ? ~(u128)0 : (((u128)1 << jhi) - 1);
+        u128 below = ((u128)1 << jlo) - 1;
+        inside = upto & ~below;
+    }
+    u128 full = OW >= 128 ? ~(u128)0 : (((u128)1 << OW) - 1);
+    win &= inside;
+    if (fill) win |= full & ~inside;
+    return win;
+}
+
+template <class G, int DOM>
+__device__ void render_env(const Params &p, const Team<G> &t, const EnvRegs<G, DOM> &e,
+                           unsigned char *es) {
+    using Row = typename G::Row;
+    constexpr int N = Dom<DOM>::N, NPL = Dom<DOM>::NPL;
+    uint32_t *img = reinterpret_cast<uint32_t *>(es);
+    for (int i = t.lane; i < p.img_words; i += G::TEAM) img[i] = 0;
+    // control planes: (value - (lo+hi)/2) / cap in float64, stored as float32
+    float *ctrl = reinterpret_cast<float *>(es + p.off_ctrl);
+    if (t.lane < p.n_ctrl) {
+        int m = p.ctrl[t.lane];
+        int vm = 0, lm = 0, hm = 0;
+#pragma unroll
+        for (int q = 0; q < 8; q++)
+            if (q == m) {
+                vm = e.val[q];
+                lm = e.lo[q];
+                hm = e.hi[q];
+            }
+        double tgt = __ddiv_rn(__dadd_rn((double)lm, (double)hm), 2.0);
+        double v = __ddiv_rn(__dsub_rn((double)vm, tgt), (double)(e.h * e.w));
+        ctrl[t.lane] = __double2float_rn(v);
+    }
+    t.sync();
+    int r0 = 0, c0 = 0;
+    if (p.rep != REP_WIDE) {
+        r0 = e.pr - p.half;
+        c0 = e.pc - p.half;
+    }
+    const int OH = p.OH, OW = p.OW;
+    const uint32_t plane_bits = (uint32_t)OH * OW;
+    Row wmask = low_mask<Row>(p.W);
+    // rows inside the max grid, emitted by the lane that holds them
+#pragma unroll
+    for (int k = 0; k < G::RPL; k++) {
+        int gr = t.row(k);
+        int i = gr - r0;
+        if (gr < p.H && i >= 0 && i < OH) {
+            Row act = gr < e.h ? low_mask<Row>(e.w) : Row(0);
+            Row any = 0;
+#pragma unroll
+            for (int q = 0; q < NPL; q++) any |= e.pl[q].r[k];
+            uint32_t rowoff = (uint32_t)i * OW;
+            img_or(img, rowoff, window_bits((uint64_t)(act & ~any), c0, OW, p.W, false));
+#pragma unroll
+            for (int q = 0; q < NPL; q++)
+                img_or(img, (q + 1) * plane_bits + rowoff,
+                       window_bits((uint64_t)e.pl[q].r[k], c0, OW, p.W, false));
+            img_or(img, N * plane_bits + rowoff,
+                   window_bits((uint64_t)(~act & wmask), c0, OW, p.W, true));
+            img_or(img, (N + 1) * plane_bits + rowoff,
+                   window_bits((uint64_t)e.frz.r[k], c0, OW, p.W, true));
+        }
+    }
+    // window rows outside the max grid: border and frozen everywhere
+    u128 full = OW >= 128 ? ~(u128)0 : (((u128)1 << OW) - 1);
+    for (int i = t.lane; i < OH; i += G::TEAM) {
+        int gr = r0 + i;
+        if (gr < 0 || gr >= p.H) {
+            img_or(img, N * plane_bits + (uint32_t)i * OW, full);
+            img_or(img, (N + 1) * plane_bits + (uint32_t)i * OW, full);
+        }
+    }
+}
+
+// Phase 2: expand the block's bit images to float32, coalesced 16-byte stores.
+__device__ __forceinline__ float obs_value(const Params &p, const unsigned char *smem, uint32_t e) {
+    uint32_t el = fdiv(p.divPE, e);
+    uint32_t le = e - el * p.PE;
+    const unsigned char *es = smem + (size_t)el * p.env_smem;
+    if (le < p.PB) {
+        const uint32_t *img = reinterpret_cast<const uint32_t *>(es);
+        return ((img[le >> 5] >> (le & 31)) & 1u) ? 1.0f : 0.0f;
+    }
+    const float *ctrl = reinterpret_cast<const float *>(es + p.off_ctrl);
+    return ctrl[fdiv(p.divOO, le - p.PB)];
+}
+
+__device__ void write_obs_block(const Params &p, const unsigned char *smem, long long env0, int E) {
+    long long rem = (long long)p.B - env0;
+    int nenv = rem < E ? (int)rem : E;
+    if (nenv <= 0) return;
+    float *out = p.obs + (size_t)env0 * p.PE;
+    uint32_t total = (uint32_t)nenv * p.PE;
+    uint32_t nvec = total >> 2;
+    float4 *out4 = reinterpret_cast<float4 *>(out);
+    for (uint32_t q = threadIdx.x; q < nvec; q += blockDim.x) {
+        uint32_t e = q << 2;
+        uint32_t el = fdiv(p.divPE, e);
+        uint32_t le = e - el * p.PE;
+        float4 v;
+        if (le + 3 < p.PB) {
+            const uint32_t *img = reinterpret_cast<const uint32_t *>(smem + (size_t)el * p.env_smem);
+            uint32_t wi = le >> 5, sh = le & 31;
+            uint64_t two = (uint64_t)img[wi] | ((uint64_t)img[wi + 1] << 32);
+            uint32_t bits = (uint32_t)(two >> sh);
+            v.x = (bits & 1u) ? 1.0f : 0.0f;
+            v.y = (bits & 2u) ? 1.0f : 0.0f;
+            v.z = (bits & 4u) ? 1.0f : 0.0f;
+            v.w = (bits & 8u) ? 1.0f : 0.0f;
+        } else {
+            v.x = obs_value(p, smem, e);
+            v.y = obs_value(p, smem, e + 1);
+            v.z = obs_value(p, smem, e + 2);
+            v.w = obs_value(p, smem, e + 3);
+        }
+        __stcs(out4 + q, v);
+    }
+    for (uint32_t e = (nvec << 2) + threadIdx.x; e < total; e += blockDim.x)
+        out[e] = obs_value(p, smem, e);
+}
+
+// ---------------------------------------------------------------------------
+// the kernel
+// ---------------------------------------------------------------------------
+
+template <class G, int DOM>
+__global__ void __launch_bounds__(256) env_kernel(const Params p, int mode) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    using Row = typename G::Row;
+    constexpr int N = Dom<DOM>::N, NPL = Dom<DOM>::NPL;
+    Team<G> t;
+    const int E = blockDim.x / G::TEAM;
+    const int ti = threadIdx.x / G::TEAM;
+    const long long env0 = (long long)blockIdx.x * E;
+    const long long env = env0 + ti;
+    unsigned char *es = smem + (size_t)ti * p.env_smem;
+    uint16_t *uf = reinterpret_cast<uint16_t *>(es);  // aliases the bit image (phases differ)
+
+    if (env < p.B) {
+        EnvRegs<G, DOM> e;
+        load_env<G, DOM>(p, t, env, e);
+        bool rows_dirty = false, metrics_dirty = false, rng_dirty = false;
+        int dirty_row = -1;
+        if (mode == MODE_STEP) {
+            long long a = p.actions[env];
+            bool ok = a >= 0 && a < p.n_actions;
+            if (!ok && t.lane == 0) atomicOr(p.err, (unsigned)FLAG_BAD_ACTION);
+            int r = e.pr, c = e.pc, tile = -1;
+            if (p.rep == REP_NARROW) {
+                if (ok && a != 0) tile = (int)a - 1;
+            } else if (p.rep == REP_TURTLE) {
+                if (ok && a < 4) {  // moves, clamped to the episode rectangle
+                    if (a == 0) r = r > 0 ? r - 1 : 0;
+                    else if (a == 1) r = r < e.h - 1 ? r + 1 : e.h - 1;
+                    else if (a == 2) c = c > 0 ? c - 1 : 0;
+                    else c = c < e.w - 1 ? c + 1 : e.w - 1;
+                    e.pr = r;
+                    e.pc = c;
+                } else if (ok) {
+                    tile = (int)a - 4;
+                }
+            } else {  // wide
+                if (ok) {
+                    long long cell = a / N;
+                    tile = (int)(a - cell * N);
+                    r = (int)(cell / p.W);
+                    c = (int)(cell - (long long)r * p.W);
+                }
+            }
+            // tile currently at (r, c) and editability, from the owning lane
+            int cur = 0, editable = 0;
+            int src = r / G::RPL;
+            if (t.lane == src) {
+#pragma unroll
+                for (int k = 0; k < G::RPL; k++)
+                    if (t.row(k) == r) {
+                        Row bit = Row(1) << c;
+                        bool act = r < e.h && c < e.w;
+                        cur = act ? 0 : N;
+#pragma unroll
+                        for (int q = 0; q < NPL; q++)
+                            if (e.pl[q].r[k] & bit) cur = q + 1;
+                        editable = act && !(e.frz.r[k] & bit);
+                    }
+            }
+            cur = t.from(cur, src);
+            editable = t.from(editable, src);
+            // narrow: the scan cell is always editable (env.py:366-367)
+            bool wrote = tile >= 0 && tile != cur && (p.rep == REP_NARROW || editable);
+            double reward = 0.0;
+            if (wrote) {
+                if (t.lane == src) {
+#pragma unroll
+                    for (int k = 0; k < G::RPL; k++)
+                        if (t.row(k) == r) {
+                            Row bit = Row(1) << c;
+#pragma unroll
+                            for (int q = 0; q < NPL; q++) {
+                                e.pl[q].r[k] &= ~bit;
+                                if (q == tile - 1) e.pl[q].r[k] |= bit;
+                            }
+                        }
+                }
+                dirty_row = r;
+                e.changes += 1;
+                double before = e.prev_loss;
+                recompute<G, DOM>(p, t, e, uf, false);
+                reward = __dsub_rn(before, e.prev_loss);
+                metrics_dirty = true;
+                rng_dirty = true;
+            }
+            e.ep_reward = __dadd_rn(e.ep_reward, reward);
+            if (p.rep == REP_NARROW) {  // pos_idx = (pos_idx + 1) % order_len
+                int nidx = e.pos_idx + 1;
+                int nxt;
+                Bd<G> ed = andnot(rect_board(t, e.h, e.w), e.frz);
+                if (nidx >= e.order_len) {
+                    nidx = 0;
+                    nxt = serp_first_from(t, ed, 0);
+                } else {
+                    nxt = serp_next(t, ed, e.pr, e.pc);
+                }
+                e.pos_idx = nidx;
+                e.pr = nxt >> 6;
+                e.pc = nxt & 63;
+            }
+            e.t += 1;
+            bool done = e.t >= e.max_steps;
+            if (p.budget > 0) done |= e.changes >= p.budget;
+            if (t.lane == 0) {
+                p.reward[env] = reward;
+                p.done[env] = done;
+                if (p.terminal) p.terminal[env] = done;
+                if (p.ep_rew) p.ep_rew[env] = done ? e.ep_reward : 0.0;
+                if (p.ep_len) p.ep_len[env] = done ? e.t : 0;
+                if (p.ep_start) p.ep_start[env] = done ? e.ep_start_loss : 0.0;
+                if (p.fin_loss) p.fin_loss[env] = done ? e.prev_loss : 0.0;
+                if (done && p.stats) {
+                    atomicAdd(p.stats + 0, 1.0);
+                    atomicAdd(p.stats + 1, e.ep_reward);
+                    atomicAdd(p.stats + 2, (double)e.t);
+                    atomicAdd(p.stats + 3, e.ep_start_loss);
+                    atomicAdd(p.stats + 4, e.prev_loss);
+                }
+            }
+            if (done) {
+                reset_env<G, DOM>(p, t, e, uf);
+                rows_dirty = metrics_dirty = rng_dirty = true;
+            }
+        } else if (mode == MODE_RESET) {
+            if (!p.reset_mask || p.reset_mask[env]) {
+                reset_env<G, DOM>(p, t, e, uf);
+                rows_dirty = metrics_dirty = rng_dirty = true;
+            }
+        }
+        if (mode != MODE_OBSERVE) store_env<G, DOM>(p, t, env, e, rows_dirty, dirty_row, metrics_dirty, rng_dirty);
+        if (p.obs) {
+            t.sync();  // union-find scratch is reused for the image
+            render_env<G, DOM>(p, t, e, es);
+        }
+    }
+    if (p.obs) {
+        __syncthreads();
+        write_obs_block(p, smem, env0, E);
+    }
+}
+
+}  // namespace lg

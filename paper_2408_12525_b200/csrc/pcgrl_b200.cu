@@ -1,0 +1,755 @@
+// pcgrl_b200.cu -- C ABI (include/pcgrl_b200.h) over the sm_100a env kernels.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <mutex>
+#include <new>
+
+#include "../../include/pcgrl_b200.h"
+#include "env_kernels.cuh"
+
+using namespace lg;
+
+static thread_local char g_err[512];
+static void set_err(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+}
+extern "C" const char *lg_last_error(void) { return g_err; }
+extern "C" const char *lg_version(void) { return "pcgrl_b200 0.1 sm_100a"; }
+
+#define CU(call)                                                           \
+    do {                                                                   \
+        cudaError_t _e = (call);                                           \
+        if (_e != cudaSuccess) {                                           \
+            set_err("CUDA error: %s (line %d)", cudaGetErrorString(_e), __LINE__); \
+            return LG_ECUDA;                                               \
+        }                                                                  \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// auxiliary kernels
+// ---------------------------------------------------------------------------
+
+__global__ void seed_kernel(long long B, unsigned long long seed, long long offset, ulonglong2 *rs,
+                            ulonglong2 *ri, uint2 *rb) {
+    long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    Pcg g;
+    seedseq_pcg(seed, true, (uint64_t)(offset + b), g);
+    rs[b] = make_ulonglong2((unsigned long long)(g.s >> 64), (unsigned long long)g.s);
+    ri[b] = make_ulonglong2((unsigned long long)(g.inc >> 64), (unsigned long long)g.inc);
+    rb[b] = make_uint2(0, 0);
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ULL;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+    return x ^ (x >> 31);
+}
+
+__global__ void random_actions_kernel(long long B, long long goffset, unsigned long long seed,
+                                      long long n_actions, long long *out) {
+    long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    uint64_t x = splitmix64(seed * 0xD1B54A32D192ED03ULL ^ splitmix64((uint64_t)(goffset + b)));
+    out[b] = (long long)(((unsigned __int128)x * (unsigned long long)n_actions) >> 64);
+}
+
+// state_dict export (env.py:535-559), team per env
+template <class G, int DOM>
+__global__ void __launch_bounds__(256) export_kernel(const Params p, lg_state dst) {
+    using Row = typename G::Row;
+    constexpr int N = Dom<DOM>::N, NPL = Dom<DOM>::NPL, M = Dom<DOM>::M;
+    Team<G> t;
+    const long long env = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / G::TEAM;
+    if (env >= p.B) return;
+    EnvRegs<G, DOM> e;
+    load_env<G, DOM>(p, t, env, e);
+    const int H = p.H, W = p.W, HW = H * W;
+    Bd<G> act = rect_board(t, e.h, e.w);
+    Bd<G> ed = andnot(act, e.frz);
+    int cnt = 0;
+#pragma unroll
+    for (int k = 0; k < G::RPL; k++) {
+        int r = t.row(k);
+        if (r >= H) continue;
+        cnt += popc(ed.r[k]);
+        for (int c = 0; c < W; c++) {
+            Row bit = Row(1) << c;
+            bool a = (act.r[k] & bit) != 0;
+            int tile = a ? 0 : N;
+#pragma unroll
+            for (int q = 0; q < NPL; q++)
+                if (e.pl[q].r[k] & bit) tile = q + 1;
+            size_t o = ((size_t)env * H + r) * W + c;
+            dst.tiles[o] = (uint8_t)tile;
+            dst.active[o] = a;
+            dst.frozen[o] = (e.frz.r[k] & bit) != 0;
+        }
+    }
+    int inc = t.scan(cnt);
+    int off = inc - cnt;
+    int32_t *ord = dst.order + (size_t)env * HW;
+#pragma unroll
+    for (int k = 0; k < G::RPL; k++) {
+        int r = t.row(k);
+        if (r >= H) continue;
+        Row x = ed.r[k];
+        if (r & 1) {
+            while (x) {
+                int c = msb(x);
+                x &= ~(Row(1) << c);
+                ord[off++] = r * W + c;
+            }
+        } else {
+            while (x) {
+                int c = ctz(x);
+                x &= x - 1;
+                ord[off++] = r * W + c;
+            }
+        }
+    }
+    int total = t.from(inc, G::TEAM - 1);
+    for (int i = total + t.lane; i < HW; i += G::TEAM) ord[i] = -1;
+    if (t.lane != 0) return;
+    dst.shape_hw[2 * env] = e.h;
+    dst.shape_hw[2 * env + 1] = e.w;
+    dst.order_len[env] = e.order_len;
+    dst.pos_idx[env] = e.pos_idx;
+    dst.pos[2 * env] = e.pr;
+    dst.pos[2 * env + 1] = e.pc;
+    dst.t[env] = e.t;
+    dst.changes[env] = e.changes;
+    dst.max_steps[env] = e.max_steps;
+    for (int m = 0; m < M; m++) {
+        dst.lo[(size_t)m * p.B + env] = e.lo[m];
+        dst.hi[(size_t)m * p.B + env] = e.hi[m];
+        dst.values[(size_t)m * p.B + env] = e.val[m];
+        dst.unreach[(size_t)m * p.B + env] = (e.unr >> m) & 1;
+    }
+    dst.prev_loss[env] = e.prev_loss;
+    dst.ep_reward[env] = e.ep_reward;
+    dst.ep_start_loss[env] = e.ep_start_loss;
+    dst.metric_seeds[env] = p.det ? e.mseed : p.mseed[env];
+    uint64_t *rg = dst.rng + 6 * env;
+    rg[0] = (uint64_t)(e.g.s >> 64);
+    rg[1] = (uint64_t)e.g.s;
+    rg[2] = (uint64_t)(e.g.inc >> 64);
+    rg[3] = (uint64_t)e.g.inc;
+    rg[4] = e.g.has;
+    rg[5] = e.g.u;
+}
+
+// load_state_dict (env.py:561-585), team per env. `pos` must hold the
+// current cell (the Python mirror derives it from order[pos_idx] for narrow).
+template <class G, int DOM>
+__global__ void __launch_bounds__(256) import_kernel(const Params p, lg_state src) {
+    using Row = typename G::Row;
+    constexpr int NPL = Dom<DOM>::NPL, M = Dom<DOM>::M;
+    Team<G> t;
+    const long long env = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / G::TEAM;
+    if (env >= p.B) return;
+    const int H = p.H, W = p.W;
+    typename G::Row *rw = rows_of<G, DOM>(p, env);
+#pragma unroll
+    for (int k = 0; k < G::RPL; k++) {
+        int r = t.row(k);
+        Row pl[NPL > 0 ? NPL : 1], fr = 0;
+        for (int q = 0; q < NPL; q++) pl[q] = 0;
+        if (r < H) {
+            for (int c = 0; c < W; c++) {
+                size_t o = ((size_t)env * H + r) * W + c;
+                int tile = src.tiles[o];
+                bool a = src.active[o] != 0;
+                if (a && tile >= 1 && tile <= NPL) pl[tile - 1] |= Row(1) << c;
+                if (src.frozen[o]) fr |= Row(1) << c;
+            }
+        }
+        for (int q = 0; q < NPL; q++) rw[q * G::ROWS + r] = pl[q];
+        rw[NPL * G::ROWS + r] = fr;
+    }
+    if (t.lane != 0) return;
+    Hot hv;
+    uint32_t h = (uint32_t)src.shape_hw[2 * env], w = (uint32_t)src.shape_hw[2 * env + 1];
+    uint32_t pr = (uint32_t)src.pos[2 * env], pc = (uint32_t)src.pos[2 * env + 1];
+    hv.geo = h | (w << 8) | (pr << 16) | (pc << 24);
+    hv.pos_idx = (int32_t)src.pos_idx[env];
+    hv.order_len = (int32_t)src.order_len[env];
+    hv.changes = (int32_t)src.changes[env];
+    hv.t = src.t[env];
+    hv.max_steps = src.max_steps[env];
+    p.hot[env] = hv;
+    int *mv = p.mv + env * 24;
+    int unr = 0;
+    for (int m = 0; m < 8; m++) {
+        bool in = m < M;
+        mv[m] = in ? (int)src.values[(size_t)m * p.B + env] : 0;
+        mv[8 + m] = in ? (int)src.lo[(size_t)m * p.B + env] : 0;
+        mv[16 + m] = in ? (int)src.hi[(size_t)m * p.B + env] : 0;
+        if (in && src.unreach[(size_t)m * p.B + env]) unr |= 1 << m;
+    }
+    mv[7] = unr;
+    double *lv = p.lossv + env * 4;
+    lv[0] = src.prev_loss[env];
+    lv[1] = src.ep_reward[env];
+    lv[2] = src.ep_start_loss[env];
+    lv[3] = 0.0;
+    p.mseed[env] = src.metric_seeds[env];
+    const uint64_t *rg = src.rng + 6 * env;
+    p.rs[env] = make_ulonglong2(rg[0], rg[1]);
+    p.ri[env] = make_ulonglong2(rg[2], rg[3]);
+    p.rb[env] = make_uint2((unsigned)rg[4], (unsigned)rg[5]);
+}
+
+// compute_metrics_batch on raw stacks (problems.py:105-129), team per grid.
+template <class G, int DOM>
+__global__ void __launch_bounds__(256) metrics_kernel(long long n, int H, int W, const uint8_t *tiles,
+                                                      const uint8_t *active, uint64_t *rng,
+                                                      int64_t *values, uint8_t *unreach) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    using Row = typename G::Row;
+    constexpr int NPL = Dom<DOM>::NPL, M = Dom<DOM>::M;
+    Team<G> t;
+    const int ti = threadIdx.x / G::TEAM;
+    const long long b = (long long)blockIdx.x * (blockDim.x / G::TEAM) + ti;
+    if (b >= n) return;
+    uint16_t *uf = reinterpret_cast<uint16_t *>(smem + (size_t)ti * G::ROWS * G::RUNS * 2);
+    Bd<G> pl[NPL], act;
+#pragma unroll
+    for (int k = 0; k < G::RPL; k++) {
+        int r = t.row(k);
+        Row a = 0;
+        Row q[NPL];
+        for (int j = 0; j < NPL; j++) q[j] = 0;
+        if (r < H) {
+            for (int c = 0; c < W; c++) {
+                size_t o = ((size_t)b * H + r) * W + c;
+                if (active[o]) {
+                    a |= Row(1) << c;
+                    int tile = tiles[o];
+                    if (tile >= 1 && tile <= NPL) q[tile - 1] |= Row(1) << c;
+                }
+            }
+        }
+        act.r[k] = a;
+        for (int j = 0; j < NPL; j++) pl[j].r[k] = q[j];
+    }
+    Pcg g;
+    g.s = g.inc = 0;
+    g.has = g.u = 0;
+    if (rng) {
+        const uint64_t *rg = rng + 6 * b;
+        g.s = ((u128)rg[0] << 64) | rg[1];
+        g.inc = ((u128)rg[2] << 64) | rg[3];
+        g.has = (uint32_t)rg[4];
+        g.u = (uint32_t)rg[5];
+    }
+    int val[8] = {0, 0, 0, 0, 0, 0, 0, 0}, unr = 0;
+    compute_metrics<G, DOM>(t, pl, act, low_mask<Row>(W), g, uf, val, unr);
+    if (t.lane != 0) return;
+    for (int m = 0; m < M; m++) {
+        values[(size_t)m * n + b] = val[m];
+        unreach[(size_t)m * n + b] = (unr >> m) & 1;
+    }
+    if (rng) {
+        uint64_t *rg = rng + 6 * b;
+        rg[0] = (uint64_t)(g.s >> 64);
+        rg[1] = (uint64_t)g.s;
+        rg[4] = g.has;
+        rg[5] = g.u;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+
+struct lg_env {
+    lg_config cfg;
+    int device;
+    long long B, offset;
+    unsigned long long seed;
+    int geo;  // 16, 32, 64
+    int team, threads, E;
+    int N, M, NPL, C, OH, OW;
+    long long n_actions;
+    size_t row_bytes, rows_per_env;
+    Params base;
+    size_t smem;
+    // e2e staging (lazy)
+    long long *d_act = nullptr;
+    float *d_obs = nullptr;
+    double *d_rew = nullptr;
+    unsigned char *d_done = nullptr, *d_term = nullptr;
+    double *d_er = nullptr, *d_es = nullptr, *d_fl = nullptr;
+    long long *d_el = nullptr;
+};
+
+static void fastdiv_init(FastDiv &f, uint32_t d) {
+    f.d = d;
+    if (d <= 1) {
+        f.mul = 0;
+        f.shr = 0;
+        return;
+    }
+    uint32_t l = 0;
+    while ((1ull << l) < d) l++;  // ceil(log2 d)
+    uint32_t pw = 31 + l;
+    f.mul = (uint32_t)(((1ull << pw) + d - 1) / d);
+    f.shr = pw - 32;
+}
+
+static int dom_n(int d) { return d == 0 ? 2 : d == 1 ? 4 : 6; }
+static int dom_m(int d) { return d == 0 ? 2 : d == 1 ? 4 : 7; }
+
+template <class G, int DOM>
+static int launch_env_t(lg_env *e, const Params &p, int mode, cudaStream_t s) {
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [] {
+        attr_err = cudaFuncSetAttribute(env_kernel<G, DOM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        200 * 1024);
+    });
+    CU(attr_err);
+    int E = e->threads / G::TEAM;
+    long long grid = (e->B + E - 1) / E;
+    env_kernel<G, DOM><<<(unsigned)grid, e->threads, e->smem, s>>>(p, mode);
+    CU(cudaGetLastError());
+    return LG_OK;
+}
+
+static int launch_env(lg_env *e, const Params &p, int mode, cudaStream_t s) {
+    int d = e->cfg.domain;
+    switch (e->geo) {
+    case 16:
+        return d == 0 ? launch_env_t<G16, 0>(e, p, mode, s)
+               : d == 1 ? launch_env_t<G16, 1>(e, p, mode, s)
+                        : launch_env_t<G16, 2>(e, p, mode, s);
+    case 32:
+        return d == 0 ? launch_env_t<G32, 0>(e, p, mode, s)
+               : d == 1 ? launch_env_t<G32, 1>(e, p, mode, s)
+                        : launch_env_t<G32, 2>(e, p, mode, s);
+    default:
+        return d == 0 ? launch_env_t<G64, 0>(e, p, mode, s)
+               : d == 1 ? launch_env_t<G64, 1>(e, p, mode, s)
+                        : launch_env_t<G64, 2>(e, p, mode, s);
+    }
+}
+
+template <class G, int DOM>
+static int launch_state_t(lg_env *e, const Params &p, const lg_state &st, bool exp, cudaStream_t s) {
+    long long threads = e->B * G::TEAM;
+    unsigned grid = (unsigned)((threads + 255) / 256);
+    if (exp) export_kernel<G, DOM><<<grid, 256, 0, s>>>(p, st);
+    else import_kernel<G, DOM><<<grid, 256, 0, s>>>(p, st);
+    CU(cudaGetLastError());
+    return LG_OK;
+}
+
+static int launch_state(lg_env *e, const lg_state &st, bool exp, cudaStream_t s) {
+    int d = e->cfg.domain;
+    const Params &p = e->base;
+    switch (e->geo) {
+    case 16:
+        return d == 0 ? launch_state_t<G16, 0>(e, p, st, exp, s)
+               : d == 1 ? launch_state_t<G16, 1>(e, p, st, exp, s)
+                        : launch_state_t<G16, 2>(e, p, st, exp, s);
+    case 32:
+        return d == 0 ? launch_state_t<G32, 0>(e, p, st, exp, s)
+               : d == 1 ? launch_state_t<G32, 1>(e, p, st, exp, s)
+                        : launch_state_t<G32, 2>(e, p, st, exp, s);
+    default:
+        return d == 0 ? launch_state_t<G64, 0>(e, p, st, exp, s)
+               : d == 1 ? launch_state_t<G64, 1>(e, p, st, exp, s)
+                        : launch_state_t<G64, 2>(e, p, st, exp, s);
+    }
+}
+
+static int pick_geo(int H, int W) {
+    if (W <= 32 && H <= 16) return 16;
+    if (W <= 32 && H <= 32) return 32;
+    return 64;
+}
+
+static int validate_cfg(const lg_config *c) {
+    if (!c) {
+        set_err("null config");
+        return LG_EINVAL;
+    }
+    if (c->domain < 0 || c->domain > 2) {
+        set_err("unknown domain id %d", c->domain);
+        return LG_EINVAL;
+    }
+    if (c->representation < 0 || c->representation > 2) {
+        set_err("unknown representation id %d", c->representation);
+        return LG_EINVAL;
+    }
+    if (c->max_h < 3 || c->max_w < 3 || c->max_h > 64 || c->max_w > 64) {
+        set_err("max shape must be within 3..64 per side on device");
+        return LG_EINVAL;
+    }
+    if (c->representation != LG_WIDE && (c->obs_size < 3 || c->obs_size > 128)) {
+        set_err("obs_size must be within 3..128 on device");
+        return LG_EINVAL;
+    }
+    if (c->n_pins < 0 || c->n_pins > 16 || c->n_ctrl < 0 || c->n_ctrl > 7) {
+        set_err("too many pinpoints or controls");
+        return LG_EINVAL;
+    }
+    return LG_OK;
+}
+
+extern "C" int lg_create(const lg_config *cfg, int64_t n_envs, int64_t global_offset, uint64_t seed,
+                         int device, lg_env **out) {
+    if (validate_cfg(cfg)) return LG_EINVAL;
+    if (n_envs < 1) {
+        set_err("need at least one environment");
+        return LG_EINVAL;
+    }
+    if (n_envs > (1LL << 31) - 1) {
+        set_err("at most 2^31-1 environments per device");
+        return LG_EINVAL;
+    }
+    CU(cudaSetDevice(device));
+    lg_env *e = new (std::nothrow) lg_env();
+    if (!e) {
+        set_err("out of host memory");
+        return LG_ECUDA;
+    }
+    e->cfg = *cfg;
+    e->device = device;
+    e->B = n_envs;
+    e->offset = global_offset;
+    e->seed = seed;
+    const int H = cfg->max_h, W = cfg->max_w;
+    e->geo = pick_geo(H, W);
+    e->team = e->geo == 16 ? 16 : 32;
+    e->threads = 256;
+    e->E = e->threads / e->team;
+    e->N = dom_n(cfg->domain);
+    e->M = dom_m(cfg->domain);
+    e->NPL = e->N - 1;
+    e->C = e->N + 2 + cfg->n_ctrl;
+    if (cfg->representation == LG_WIDE) {
+        e->OH = H;
+        e->OW = W;
+    } else {
+        e->OH = e->OW = cfg->obs_size;
+    }
+    e->n_actions = cfg->representation == LG_TURTLE ? 4 + e->N
+                   : cfg->representation == LG_WIDE ? (long long)H * W * e->N
+                                                    : e->N + 1;
+    int rows = e->geo == 16 ? 16 : e->geo == 32 ? 32 : 64;
+    e->row_bytes = e->geo == 64 ? 8 : 4;
+    e->rows_per_env = (size_t)(e->NPL + 1) * rows;
+    int runs = e->geo == 64 ? 32 : 16;
+    size_t uf_bytes = (size_t)rows * runs * 2;
+
+    Params &p = e->base;
+    memset(&p, 0, sizeof p);
+    p.B = (int)n_envs;
+    p.H = H;
+    p.W = W;
+    p.rep = cfg->representation;
+    p.OH = e->OH;
+    p.OW = e->OW;
+    p.half = (cfg->obs_size - 1) / 2;
+    p.randomize = cfg->randomize_shape;
+    p.weighted = cfg->init_weighted;
+    p.n_pins = cfg->n_pins;
+    p.n_ctrl = cfg->n_ctrl;
+    p.det = cfg->det_metrics;
+    p.max_steps = cfg->max_steps;
+    p.budget = cfg->change_budget;
+    p.n_actions = e->n_actions;
+    p.goffset = global_offset;
+    for (int i = 0; i < 16; i++) p.pins[i] = cfg->pins[i];
+    for (int i = 0; i < 8; i++) {
+        p.ctrl[i] = cfg->ctrl[i];
+        p.cdf[i] = cfg->init_cdf[i];
+        p.w[i] = cfg->weights[i];
+    }
+    p.OO = (uint32_t)(e->OH * e->OW);
+    p.PB = (uint32_t)(e->N + 2) * p.OO;
+    p.PE = (uint32_t)e->C * p.OO;
+    fastdiv_init(p.divPE, p.PE);
+    fastdiv_init(p.divOO, p.OO);
+    p.img_words = (int)((p.PB + 31) / 32 + 1);
+    size_t scratch = uf_bytes > (size_t)p.img_words * 4 ? uf_bytes : (size_t)p.img_words * 4;
+    scratch = (scratch + 15) & ~(size_t)15;
+    p.off_ctrl = (int)scratch;
+    p.env_smem = (int)(scratch + 32);
+    e->smem = (size_t)e->E * p.env_smem;
+    if (e->smem > 200 * 1024) {
+        set_err("observation window too large for shared memory staging");
+        delete e;
+        return LG_EINVAL;
+    }
+
+    size_t B = (size_t)n_envs;
+    cudaError_t err = cudaSuccess;
+    auto alloc = [&](void **ptr, size_t bytes) {
+        if (err == cudaSuccess) err = cudaMalloc(ptr, bytes);
+        if (err == cudaSuccess) err = cudaMemset(*ptr, 0, bytes);
+    };
+    alloc(&p.rows, B * e->rows_per_env * e->row_bytes);
+    alloc((void **)&p.hot, B * sizeof(Hot));
+    alloc((void **)&p.mv, B * 24 * sizeof(int));
+    alloc((void **)&p.lossv, B * 4 * sizeof(double));
+    alloc((void **)&p.rs, B * sizeof(ulonglong2));
+    alloc((void **)&p.ri, B * sizeof(ulonglong2));
+    alloc((void **)&p.rb, B * sizeof(uint2));
+    alloc((void **)&p.mseed, B * sizeof(long long));
+    alloc((void **)&p.err, sizeof(unsigned));
+    if (err != cudaSuccess) {
+        set_err("CUDA allocation failed: %s", cudaGetErrorString(err));
+        lg_destroy(e);
+        return LG_ECUDA;
+    }
+    seed_kernel<<<(unsigned)((B + 255) / 256), 256>>>((long long)B, seed, global_offset, p.rs, p.ri, p.rb);
+    err = cudaGetLastError();
+    if (err == cudaSuccess) err = cudaDeviceSynchronize();
+    if (err != cudaSuccess) {
+        set_err("seeding failed: %s", cudaGetErrorString(err));
+        lg_destroy(e);
+        return LG_ECUDA;
+    }
+    *out = e;
+    return LG_OK;
+}
+
+extern "C" int lg_destroy(lg_env *e) {
+    if (!e) return LG_OK;
+    cudaSetDevice(e->device);
+    Params &p = e->base;
+    void *ptrs[] = {p.rows, p.hot, p.mv, p.lossv, p.rs, p.ri, p.rb, p.mseed, p.err,
+                    e->d_act, e->d_obs, e->d_rew, e->d_done, e->d_term, e->d_er, e->d_es, e->d_fl, e->d_el};
+    for (void *q : ptrs)
+        if (q) cudaFree(q);
+    delete e;
+    return LG_OK;
+}
+
+extern "C" int lg_describe(const lg_env *e, lg_desc *out) {
+    if (!e || !out) {
+        set_err("null argument");
+        return LG_EINVAL;
+    }
+    out->n_envs = e->B;
+    out->n_actions = (int32_t)e->n_actions;
+    out->n_metrics = e->M;
+    out->obs_c = e->C;
+    out->obs_h = e->OH;
+    out->obs_w = e->OW;
+    out->team = e->team;
+    out->obs_bytes_per_env = (int64_t)e->C * e->OH * e->OW * 4;
+    out->state_bytes_per_env =
+        (int64_t)(e->rows_per_env * e->row_bytes + sizeof(Hot) + 24 * 4 + 32 + 16 + 16 + 8 + 8);
+    return LG_OK;
+}
+
+static int check_obs_ptr(const float *obs) {
+    if (obs && ((uintptr_t)obs & 15)) {
+        set_err("observation buffer must be 16-byte aligned");
+        return LG_EINVAL;
+    }
+    return LG_OK;
+}
+
+static int run_mode(lg_env *e, int mode, const long long *actions, float *obs, double *reward,
+                    uint8_t *done, const lg_info *info, double *stats, const uint8_t *mask, void *stream) {
+    if (!e) {
+        set_err("null env");
+        return LG_EINVAL;
+    }
+    if (check_obs_ptr(obs)) return LG_EINVAL;
+    if (mode == MODE_STEP && (!actions || !reward || !done)) {
+        set_err("step needs actions, reward and done buffers");
+        return LG_EINVAL;
+    }
+    CU(cudaSetDevice(e->device));
+    Params p = e->base;
+    p.actions = actions;
+    p.obs = obs;
+    p.reward = reward;
+    p.done = done;
+    if (info) {
+        p.terminal = info->terminal;
+        p.ep_rew = info->episode_reward;
+        p.ep_len = (long long *)info->episode_length;
+        p.ep_start = info->episode_start_loss;
+        p.fin_loss = info->final_loss;
+    }
+    p.stats = stats;
+    p.reset_mask = mask;
+    return launch_env(e, p, mode, (cudaStream_t)stream);
+}
+
+extern "C" int lg_reset(lg_env *e, float *obs, void *stream) {
+    return run_mode(e, MODE_RESET, nullptr, obs, nullptr, nullptr, nullptr, nullptr, nullptr, stream);
+}
+extern "C" int lg_reset_masked(lg_env *e, const uint8_t *mask, float *obs, void *stream) {
+    return run_mode(e, MODE_RESET, nullptr, obs, nullptr, nullptr, nullptr, nullptr, mask, stream);
+}
+extern "C" int lg_observe(lg_env *e, float *obs, void *stream) {
+    if (!obs) {
+        set_err("observe needs an output buffer");
+        return LG_EINVAL;
+    }
+    return run_mode(e, MODE_OBSERVE, nullptr, obs, nullptr, nullptr, nullptr, nullptr, nullptr, stream);
+}
+extern "C" int lg_step(lg_env *e, const int64_t *actions, float *obs, double *reward, uint8_t *done,
+                       const lg_info *info, double *stats, void *stream) {
+    return run_mode(e, MODE_STEP, (const long long *)actions, obs, reward, done, info, stats, nullptr,
+                    stream);
+}
+
+extern "C" int lg_step_host(lg_env *e, const int64_t *actions_host, float *obs_host, double *reward_host,
+                            uint8_t *done_host, const lg_info *info_host, void *stream) {
+    if (!e || !actions_host || !reward_host || !done_host) {
+        set_err("step_host needs actions, reward and done buffers");
+        return LG_EINVAL;
+    }
+    CU(cudaSetDevice(e->device));
+    size_t B = (size_t)e->B;
+    size_t obs_bytes = B * (size_t)e->C * e->OH * e->OW * sizeof(float);
+    if (!e->d_act) {
+        CU(cudaMalloc((void **)&e->d_act, B * 8));
+        CU(cudaMalloc((void **)&e->d_rew, B * 8));
+        CU(cudaMalloc((void **)&e->d_done, B));
+        CU(cudaMalloc((void **)&e->d_term, B));
+        CU(cudaMalloc((void **)&e->d_er, B * 8));
+        CU(cudaMalloc((void **)&e->d_es, B * 8));
+        CU(cudaMalloc((void **)&e->d_fl, B * 8));
+        CU(cudaMalloc((void **)&e->d_el, B * 8));
+    }
+    if (obs_host && !e->d_obs) CU(cudaMalloc((void **)&e->d_obs, obs_bytes));
+    cudaStream_t s = (cudaStream_t)stream;
+    CU(cudaMemcpyAsync(e->d_act, actions_host, B * 8, cudaMemcpyHostToDevice, s));
+    lg_info di = {e->d_term, e->d_er, (int64_t *)e->d_el, e->d_es, e->d_fl};
+    int rc = lg_step(e, (const int64_t *)e->d_act, obs_host ? e->d_obs : nullptr, e->d_rew, e->d_done,
+                     info_host ? &di : nullptr, nullptr, stream);
+    if (rc) return rc;
+    if (obs_host) CU(cudaMemcpyAsync(obs_host, e->d_obs, obs_bytes, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(reward_host, e->d_rew, B * 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(done_host, e->d_done, B, cudaMemcpyDeviceToHost, s));
+    if (info_host) {
+        if (info_host->terminal) CU(cudaMemcpyAsync(info_host->terminal, e->d_term, B, cudaMemcpyDeviceToHost, s));
+        if (info_host->episode_reward)
+            CU(cudaMemcpyAsync(info_host->episode_reward, e->d_er, B * 8, cudaMemcpyDeviceToHost, s));
+        if (info_host->episode_length)
+            CU(cudaMemcpyAsync(info_host->episode_length, e->d_el, B * 8, cudaMemcpyDeviceToHost, s));
+        if (info_host->episode_start_loss)
+            CU(cudaMemcpyAsync(info_host->episode_start_loss, e->d_es, B * 8, cudaMemcpyDeviceToHost, s));
+        if (info_host->final_loss)
+            CU(cudaMemcpyAsync(info_host->final_loss, e->d_fl, B * 8, cudaMemcpyDeviceToHost, s));
+    }
+    CU(cudaStreamSynchronize(s));
+    return LG_OK;
+}
+
+extern "C" int lg_export_state(lg_env *e, const lg_state *dst, void *stream) {
+    if (!e || !dst) {
+        set_err("null argument");
+        return LG_EINVAL;
+    }
+    CU(cudaSetDevice(e->device));
+    return launch_state(e, *dst, true, (cudaStream_t)stream);
+}
+
+extern "C" int lg_import_state(lg_env *e, const lg_state *src, void *stream) {
+    if (!e || !src) {
+        set_err("null argument");
+        return LG_EINVAL;
+    }
+    CU(cudaSetDevice(e->device));
+    return launch_state(e, *src, false, (cudaStream_t)stream);
+}
+
+extern "C" int lg_errors(lg_env *e, uint32_t *flags, void *stream) {
+    if (!e || !flags) {
+        set_err("null argument");
+        return LG_EINVAL;
+    }
+    CU(cudaSetDevice(e->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    CU(cudaMemcpyAsync(flags, e->base.err, 4, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    CU(cudaMemsetAsync(e->base.err, 0, 4, s));
+    return LG_OK;
+}
+
+extern "C" int lg_random_actions(lg_env *e, int64_t *actions, uint64_t seed, void *stream) {
+    if (!e || !actions) {
+        set_err("null argument");
+        return LG_EINVAL;
+    }
+    CU(cudaSetDevice(e->device));
+    random_actions_kernel<<<(unsigned)((e->B + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        e->B, e->offset, seed, e->n_actions, (long long *)actions);
+    CU(cudaGetLastError());
+    return LG_OK;
+}
+
+template <class G, int DOM>
+static int launch_metrics_t(long long n, int H, int W, const uint8_t *tiles, const uint8_t *active,
+                            uint64_t *rng, int64_t *values, uint8_t *unreach, cudaStream_t s) {
+    int E = 256 / G::TEAM;
+    size_t smem = (size_t)E * G::ROWS * G::RUNS * 2;
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [] {
+        attr_err = cudaFuncSetAttribute(metrics_kernel<G, DOM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        200 * 1024);
+    });
+    CU(attr_err);
+    metrics_kernel<G, DOM><<<(unsigned)((n + E - 1) / E), 256, smem, s>>>(n, H, W, tiles, active, rng,
+                                                                           values, unreach);
+    CU(cudaGetLastError());
+    return LG_OK;
+}
+
+extern "C" int lg_metrics(int domain, int H, int W, int64_t n, const uint8_t *tiles, const uint8_t *active,
+                          uint64_t *rng, int64_t *values, uint8_t *unreach, void *stream) {
+    if (domain < 0 || domain > 2 || H < 1 || W < 1 || H > 64 || W > 64 || n < 0) {
+        set_err("bad metrics arguments");
+        return LG_EINVAL;
+    }
+    if (domain == 0 && !rng) {
+        set_err("binary metrics need generators");
+        return LG_EINVAL;
+    }
+    if (n == 0) return LG_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    int g = pick_geo(H, W);
+#define LGM(GG, D) launch_metrics_t<GG, D>(n, H, W, tiles, active, rng, values, unreach, s)
+    if (g == 16) return domain == 0 ? LGM(G16, 0) : domain == 1 ? LGM(G16, 1) : LGM(G16, 2);
+    if (g == 32) return domain == 0 ? LGM(G32, 0) : domain == 1 ? LGM(G32, 1) : LGM(G32, 2);
+    return domain == 0 ? LGM(G64, 0) : domain == 1 ? LGM(G64, 1) : LGM(G64, 2);
+#undef LGM
+}
+
+extern "C" int lg_seed_streams(uint64_t seed, int64_t offset, int64_t n, uint64_t *out) {
+    if (!out || n < 0) {
+        set_err("bad arguments");
+        return LG_EINVAL;
+    }
+    for (int64_t i = 0; i < n; i++) {
+        Pcg g;
+        seedseq_pcg(seed, true, (uint64_t)(offset + i), g);
+        out[6 * i + 0] = (uint64_t)(g.s >> 64);
+        out[6 * i + 1] = (uint64_t)g.s;
+        out[6 * i + 2] = (uint64_t)(g.inc >> 64);
+        out[6 * i + 3] = (uint64_t)g.inc;
+        out[6 * i + 4] = 0;
+        out[6 * i + 5] = 0;
+    }
+    return LG_OK;
+}

@@ -1,0 +1,291 @@
+// team.cuh -- one environment per lane team: bit-packed rows + warp collectives.
+//
+// A "team" of TEAM lanes (16 or 32, a warp or half a warp) owns one
+// environment. Lane l holds rows [l*RPL, l*RPL+RPL) of every bit-plane of the
+// max grid as machine words (bit c = column c). All grid algorithms are then
+// word-parallel per row and shuffle/vote-parallel across rows:
+//   * BFS layer  = row dilation (shift by one bit, shuffle one lane up/down)
+//                  masked by the passable plane (replaces the reference's
+//                  max-filter fixpoint, pathfind.py:143-175);
+//   * any/sum    = __any_sync / __reduce_add_sync over the team mask;
+//   * regions    = run-based union-find in shared memory (count_regions,
+//                  pathfind.py:116-130, same count).
+#pragma once
+#include <stdint.h>
+
+namespace lg {
+
+template <int TEAM_, int RPL_, typename Row_>
+struct Geo {
+    static constexpr int TEAM = TEAM_;
+    static constexpr int RPL = RPL_;
+    static constexpr int ROWS = TEAM_ * RPL_;
+    static constexpr int BITS = (int)sizeof(Row_) * 8;
+    static constexpr int RUNS = BITS / 2;  // max runs of set bits in one row
+    using Row = Row_;
+};
+using G16 = Geo<16, 1, uint32_t>;  // H <= 16, W <= 32
+using G32 = Geo<32, 1, uint32_t>;  // H <= 32, W <= 32
+using G64 = Geo<32, 2, uint64_t>;  // H <= 64, W <= 64
+
+__device__ __forceinline__ int ctz(uint32_t x) { return __ffs((int)x) - 1; }
+__device__ __forceinline__ int ctz(uint64_t x) { return __ffsll((long long)x) - 1; }
+__device__ __forceinline__ int msb(uint32_t x) { return 31 - __clz((int)x); }
+__device__ __forceinline__ int msb(uint64_t x) { return 63 - __clzll((long long)x); }
+__device__ __forceinline__ int popc(uint32_t x) { return __popc(x); }
+__device__ __forceinline__ int popc(uint64_t x) { return __popcll(x); }
+
+template <typename Row>
+__device__ __forceinline__ Row low_mask(int n) {
+    constexpr int B = (int)sizeof(Row) * 8;
+    return n >= B ? ~Row(0) : ((Row(1) << n) - Row(1));
+}
+
+template <class G>
+struct Team {
+    unsigned mask;  // lanes of this team within the warp
+    int lane;       // 0..TEAM-1
+    int base;       // first warp lane of the team
+    __device__ __forceinline__ Team() {
+        int l = threadIdx.x & 31;
+        lane = l & (G::TEAM - 1);
+        base = l - lane;
+        mask = G::TEAM == 32 ? 0xffffffffu : (((1u << G::TEAM) - 1u) << base);
+    }
+    __device__ __forceinline__ int row(int k) const { return lane * G::RPL + k; }
+    __device__ __forceinline__ bool any(bool p) const { return __any_sync(mask, p); }
+    __device__ __forceinline__ unsigned ballot(bool p) const {
+        return __ballot_sync(mask, p) >> base;
+    }
+    __device__ __forceinline__ int sum(int v) const {
+        return (int)__reduce_add_sync(mask, (unsigned)v);
+    }
+    __device__ __forceinline__ void sync() const { __syncwarp(mask); }
+    template <typename T>
+    __device__ __forceinline__ T from(T v, int src_lane) const {
+        return __shfl_sync(mask, v, src_lane, G::TEAM);
+    }
+    // value held by lane-1 (0 for the first lane)
+    template <typename T>
+    __device__ __forceinline__ T up(T v) const {
+        T r = __shfl_up_sync(mask, v, 1, G::TEAM);
+        return lane == 0 ? T(0) : r;
+    }
+    // value held by lane+1 (0 for the last lane)
+    template <typename T>
+    __device__ __forceinline__ T down(T v) const {
+        T r = __shfl_down_sync(mask, v, 1, G::TEAM);
+        return lane == G::TEAM - 1 ? T(0) : r;
+    }
+    // inclusive prefix sum over lanes
+    __device__ __forceinline__ int scan(int v) const {
+#pragma unroll
+        for (int o = 1; o < G::TEAM; o <<= 1) {
+            int y = __shfl_up_sync(mask, v, o, G::TEAM);
+            if (lane >= o) v += y;
+        }
+        return v;
+    }
+};
+
+// The lane's slice of one bit-plane.
+template <class G>
+struct Bd {
+    typename G::Row r[G::RPL];
+    __device__ __forceinline__ static Bd zero() {
+        Bd b;
+#pragma unroll
+        for (int k = 0; k < G::RPL; k++) b.r[k] = 0;
+        return b;
+    }
+    __device__ __forceinline__ bool nz() const {
+        typename G::Row x = 0;
+#pragma unroll
+        for (int k = 0; k < G::RPL; k++) x |= r[k];
+        return x != 0;
+    }
+    __device__ __forceinline__ int count() const {
+        int c = 0;
+#pragma unroll
+        for (int k = 0; k < G::RPL; k++) c += popc(r[k]);
+        return c;
+    }
+};
+
+#define LG_BD_OP(op)                                                              \
+    template <class G>                                                            \
+    __device__ __forceinline__ Bd<G> operator op(const Bd<G> &a, const Bd<G> &b) { \
+        Bd<G> o;                                                                  \
+        _Pragma("unroll") for (int k = 0; k < G::RPL; k++) o.r[k] = a.r[k] op b.r[k]; \
+        return o;                                                                 \
+    }
+LG_BD_OP(&)
+LG_BD_OP(|)
+#undef LG_BD_OP
+
+template <class G>
+__device__ __forceinline__ Bd<G> andnot(const Bd<G> &a, const Bd<G> &b) {
+    Bd<G> o;
+#pragma unroll
+    for (int k = 0; k < G::RPL; k++) o.r[k] = a.r[k] & ~b.r[k];
+    return o;
+}
+
+// Von Neumann dilation (cell plus its 4 neighbours), clipped to W columns.
+template <class G>
+__device__ __forceinline__ Bd<G> dilate(const Team<G> &t, const Bd<G> &f, typename G::Row wm) {
+    Bd<G> o;
+    if constexpr (G::RPL == 1) {
+        auto a = t.up(f.r[0]);
+        auto b = t.down(f.r[0]);
+        o.r[0] = (f.r[0] | (f.r[0] << 1) | (f.r[0] >> 1) | a | b) & wm;
+    } else {
+        auto a = t.up(f.r[1]);    // row 2l-1
+        auto b = t.down(f.r[0]);  // row 2l+2
+        o.r[0] = (f.r[0] | (f.r[0] << 1) | (f.r[0] >> 1) | a | f.r[1]) & wm;
+        o.r[1] = (f.r[1] | (f.r[1] << 1) | (f.r[1] >> 1) | f.r[0] | b) & wm;
+    }
+    return o;
+}
+
+// BFS from the cells of `f` through `pass`; on return `f` holds the last
+// non-empty layer and the result is its depth (flood_distance layers).
+template <class G>
+__device__ int bfs_last_layer(const Team<G> &t, Bd<G> &f, const Bd<G> &pass, typename G::Row wm) {
+    Bd<G> vis = f;
+    int depth = 0;
+    while (true) {
+        Bd<G> nx = andnot(dilate(t, f, wm) & pass, vis);
+        if (!t.any(nx.nz())) return depth;
+        vis = vis | nx;
+        f = nx;
+        depth++;
+    }
+}
+
+// First-touch distances of a BFS from `f` through `pass` to up to two target
+// sets. ENDPOINT=false: first layer containing a target cell (raw distance,
+// problems.py:190-191). ENDPOINT=true: targets are impassable endpoints read
+// one step past their nearest reached neighbour (endpoint_field,
+// pathfind.py:188-203), i.e. first layer whose dilation touches a target, +1.
+// -1 = never touched.
+template <class G, bool ENDPOINT>
+__device__ void bfs_touch(const Team<G> &t, Bd<G> f, const Bd<G> &pass, typename G::Row wm,
+                          const Bd<G> &ta, const Bd<G> &tb, bool want_b, int &da, int &db) {
+    da = -1;
+    db = -1;
+    bool need_a = t.any(ta.nz());
+    bool need_b = want_b && t.any(tb.nz());
+    Bd<G> vis = f;
+    int depth = 0;
+    while (need_a || need_b) {
+        Bd<G> d = dilate(t, f, wm);
+        if (ENDPOINT) {
+            if (need_a && t.any((d & ta).nz())) {
+                da = depth + 1;
+                need_a = false;
+            }
+            if (need_b && t.any((d & tb).nz())) {
+                db = depth + 1;
+                need_b = false;
+            }
+        } else {
+            if (need_a && t.any((f & ta).nz())) {
+                da = depth;
+                need_a = false;
+            }
+            if (need_b && t.any((f & tb).nz())) {
+                db = depth;
+                need_b = false;
+            }
+        }
+        if (!need_a && !need_b) break;
+        Bd<G> nx = andnot(d & pass, vis);
+        if (!t.any(nx.nz())) break;
+        vis = vis | nx;
+        f = nx;
+        depth++;
+    }
+}
+
+// ---- run-based union-find region count -----------------------------------
+// Nodes are runs of set bits, id = row * RUNS + run index (ids grow with the
+// row, so links always point to smaller ids: ECL-CC style lock-free hooking).
+
+__device__ __forceinline__ int uf_find(volatile uint16_t *par, int x) {
+    int cur = par[x];
+    if (cur != x) {
+        int prev = x, next;
+        while (cur > (next = par[cur])) {
+            par[prev] = (uint16_t)next;
+            prev = cur;
+            cur = next;
+        }
+    }
+    return cur;
+}
+
+// returns 1 when two distinct trees were merged
+__device__ __forceinline__ int uf_unite(volatile uint16_t *par, int a, int b) {
+    int ra = uf_find(par, a), rb = uf_find(par, b);
+    while (ra != rb) {
+        if (ra < rb) {
+            int t = ra;
+            ra = rb;
+            rb = t;
+        }
+        // hook root ra (larger id) under rb
+        unsigned short old = atomicCAS((unsigned short *)&par[ra], (unsigned short)ra,
+                                       (unsigned short)rb);
+        if (old == ra) return 1;
+        ra = old;
+    }
+    return 0;
+}
+
+template <class G>
+__device__ int count_regions(const Team<G> &t, const Bd<G> &pass, uint16_t *par_smem) {
+    using Row = typename G::Row;
+    volatile uint16_t *par = par_smem;
+    int runs = 0;
+#pragma unroll
+    for (int k = 0; k < G::RPL; k++) {
+        Row s = pass.r[k] & ~(pass.r[k] << 1);
+        int base = t.row(k) * G::RUNS;
+        int i = 0;
+        while (s) {
+            par[base + i] = (uint16_t)(base + i);
+            i++;
+            s &= s - 1;
+        }
+        runs += i;
+    }
+    t.sync();
+    Row above[G::RPL];
+    if constexpr (G::RPL == 1) {
+        above[0] = t.up(pass.r[0]);
+    } else {
+        above[0] = t.up(pass.r[1]);
+        above[1] = pass.r[0];
+    }
+    int links = 0;
+#pragma unroll
+    for (int k = 0; k < G::RPL; k++) {
+        int row = t.row(k);
+        Row R = pass.r[k], A = above[k];
+        Row C = R & A;
+        if (row == 0 || C == 0) continue;
+        Row SR = R & ~(R << 1), SA = A & ~(A << 1);
+        Row CS = C & ~(C << 1);
+        while (CS) {
+            int c = ctz(CS);
+            CS &= CS - 1;
+            Row upto = (c == G::BITS - 1) ? ~Row(0) : ((Row(2) << c) - Row(1));
+            int ir = popc(SR & upto) - 1, ia = popc(SA & upto) - 1;
+            links += uf_unite(par, row * G::RUNS + ir, (row - 1) * G::RUNS + ia);
+        }
+    }
+    return t.sum(runs - links);
+}
+
+}  // namespace lg

@@ -1,0 +1,426 @@
+"""``BatchEnv`` on B200: the reference's batched env API over the CUDA library.
+
+Host mirror of ``levelgen.env.BatchEnv`` (reference env.py:486-588): same
+constructor, properties, ``reset``/``step``/``observe``/``state_dict``/
+``load_state_dict`` and the same exceptions, backed by the C ABI in
+include/pcgrl_b200.h. Per-env random streams are
+``SeedSequence(seed).spawn(...)[global_offset + i]`` exactly as
+``spawn_rngs`` (env.py:591-594), so results are bit-identical to the
+reference for the same seed and actions, and independent of how a batch is
+sharded over GPUs.
+
+Outputs are CUDA tensors (obs float32 [B,C,OH,OW], reward float64 [B], done
+bool [B], info dict of [B] tensors). ``NumpyBatchEnv`` returns numpy arrays
+like the reference, copying through host buffers inside the library call.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Any
+
+import numpy as np
+
+from . import _lib
+from .config import EnvConfig
+from .tiles import get_domain
+
+INFO_KEYS = ("terminal", "episode_reward", "episode_length", "episode_start_loss", "final_loss")
+
+
+def make_lg_config(cfg: EnvConfig) -> _lib.LgConfig:
+    d = cfg.domain_obj
+    c = _lib.LgConfig()
+    c.domain = d.code
+    c.representation = ("narrow", "turtle", "wide").index(cfg.representation)
+    c.max_h, c.max_w = cfg.max_height, cfg.max_width
+    c.obs_size = cfg.obs_size
+    c.randomize_shape = int(bool(cfg.randomize_shape))
+    c.init_weighted = int((cfg.init_mode or d.default_init_mode) == "weighted")
+    for i, v in enumerate(cfg.init_cdf()):
+        c.init_cdf[i] = float(v)
+    pins = [d.tile_id(t) for t in cfg.pinpoints]
+    if len(pins) > 16:
+        raise ValueError("at most 16 pinpoints are supported on device")
+    c.n_pins = len(pins)
+    for i, t in enumerate(pins):
+        c.pins[i] = t
+    ctrl = [i for i, m in enumerate(d.metric_names) if m in cfg.controllable]
+    c.n_ctrl = len(ctrl)
+    for i, m in enumerate(ctrl):
+        c.ctrl[i] = m
+    if cfg.max_steps is not None and cfg.max_steps >= 2 ** 62:
+        raise ValueError("max_steps too large")
+    c.max_steps = int(cfg.max_steps or 0)
+    c.change_budget = int(cfg.change_budget or 0)
+    c.det_metrics = int(bool(cfg.deterministic_metrics))
+    w = cfg.weights()
+    for i, m in enumerate(d.metric_names):
+        c.weights[i] = float(w[m])
+    return c
+
+
+def _stream(torch, device):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _ptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class BatchEnv:
+    """Lockstep batch of identical-config environments with auto-reset."""
+
+    def __init__(self, config: EnvConfig, n_envs: int, seed: int = 0, *, device: Any = None,
+                 global_offset: int = 0, validate: bool = True):
+        import torch
+
+        self._torch = torch
+        if n_envs < 1:
+            raise ValueError("need at least one environment")
+        lib = _lib.load()
+        self._cfg = config
+        self.device = torch.device(device if device is not None else "cuda")
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        self.validate = validate
+        self._global_offset = int(global_offset)
+        self._seed = int(seed)
+        handle = ctypes.c_void_p()
+        cfgc = make_lg_config(config)
+        _lib.check(lib.lg_create(ctypes.byref(cfgc), int(n_envs), int(global_offset),
+                                 int(seed) & ((1 << 64) - 1), self.device.index, ctypes.byref(handle)))
+        self._h = handle
+        desc = _lib.LgDesc()
+        _lib.check(lib.lg_describe(self._h, ctypes.byref(desc)))
+        self._desc = desc
+        self._n = int(n_envs)
+        self._started = False
+
+    # -- properties (env.py:499-514) ----------------------------------------
+    @property
+    def config(self) -> EnvConfig:
+        return self._cfg
+
+    @property
+    def n_envs(self) -> int:
+        return self._n
+
+    @property
+    def n_actions(self) -> int:
+        return self._cfg.n_actions
+
+    @property
+    def observation_shape(self) -> tuple[int, int, int]:
+        return (self._desc.obs_c, self._desc.obs_h, self._desc.obs_w)
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        return self._h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                _lib.load().lg_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    # -- buffers -------------------------------------------------------------
+    def new_obs(self):
+        return self._torch.empty((self._n,) + self.observation_shape, dtype=self._torch.float32,
+                                 device=self.device)
+
+    def _info_buffers(self):
+        t, B, dev = self._torch, self._n, self.device
+        return {
+            "terminal": t.empty(B, dtype=t.bool, device=dev),
+            "episode_reward": t.empty(B, dtype=t.float64, device=dev),
+            "episode_length": t.empty(B, dtype=t.int64, device=dev),
+            "episode_start_loss": t.empty(B, dtype=t.float64, device=dev),
+            "final_loss": t.empty(B, dtype=t.float64, device=dev),
+        }
+
+    # -- API -------------------------------------------------------------------
+    def reset(self, out=None):
+        obs = self.new_obs() if out is None else out
+        with self._torch.cuda.device(self.device):
+            _lib.check(_lib.load().lg_reset(self._h, _ptr(obs), _stream(self._torch, self.device)))
+        self._started = True
+        if self.validate:
+            self.check_errors()
+        return obs
+
+    def _actions(self, actions):
+        t = self._torch
+        if isinstance(actions, t.Tensor):
+            a = actions
+            if a.shape != (self._n,):
+                raise ValueError(f"expected {self._n} actions, got shape {tuple(a.shape)}")
+            if a.device != self.device or a.dtype != t.int64:
+                a = a.to(device=self.device, dtype=t.int64)
+            a = a.contiguous()
+            if self.validate:
+                lo, hi = int(a.min()), int(a.max())
+                if lo < 0 or hi >= self.n_actions:
+                    raise ValueError("action id out of range")
+            return a
+        a = np.asarray(actions, dtype=np.int64)
+        if a.shape != (self._n,):
+            raise ValueError(f"expected {self._n} actions, got shape {a.shape}")
+        if a.size and (a.min() < 0 or a.max() >= self.n_actions):
+            raise ValueError("action id out of range")
+        return t.from_numpy(np.ascontiguousarray(a)).to(self.device, non_blocking=False)
+
+    def step(self, actions, *, out=None, stats=None, with_obs: bool = True):
+        """One transition (env.py:521-525): ``(obs, reward, done, info)``."""
+        if not self._started:
+            raise RuntimeError("reset() the batch before stepping")
+        t = self._torch
+        a = self._actions(actions)
+        obs = (self.new_obs() if out is None else out) if with_obs else None
+        reward = t.empty(self._n, dtype=t.float64, device=self.device)
+        done = t.empty(self._n, dtype=t.bool, device=self.device)
+        info = self._info_buffers()
+        ci = _lib.LgInfo(*[_ptr(info[k]) for k in INFO_KEYS])
+        with t.cuda.device(self.device):
+            _lib.check(_lib.load().lg_step(
+                self._h, _ptr(a), _ptr(obs) if obs is not None else None, _ptr(reward), _ptr(done),
+                ctypes.byref(ci), _ptr(stats) if stats is not None else None,
+                _stream(t, self.device)))
+        return obs, reward, done, info
+
+    def step_raw(self, actions, obs, reward, done, info=None, stats=None) -> None:
+        """Allocation-free step into caller-owned device tensors (bench path)."""
+        ci = None
+        if info is not None:
+            ci = ctypes.byref(_lib.LgInfo(*[_ptr(info[k]) if k in info else None for k in INFO_KEYS]))
+        _lib.check(_lib.load().lg_step(
+            self._h, _ptr(actions), _ptr(obs) if obs is not None else None, _ptr(reward), _ptr(done),
+            ci, _ptr(stats) if stats is not None else None, _stream(self._torch, self.device)))
+
+    def observe(self, out=None):
+        obs = self.new_obs() if out is None else out
+        with self._torch.cuda.device(self.device):
+            _lib.check(_lib.load().lg_observe(self._h, _ptr(obs), _stream(self._torch, self.device)))
+        return obs
+
+    def random_actions(self, seed: int, out=None):
+        t = self._torch
+        a = t.empty(self._n, dtype=t.int64, device=self.device) if out is None else out
+        _lib.check(_lib.load().lg_random_actions(self._h, _ptr(a), int(seed) & ((1 << 64) - 1),
+                                                 _stream(t, self.device)))
+        return a
+
+    def errors(self) -> int:
+        flags = ctypes.c_uint32(0)
+        _lib.check(_lib.load().lg_errors(self._h, ctypes.byref(flags), _stream(self._torch, self.device)))
+        return int(flags.value)
+
+    def check_errors(self) -> None:
+        f = self.errors()
+        if f & _lib.FLAG_BAD_ACTION:
+            raise ValueError("action id out of range")
+        if f & _lib.FLAG_PINPOINTS:
+            raise ValueError("pinpoints requested but not enough free cells")
+        if f & _lib.FLAG_NO_EDITABLE:
+            raise ValueError("no editable cells: every active cell is frozen")
+
+    # -- checkpoint support (env.py:535-585) ----------------------------------
+    def _state_tensors(self):
+        t, B, dev = self._torch, self._n, self.device
+        cfg = self._cfg
+        H, W, M = cfg.max_height, cfg.max_width, len(cfg.domain_obj.metric_names)
+        spec = {
+            "tiles": ((B, H, W), t.uint8), "active": ((B, H, W), t.uint8),
+            "frozen": ((B, H, W), t.uint8), "shape_hw": ((B, 2), t.int64),
+            "order": ((B, H * W), t.int32), "order_len": ((B,), t.int64),
+            "pos_idx": ((B,), t.int64), "pos": ((B, 2), t.int64), "t": ((B,), t.int64),
+            "changes": ((B,), t.int64), "max_steps": ((B,), t.int64), "lo": ((M, B), t.int64),
+            "hi": ((M, B), t.int64), "values": ((M, B), t.int64), "unreach": ((M, B), t.uint8),
+            "prev_loss": ((B,), t.float64), "ep_reward": ((B,), t.float64),
+            "ep_start_loss": ((B,), t.float64), "metric_seeds": ((B,), t.int64),
+            "rng": ((B, 6), t.int64),
+        }
+        return {k: t.empty(s, dtype=d, device=dev) for k, (s, d) in spec.items()}
+
+    def state_tensors(self) -> dict:
+        """Device-side state_dict (CUDA tensors, same keys/layout)."""
+        ts = self._state_tensors()
+        st = _lib.LgState(*[_ptr(ts[k]) for k in _lib.STATE_FIELDS])
+        with self._torch.cuda.device(self.device):
+            _lib.check(_lib.load().lg_export_state(self._h, ctypes.byref(st),
+                                                   _stream(self._torch, self.device)))
+        return ts
+
+    def state_dict(self) -> dict[str, Any]:
+        ts = self.state_tensors()
+        out = {k: v.cpu().numpy() for k, v in ts.items()}
+        for k in ("active", "frozen", "unreach"):
+            out[k] = out[k].astype(bool)
+        rng = out.pop("rng").view(np.uint64)
+        out["rng"] = rng
+        out["rng_states"] = [_rng_state_dict(r) for r in rng]
+        out["started"] = np.array([self._started])
+        return out
+
+    def load_state_dict(self, state: dict[str, Any]) -> None:
+        t = self._torch
+        cfg = self._cfg
+        B, W = self._n, cfg.max_width
+        host = {}
+        for k in _lib.STATE_FIELDS:
+            if k == "rng":
+                if "rng" in state:
+                    v = np.asarray(state["rng"], dtype=np.uint64)
+                else:
+                    v = np.stack([_rng_row(s) for s in state["rng_states"]])
+                host[k] = v.view(np.int64)
+                continue
+            if k == "pos":
+                if "pos" in state and cfg.representation == "turtle":
+                    v = np.asarray(state["pos"], dtype=np.int64)
+                else:
+                    order = np.asarray(state["order"])
+                    idx = np.asarray(state["pos_idx"], dtype=np.int64)
+                    flat = order[np.arange(B), np.clip(idx, 0, order.shape[1] - 1)].astype(np.int64)
+                    flat = np.maximum(flat, 0)
+                    v = np.stack([flat // W, flat % W], axis=1)
+                host[k] = v
+                continue
+            v = np.asarray(state[k])
+            if v.dtype == bool:
+                v = v.astype(np.uint8)
+            host[k] = v
+        ref = self._state_tensors()
+        dev = {}
+        for k, v in host.items():
+            npdt = _NP_OF[ref[k].dtype]
+            dev[k] = t.from_numpy(np.ascontiguousarray(v).astype(npdt)).to(self.device).reshape(
+                ref[k].shape)
+        st = _lib.LgState(*[_ptr(dev[k]) for k in _lib.STATE_FIELDS])
+        with t.cuda.device(self.device):
+            _lib.check(_lib.load().lg_import_state(self._h, ctypes.byref(st), _stream(t, self.device)))
+            t.cuda.current_stream(self.device).synchronize()
+        if "started" in state:
+            self._started = bool(np.asarray(state["started"]).ravel()[0])
+        else:
+            self._started = True
+
+    def grid_view(self, i: int):
+        sd = self.state_dict()
+        return {"tiles": sd["tiles"][i], "active": sd["active"][i], "frozen": sd["frozen"][i]}
+
+
+def _np_of():
+    import torch
+    return {torch.uint8: np.uint8, torch.int32: np.int32, torch.int64: np.int64,
+            torch.float64: np.float64, torch.float32: np.float32, torch.bool: np.bool_}
+
+
+class _LazyNp(dict):
+    def __missing__(self, key):
+        self.update(_np_of())
+        return dict.__getitem__(self, key)
+
+
+_NP_OF = _LazyNp()
+
+
+def _rng_state_dict(row) -> dict:
+    row = [int(x) for x in row]
+    return {"bit_generator": "PCG64", "state": {"state": (row[0] << 64) | row[1],
+                                                "inc": (row[2] << 64) | row[3]},
+            "has_uint32": row[4], "uinteger": row[5]}
+
+
+def _rng_row(st: dict) -> np.ndarray:
+    s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
+    m = (1 << 64) - 1
+    return np.array([s >> 64, s & m, inc >> 64, inc & m, int(st["has_uint32"]), int(st["uinteger"])],
+                    dtype=np.uint64)
+
+
+def spawn_streams(seed: int, n: int, offset: int = 0) -> np.ndarray:
+    """Host SeedSequence(seed).spawn(...)[offset:offset+n] PCG64 states ([n, 6] uint64)."""
+    out = np.zeros((n, 6), dtype=np.uint64)
+    _lib.check(_lib.load().lg_seed_streams(int(seed), int(offset), int(n),
+                                           out.ctypes.data_as(ctypes.c_void_p)))
+    return out
+
+
+class NumpyBatchEnv:
+    """Reference-shaped facade: numpy in, numpy out (env.py:486-588).
+
+    Every ``step`` goes through ``lg_step_host``: the host->device copy of the
+    actions and the device->host copies of obs/reward/done/info happen inside
+    the library call. Pass ``pinned=True`` to stage through page-locked
+    buffers (reused across steps; the arrays returned by ``step`` are then
+    overwritten by the next step unless ``copy=True``).
+    """
+
+    def __init__(self, config: EnvConfig, n_envs: int, seed: int = 0, *, device: Any = None,
+                 global_offset: int = 0, pinned: bool = False, copy: bool = True):
+        self.env = BatchEnv(config, n_envs, seed, device=device, global_offset=global_offset)
+        self.pinned = pinned
+        self.copy = copy
+        self._bufs = None
+
+    config = property(lambda self: self.env.config)
+    n_envs = property(lambda self: self.env.n_envs)
+    n_actions = property(lambda self: self.env.n_actions)
+    observation_shape = property(lambda self: self.env.observation_shape)
+
+    def _host(self):
+        t = self.env._torch
+        B = self.env.n_envs
+        def mk(shape, dt):
+            if self.pinned:
+                return t.empty(shape, dtype=dt, pin_memory=True).numpy()
+            return np.empty(shape, dtype=t.empty(0, dtype=dt).numpy().dtype)
+        return {"obs": mk((B,) + self.env.observation_shape, t.float32),
+                "actions": mk((B,), t.int64), "reward": mk((B,), t.float64),
+                "done": mk((B,), t.bool), "terminal": mk((B,), t.bool),
+                "episode_reward": mk((B,), t.float64), "episode_length": mk((B,), t.int64),
+                "episode_start_loss": mk((B,), t.float64), "final_loss": mk((B,), t.float64)}
+
+    def reset(self) -> np.ndarray:
+        return self.env.reset().cpu().numpy()
+
+    def observe(self) -> np.ndarray:
+        return self.env.observe().cpu().numpy()
+
+    def step(self, actions):
+        if not self.env._started:
+            raise RuntimeError("reset() the batch before stepping")
+        a = np.asarray(actions, dtype=np.int64)
+        if a.shape != (self.n_envs,):
+            raise ValueError(f"expected {self.n_envs} actions, got shape {a.shape}")
+        if a.size and (a.min() < 0 or a.max() >= self.n_actions):
+            raise ValueError("action id out of range")
+        if self._bufs is None or (self.copy and not self.pinned):
+            self._bufs = self._host()
+        b = self._bufs
+        np.copyto(b["actions"], a)
+        p = lambda x: x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        ci = _lib.LgInfo(*[p(b[k]) for k in INFO_KEYS])
+        t = self.env._torch
+        with t.cuda.device(self.env.device):
+            _lib.check(_lib.load().lg_step_host(self.env.handle, p(b["actions"]), p(b["obs"]),
+                                                p(b["reward"]), p(b["done"]), ctypes.byref(ci),
+                                                _stream(t, self.env.device)))
+        info = {k: b[k] for k in INFO_KEYS}
+        out = (b["obs"], b["reward"], b["done"], info)
+        if self.copy and self.pinned:
+            out = (b["obs"].copy(), b["reward"].copy(), b["done"].copy(),
+                   {k: v.copy() for k, v in info.items()})
+        return out
+
+    def state_dict(self):
+        return self.env.state_dict()
+
+    def load_state_dict(self, state):
+        self.env.load_state_dict(state)
+
+
+__all__ = ["BatchEnv", "NumpyBatchEnv", "EnvConfig", "get_domain", "spawn_streams", "make_lg_config"]
