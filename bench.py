@@ -1,0 +1,343 @@
+"""Throughput bench of the batched PCGRL env step (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c1..c5] [--envs B]
+
+A "step" is one pass of the hot path over the whole batch: device-side
+uniform random actions (harness.uniform_policy, harness.py:83-87) + BatchEnv.step
+(action apply, metric recompute, reward, auto-reset, observation write), as
+timed by the reference harness (harness.py:149-175).
+
+Default workload = config c5 (BASELINE.json configs[4]): binary 16x16 narrow,
+obs 31x31, 2^20 environments in total, sharded over the N GPUs (strong
+scaling: the global batch is fixed). The per-step observation output alone is
+16.1 GB, far larger than L2 (126 MB), so no L2 flush is needed between steps.
+
+For N > 1 run under torchrun (one process per GPU, NCCL); the timed region is
+bracketed by a barrier + synchronize, and the max over ranks is reported.
+``--impl reference`` times the CPU oracle port (oracle/, the reference's
+algorithm restated in C, all host cores) on a bounded sample of the same
+workload; under torchrun only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# BASELINE.json configs -> EnvConfig kwargs and global env counts
+CONFIGS = {
+    "c1": ("binary 16x16 narrow, full-map obs 31, 64 envs", dict(domain="binary"), 64),
+    "c2": ("maze 16x16 turtle, obs 31, 4096 envs", dict(domain="maze", representation="turtle"), 4096),
+    "c3": ("dungeon 16x16 wide, pinpoints + randomized shapes, 65536 envs",
+           dict(domain="dungeon", representation="wide", pinpoints=("player", "key", "door"),
+                randomize_shape=True), 65536),
+    "c4": ("binary narrow obs 7x7 on 64x64 maps, 65536 envs",
+           dict(domain="binary", max_width=64, max_height=64, obs_size=7), 65536),
+    "c5": ("binary 16x16 narrow, obs 31, 2^20 envs sharded over the GPUs",
+           dict(domain="binary"), 1 << 20),
+}
+METRIC = "env-steps/sec (binary 16x16 narrow) at 1/2/4/8 B200 vs host-CPU ref; HBM GB/s"
+UNIT = "env-steps/s"
+
+
+def algorithmic_bytes_per_env_step(obs_shape) -> int:
+    """API-mandated I/O = obs write 4*C*OH*OW + action read 8
+    + reward write 8 + done write 1."""
+    c, h, w = obs_shape
+    return 4 * c * h * w + 8 + 8 + 1
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic(config: str):
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(config)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+        self._t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self._t:
+            self._t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_oracle_run(cfg, n_envs: int, steps: int, warmup: int, threads: int):
+    """Time the CPU oracle (reference algorithm, C port) on the host cores."""
+    import numpy as np
+    from oracle import oracle as O
+
+    O.set_threads(threads)
+    env = O.OracleBatchEnv(cfg, n_envs, seed=0)
+    env.reset()
+    rng = np.random.default_rng(n_envs)
+    obs = np.empty((n_envs,) + env.observation_shape, dtype=np.float32)
+    for _ in range(warmup):
+        env.step_no_obs(rng.integers(0, cfg.n_actions, size=n_envs))
+        env.observe(obs)
+    acts = [rng.integers(0, cfg.n_actions, size=n_envs) for _ in range(steps)]
+    t0 = time.perf_counter()
+    for a in acts:
+        env.step_no_obs(a)
+        env.observe(obs)
+    dt = time.perf_counter() - t0
+    return n_envs * steps / dt, dt
+
+
+def run_reference(args, cfg, workload, rank):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    n = args.cpu_envs or min(CONFIGS[args.config][2], 65536)
+    value, dt = cpu_oracle_run(cfg, n, args.steps, args.warmup, threads)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8/int32/f64",
+        "data": "synthetic (uniform random actions, seed 0)",
+        "config": {"workload": workload, "config": args.config, "envs_sampled": n},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{n} envs x {args.steps} steps of the same config "
+                                   f"(oracle/ C restatement of levelgen BatchEnv.step+observe)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
+    ap.add_argument("--envs", type=int, default=0, help="override the global env count")
+    ap.add_argument("--cpu-envs", type=int, default=0)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        args.gpus = world
+
+    from paper_2408_12525_b200.config import EnvConfig
+    desc, kw, default_b = CONFIGS[args.config]
+    cfg = EnvConfig(**kw)
+    global_b = args.envs or default_b
+    workload = f"{args.config}: {desc}"
+
+    if args.impl == "reference":
+        run_reference(args, cfg, workload, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2408_12525_b200.env import INFO_KEYS, BatchEnv, NumpyBatchEnv
+
+    if global_b % world:
+        raise SystemExit("global env count must divide by the number of GPUs")
+    B = global_b // world
+    env = BatchEnv(cfg, B, seed=0, device=dev, global_offset=rank * B, validate=False)
+    obs = env.new_obs()
+    acts = torch.empty(B, dtype=torch.int64, device=dev)
+    reward = torch.empty(B, dtype=torch.float64, device=dev)
+    done = torch.empty(B, dtype=torch.bool, device=dev)
+    info = env._info_buffers()
+    stats = torch.zeros(5, dtype=torch.float64, device=dev)
+    env.reset(out=obs)
+    stream = torch.cuda.current_stream(dev)
+
+    def one_step(i):
+        env.random_actions(1_000_003 * i + 17, out=acts)
+        env.step_raw(acts, obs, reward, done, info, stats)
+
+    for i in range(args.warmup):
+        one_step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = ClockSampler(local_rank)
+    clk.start()
+    time.sleep(0.3)
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_start.record(stream)
+    for i in range(K):
+        env.random_actions(1_000_003 * (i + args.warmup) + 17, out=acts)
+        ev[i][0].record(stream)
+        env.step_raw(acts, obs, reward, done, info, stats)
+        ev[i][1].record(stream)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    step_ms = sum(a.elapsed_time(b) for a, b in ev) / K
+    if world > 1:
+        t = torch.tensor([elapsed_ms, step_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms, step_ms = float(t[0]), float(t[1])
+        dist.all_reduce(stats)  # the episode-stats reduce over NVLink
+    errs = env.errors()
+    if errs:
+        raise SystemExit(f"device error flags {errs}")
+    value = global_b * K / (elapsed_ms / 1e3)
+
+    bytes_step = algorithmic_bytes_per_env_step(env.observation_shape)
+    peak, peak_kind = load_peaks()
+    achieved_gbs = B * bytes_step / (step_ms / 1e3) / 1e9
+
+    # end to end through the public numpy API: H2D actions from pinned host
+    # memory, D2H obs/reward/done/info into pinned host buffers, every step.
+    e2e = None
+    if not args.no_e2e:
+        del obs
+        torch.cuda.empty_cache()
+        nenv = NumpyBatchEnv(cfg, B, seed=0, device=dev, global_offset=rank * B, pinned=True, copy=False)
+        nenv.reset()
+        import numpy as np
+        rng = np.random.default_rng(1)
+        host_acts = [rng.integers(0, cfg.n_actions, size=B) for _ in range(args.e2e_steps + 1)]
+        nenv.step(host_acts[0])
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for a in host_acts[1:]:
+            nenv.step(a)
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t[0])
+        obs_b = 4 * int(np.prod(env.observation_shape))
+        e2e = {"value": global_b * args.e2e_steps / dt, "unit": UNIT,
+               "h2d_bytes_per_step": B * 8,
+               "d2h_bytes_per_step": B * (obs_b + 8 + 1 + 1 + 8 + 8 + 8 + 8),
+               "steps": args.e2e_steps, "api": "NumpyBatchEnv.step -> lg_step_host (pinned)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        n_cpu = args.cpu_envs or min(global_b, 65536)
+        # size the sample to roughly cpu-seconds of work
+        v0, dt0 = cpu_oracle_run(cfg, n_cpu, 2, 1, threads)
+        steps_cpu = max(2, int(args.cpu_seconds / max(dt0 / 2, 1e-3)))
+        steps_cpu = min(steps_cpu, 200)
+        v, dt = cpu_oracle_run(cfg, n_cpu, steps_cpu, 1, threads)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{n_cpu} envs x {steps_cpu} steps ({dt:.1f} s) of {args.config}; "
+                         f"oracle/ C restatement of levelgen BatchEnv.step+observe, OpenMP"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": elapsed_ms / K, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8/int32/f64 (obs f32)",
+            "data": "synthetic (device uniform random actions; env streams SeedSequence(0).spawn)",
+            "config": {"workload": workload, "config": args.config, "global_envs": global_b,
+                       "envs_per_gpu": B, "obs_shape": list(env.observation_shape),
+                       "parallelism": f"env-sharded x{world}",
+                       "l2": "no flush: per-step obs output (%.1f GB) >> 126 MB L2" %
+                             (B * 4 * env.observation_shape[0] * env.observation_shape[1] *
+                              env.observation_shape[2] / 1e9)},
+            "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
+                         "frac": achieved_gbs / peak, "traffic": load_traffic(args.config),
+                         "peak_kind": peak_kind, "kernel": "env_kernel (fused step + obs)",
+                         "bytes_per_env_step": bytes_step, "step_kernel_ms": step_ms},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": 2 * K,
+            "clocks": clocks,
+            "episode_stats": [float(x) for x in stats.cpu()],
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

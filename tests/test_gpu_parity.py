@@ -204,8 +204,10 @@ def test_numpy_facade_and_errors():
     dev.step(torch.tensor([0, 0, 7, 0], device="cuda"))
     assert dev.errors() & _lib.FLAG_BAD_ACTION
     assert dev.errors() == 0
+    strict = BatchEnv(cfg, 4, seed=0)
+    strict.reset()
     with pytest.raises(ValueError):
-        BatchEnv(cfg, 4, seed=0).step(torch.tensor([0, 0, 7, 0], device="cuda"))
+        strict.step(torch.tensor([0, 0, 7, 0], device="cuda"))
 
 
 def test_pinpoint_overflow_flags_error():
