@@ -10,9 +10,10 @@
 //     advance scan position -> done / info -> in-kernel auto-reset
 //     (reset_rows, env.py:284-305, numpy-exact draws) -> store state ->
 //     render the env's 0/1 observation planes as a bit image in shared memory
-//   phase 2 (whole block)
-//     expand the bit images of the block's envs (contiguous in the output) to
-//     float32 with coalesced 128-bit streaming stores (st.global.cs.v4).
+//   phase 2 (same team, no block barrier)
+//     expand the env's bit image to float32 with 128-bit streaming stores.
+// This lane-team kernel serves maps larger than 16x16 (up to 64x64); smaller
+// maps run one env per thread (solo_kernel.cuh).
 //
 // The observation write is the HBM roofline of the path (15,376 B per env-step
 // for binary 16x16 / obs 31 against ~330 B of state traffic).
@@ -182,59 +183,84 @@ __device__ __forceinline__ int team_count(const Team<G> &t, const Bd<G> &b) {
     return t.sum(b.count());
 }
 
-// pl: tile planes, act: active board. g: the metric generator (binary only).
-template <class G, int DOM>
-__device__ void compute_metrics(const Team<G> &t, const Bd<G> *pl, const Bd<G> &act,
-                                typename G::Row wm, Pcg &g, uint16_t *uf, int *val, int &unr) {
+// Backend of the generic metric code for a lane team (team.cuh).
+template <class G>
+struct TeamK {
+    using B = Bd<G>;
+    Team<G> t;
+    typename G::Row wm;
+    __device__ __forceinline__ int count(const B &b) const { return t.sum(b.count()); }
+    __device__ __forceinline__ B cell(int flat) const { return cell_board(t, flat); }
+    __device__ __forceinline__ int kth(const B &b, int k) const { return kth_cell(t, b, k); }
+    __device__ __forceinline__ int lowest(const B &b) const { return lowest_cell(t, b); }
+    __device__ __forceinline__ int bfs_last(B &f, const B &pass) const {
+        return bfs_last_layer(t, f, pass, wm);
+    }
+    template <bool ENDPOINT>
+    __device__ __forceinline__ void touch(B f, const B &pass, const B &ta, const B &tb, bool want_b,
+                                          int &da, int &db) const {
+        bfs_touch<G, ENDPOINT>(t, f, pass, wm, ta, tb, want_b, da, db);
+    }
+    __device__ __forceinline__ int regions(const B &pass, void *uf) const {
+        return count_regions(t, pass, reinterpret_cast<uint16_t *>(uf));
+    }
+};
+
+// compute_metrics_batch for one level (problems.py:105-243), generic over the
+// board backend K (lane team or single thread). pl: stored tile planes
+// (tile p+1), act: active mask, g: metric generator (binary draw only).
+template <class K, int DOM>
+__device__ void compute_metrics(const K &k, const typename K::B *pl, const typename K::B &act, Pcg &g,
+                                void *uf, int *val, int &unr) {
+    using B = typename K::B;
     unr = 0;
     if constexpr (DOM == 0) {
         // _binary_metrics (problems.py:136-173)
-        Bd<G> pass = andnot(act, pl[0]);
-        val[1] = count_regions(t, pass, uf);
-        int cnt = team_count(t, pass);
+        B pass = andnot(act, pl[0]);
+        val[1] = k.regions(pass, uf);
+        int cnt = k.count(pass);
         val[0] = 0;
         if (cnt > 0) {
-            int k = (int)pcg_integers(g, 0, cnt);  // problems.py:152-154
-            Bd<G> f = cell_board(t, kth_cell(t, pass, k));
-            bfs_last_layer(t, f, pass, wm);
-            int y = lowest_cell(t, f);  // np.argmax: lowest flat index at max d1
-            Bd<G> f2 = cell_board(t, y);
-            val[0] = bfs_last_layer(t, f2, pass, wm);
+            int kk = (int)pcg_integers(g, 0, cnt);  // problems.py:152-154
+            B f = k.cell(k.kth(pass, kk));
+            k.bfs_last(f, pass);
+            int y = k.lowest(f);  // np.argmax: lowest flat index at max d1
+            B f2 = k.cell(y);
+            val[0] = k.bfs_last(f2, pass);
         }
     } else if constexpr (DOM == 1) {
-        // _maze_metrics (problems.py:176-198)
-        Bd<G> pass = andnot(act, pl[0]);  // AIR | PLAYER | DOOR
-        const Bd<G> &players = pl[1], &doors = pl[2];
-        int np = team_count(t, players), nd = team_count(t, doors);
+        // _maze_metrics (problems.py:176-198): passable AIR | PLAYER | DOOR
+        B pass = andnot(act, pl[0]);
+        const B &players = pl[1], &doors = pl[2];
+        int np = k.count(players), nd = k.count(doors);
         val[2] = np;
         val[3] = nd;
-        val[1] = count_regions(t, pass, uf);
+        val[1] = k.regions(pass, uf);
         int d = -1, dummy;
-        if (np > 0 && nd > 0) bfs_touch<G, false>(t, players, pass, wm, doors, doors, false, d, dummy);
+        if (np > 0 && nd > 0) k.template touch<false>(players, pass, doors, doors, false, d, dummy);
         bool bad = d < 0;
         val[0] = bad ? 0 : d;
         unr = bad ? 1 : 0;
     } else {
         // _dungeon_metrics (problems.py:201-243); planes WALL ENEMY KEY DOOR PLAYER
-        const Bd<G> &enemy = pl[1], &key = pl[2], &door = pl[3], &player = pl[4];
-        Bd<G> trav = andnot(andnot(andnot(andnot(act, pl[0]), enemy), key), door);  // AIR|PLAYER
-        int cp = team_count(t, player), ck = team_count(t, key), cd = team_count(t, door),
-            ce = team_count(t, enemy);
+        const B &enemy = pl[1], &key = pl[2], &door = pl[3], &player = pl[4];
+        B trav = andnot(andnot(andnot(andnot(act, pl[0]), enemy), key), door);  // AIR | PLAYER
+        int cp = k.count(player), ck = k.count(key), cd = k.count(door), ce = k.count(enemy);
         val[2] = cp;
         val[3] = ck;
         val[4] = cd;
         val[5] = ce;
         int leg1 = -1, nearv = -1, leg2 = -1, dummy;
-        if (cp > 0) bfs_touch<G, true>(t, player, trav, wm, key, enemy, true, leg1, nearv);
+        if (cp > 0) k.template touch<true>(player, trav, key, enemy, true, leg1, nearv);
         bool missing = cp == 0 || ck == 0 || cd == 0;
-        if (!missing && leg1 >= 0) bfs_touch<G, true>(t, key, trav, wm, door, door, false, leg2, dummy);
+        if (!missing && leg1 >= 0) k.template touch<true>(key, trav, door, door, false, leg2, dummy);
         bool bad = missing || leg1 < 0 || leg2 < 0;
         val[0] = bad ? 0 : leg1 + leg2;
         bool badn = cp == 0 || ce == 0 || nearv < 0;
         val[6] = badn ? 0 : nearv;
         unr = (bad ? 1 : 0) | (badn ? 64 : 0);
-        Bd<G> open = andnot(andnot(act, pl[0]), enemy);  // AIR|PLAYER|KEY|DOOR
-        val[1] = count_regions(t, open, uf);
+        B open = andnot(andnot(act, pl[0]), enemy);  // AIR | PLAYER | KEY | DOOR
+        val[1] = k.regions(open, uf);
     }
 }
 
@@ -264,14 +290,14 @@ template <class G, int DOM>
 __device__ void recompute(const Params &p, const Team<G> &t, EnvRegs<G, DOM> &e, uint16_t *uf,
                           bool reset) {
     using Row = typename G::Row;
-    Row wm = low_mask<Row>(p.W);
+    TeamK<G> k{t, low_mask<Row>(p.W)};
     Bd<G> act = rect_board(t, e.h, e.w);
     if (p.det) {  // _metric_rngs: fresh default_rng(metric_seed) (env.py:327-330)
         Pcg mg;
         seedseq_pcg((uint64_t)e.mseed, false, 0, mg);
-        compute_metrics<G, DOM>(t, e.pl, act, wm, mg, uf, e.val, e.unr);
+        compute_metrics<TeamK<G>, DOM>(k, e.pl, act, mg, uf, e.val, e.unr);
     } else {
-        compute_metrics<G, DOM>(t, e.pl, act, wm, e.g, uf, e.val, e.unr);
+        compute_metrics<TeamK<G>, DOM>(k, e.pl, act, e.g, uf, e.val, e.unr);
     }
     double l = loss_of<DOM>(p, e.val, e.unr, e.lo, e.hi);
     e.prev_loss = l;
@@ -660,51 +686,45 @@ __device__ void render_env(const Params &p, const Team<G> &t, const EnvRegs<G, D
     }
 }
 
-// Phase 2: expand the block's bit images to float32, coalesced 16-byte stores.
-__device__ __forceinline__ float obs_value(const Params &p, const unsigned char *smem, uint32_t e) {
-    uint32_t el = fdiv(p.divPE, e);
-    uint32_t le = e - el * p.PE;
-    const unsigned char *es = smem + (size_t)el * p.env_smem;
+// Expand one env's bit image to float32: its output range is written by the
+// env's own team (no block barrier), with 16-byte streaming stores.
+__device__ __forceinline__ float team_elem(const Params &p, const unsigned char *es, uint32_t le) {
     if (le < p.PB) {
         const uint32_t *img = reinterpret_cast<const uint32_t *>(es);
         return ((img[le >> 5] >> (le & 31)) & 1u) ? 1.0f : 0.0f;
     }
-    const float *ctrl = reinterpret_cast<const float *>(es + p.off_ctrl);
-    return ctrl[fdiv(p.divOO, le - p.PB)];
+    return reinterpret_cast<const float *>(es + p.off_ctrl)[fdiv(p.divOO, le - p.PB)];
 }
 
-__device__ void write_obs_block(const Params &p, const unsigned char *smem, long long env0, int E) {
-    long long rem = (long long)p.B - env0;
-    int nenv = rem < E ? (int)rem : E;
-    if (nenv <= 0) return;
-    float *out = p.obs + (size_t)env0 * p.PE;
-    uint32_t total = (uint32_t)nenv * p.PE;
-    uint32_t nvec = total >> 2;
-    float4 *out4 = reinterpret_cast<float4 *>(out);
-    for (uint32_t q = threadIdx.x; q < nvec; q += blockDim.x) {
-        uint32_t e = q << 2;
-        uint32_t el = fdiv(p.divPE, e);
-        uint32_t le = e - el * p.PE;
+template <class G>
+__device__ void write_obs_team(const Params &p, const Team<G> &t, long long env, const unsigned char *es) {
+    const uint32_t *img = reinterpret_cast<const uint32_t *>(es);
+    const size_t base = (size_t)env * p.PE;
+    float *out = p.obs + base;
+    uint32_t head = (uint32_t)((4 - (base & 3)) & 3);
+    if (head > p.PE) head = p.PE;
+    for (uint32_t e = t.lane; e < head; e += G::TEAM) out[e] = team_elem(p, es, e);
+    const uint32_t n4 = (p.PE - head) >> 2;
+    float4 *o4 = reinterpret_cast<float4 *>(out + head);
+    for (uint32_t q = t.lane; q < n4; q += G::TEAM) {
+        uint32_t le = head + (q << 2);
         float4 v;
         if (le + 3 < p.PB) {
-            const uint32_t *img = reinterpret_cast<const uint32_t *>(smem + (size_t)el * p.env_smem);
-            uint32_t wi = le >> 5, sh = le & 31;
-            uint64_t two = (uint64_t)img[wi] | ((uint64_t)img[wi + 1] << 32);
-            uint32_t bits = (uint32_t)(two >> sh);
-            v.x = (bits & 1u) ? 1.0f : 0.0f;
-            v.y = (bits & 2u) ? 1.0f : 0.0f;
-            v.z = (bits & 4u) ? 1.0f : 0.0f;
-            v.w = (bits & 8u) ? 1.0f : 0.0f;
+            uint32_t wi = le >> 5;
+            uint32_t x = __funnelshift_r(img[wi], img[wi + 1], le & 31);
+            v.x = (x & 1u) ? 1.0f : 0.0f;
+            v.y = (x & 2u) ? 1.0f : 0.0f;
+            v.z = (x & 4u) ? 1.0f : 0.0f;
+            v.w = (x & 8u) ? 1.0f : 0.0f;
         } else {
-            v.x = obs_value(p, smem, e);
-            v.y = obs_value(p, smem, e + 1);
-            v.z = obs_value(p, smem, e + 2);
-            v.w = obs_value(p, smem, e + 3);
+            v.x = team_elem(p, es, le);
+            v.y = team_elem(p, es, le + 1);
+            v.z = team_elem(p, es, le + 2);
+            v.w = team_elem(p, es, le + 3);
         }
-        __stcs(out4 + q, v);
+        __stcs(o4 + q, v);
     }
-    for (uint32_t e = (nvec << 2) + threadIdx.x; e < total; e += blockDim.x)
-        out[e] = obs_value(p, smem, e);
+    for (uint32_t e = head + (n4 << 2) + t.lane; e < p.PE; e += G::TEAM) out[e] = team_elem(p, es, e);
 }
 
 // ---------------------------------------------------------------------------
@@ -719,8 +739,7 @@ __global__ void __launch_bounds__(256) env_kernel(const Params p, int mode) {
     Team<G> t;
     const int E = blockDim.x / G::TEAM;
     const int ti = threadIdx.x / G::TEAM;
-    const long long env0 = (long long)blockIdx.x * E;
-    const long long env = env0 + ti;
+    const long long env = (long long)blockIdx.x * E + ti;
     unsigned char *es = smem + (size_t)ti * p.env_smem;
     uint16_t *uf = reinterpret_cast<uint16_t *>(es);  // aliases the bit image (phases differ)
 
@@ -845,11 +864,9 @@ __global__ void __launch_bounds__(256) env_kernel(const Params p, int mode) {
         if (p.obs) {
             t.sync();  // union-find scratch is reused for the image
             render_env<G, DOM>(p, t, e, es);
+            t.sync();
+            write_obs_team<G>(p, t, env, es);
         }
-    }
-    if (p.obs) {
-        __syncthreads();
-        write_obs_block(p, smem, env0, E);
     }
 }
 

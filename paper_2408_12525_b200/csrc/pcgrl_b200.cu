@@ -10,6 +10,7 @@
 
 #include "../../include/pcgrl_b200.h"
 #include "env_kernels.cuh"
+#include "solo_kernel.cuh"
 
 using namespace lg;
 
@@ -252,7 +253,8 @@ __global__ void __launch_bounds__(256) metrics_kernel(long long n, int H, int W,
         g.u = (uint32_t)rg[5];
     }
     int val[8] = {0, 0, 0, 0, 0, 0, 0, 0}, unr = 0;
-    compute_metrics<G, DOM>(t, pl, act, low_mask<Row>(W), g, uf, val, unr);
+    TeamK<G> k{t, low_mask<Row>(W)};
+    compute_metrics<TeamK<G>, DOM>(k, pl, act, g, uf, val, unr);
     if (t.lane != 0) return;
     for (int m = 0; m < M; m++) {
         values[(size_t)m * n + b] = val[m];
@@ -276,7 +278,7 @@ struct lg_env {
     int device;
     long long B, offset;
     unsigned long long seed;
-    int geo;  // 16, 32, 64
+    int geo;  // 1 = solo (thread per env), 16 / 32 / 64 = lane-team row capacity
     int team, threads, E;
     int N, M, NPL, C, OH, OW;
     long long n_actions;
@@ -325,9 +327,27 @@ static int launch_env_t(lg_env *e, const Params &p, int mode, cudaStream_t s) {
     return LG_OK;
 }
 
+template <int DOM>
+static int launch_solo_t(lg_env *e, const Params &p, int mode, cudaStream_t s) {
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [] {
+        attr_err = cudaFuncSetAttribute(env_solo_kernel<DOM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        200 * 1024);
+    });
+    CU(attr_err);
+    long long grid = (e->B + e->threads - 1) / e->threads;
+    env_solo_kernel<DOM><<<(unsigned)grid, e->threads, e->smem, s>>>(p, mode);
+    CU(cudaGetLastError());
+    return LG_OK;
+}
+
 static int launch_env(lg_env *e, const Params &p, int mode, cudaStream_t s) {
     int d = e->cfg.domain;
     switch (e->geo) {
+    case 1:
+        return d == 0 ? launch_solo_t<0>(e, p, mode, s) : d == 1 ? launch_solo_t<1>(e, p, mode, s)
+                                                                 : launch_solo_t<2>(e, p, mode, s);
     case 16:
         return d == 0 ? launch_env_t<G16, 0>(e, p, mode, s)
                : d == 1 ? launch_env_t<G16, 1>(e, p, mode, s)
@@ -353,10 +373,23 @@ static int launch_state_t(lg_env *e, const Params &p, const lg_state &st, bool e
     return LG_OK;
 }
 
+template <int DOM>
+static int launch_solo_state_t(lg_env *e, const Params &p, const lg_state &st, bool exp, cudaStream_t s) {
+    unsigned grid = (unsigned)((e->B + 127) / 128);
+    if (exp) solo_export_kernel<DOM><<<grid, 128, 0, s>>>(p, st);
+    else solo_import_kernel<DOM><<<grid, 128, 0, s>>>(p, st);
+    CU(cudaGetLastError());
+    return LG_OK;
+}
+
 static int launch_state(lg_env *e, const lg_state &st, bool exp, cudaStream_t s) {
     int d = e->cfg.domain;
     const Params &p = e->base;
     switch (e->geo) {
+    case 1:
+        return d == 0 ? launch_solo_state_t<0>(e, p, st, exp, s)
+               : d == 1 ? launch_solo_state_t<1>(e, p, st, exp, s)
+                        : launch_solo_state_t<2>(e, p, st, exp, s);
     case 16:
         return d == 0 ? launch_state_t<G16, 0>(e, p, st, exp, s)
                : d == 1 ? launch_state_t<G16, 1>(e, p, st, exp, s)
@@ -372,7 +405,13 @@ static int launch_state(lg_env *e, const lg_state &st, bool exp, cudaStream_t s)
     }
 }
 
+static bool force_team() {
+    const char *v = getenv("LG_FORCE_TEAM");
+    return v && v[0] == '1';
+}
+
 static int pick_geo(int H, int W) {
+    if (W <= 16 && H <= 16 && !force_team()) return 1;
     if (W <= 32 && H <= 16) return 16;
     if (W <= 32 && H <= 32) return 32;
     return 64;
@@ -429,10 +468,6 @@ extern "C" int lg_create(const lg_config *cfg, int64_t n_envs, int64_t global_of
     e->offset = global_offset;
     e->seed = seed;
     const int H = cfg->max_h, W = cfg->max_w;
-    e->geo = pick_geo(H, W);
-    e->team = e->geo == 16 ? 16 : 32;
-    e->threads = 256;
-    e->E = e->threads / e->team;
     e->N = dom_n(cfg->domain);
     e->M = dom_m(cfg->domain);
     e->NPL = e->N - 1;
@@ -446,11 +481,6 @@ extern "C" int lg_create(const lg_config *cfg, int64_t n_envs, int64_t global_of
     e->n_actions = cfg->representation == LG_TURTLE ? 4 + e->N
                    : cfg->representation == LG_WIDE ? (long long)H * W * e->N
                                                     : e->N + 1;
-    int rows = e->geo == 16 ? 16 : e->geo == 32 ? 32 : 64;
-    e->row_bytes = e->geo == 64 ? 8 : 4;
-    e->rows_per_env = (size_t)(e->NPL + 1) * rows;
-    int runs = e->geo == 64 ? 32 : 16;
-    size_t uf_bytes = (size_t)rows * runs * 2;
 
     Params &p = e->base;
     memset(&p, 0, sizeof p);
@@ -481,12 +511,41 @@ extern "C" int lg_create(const lg_config *cfg, int64_t n_envs, int64_t global_of
     p.PE = (uint32_t)e->C * p.OO;
     fastdiv_init(p.divPE, p.PE);
     fastdiv_init(p.divOO, p.OO);
-    p.img_words = (int)((p.PB + 31) / 32 + 1);
-    size_t scratch = uf_bytes > (size_t)p.img_words * 4 ? uf_bytes : (size_t)p.img_words * 4;
-    scratch = (scratch + 15) & ~(size_t)15;
-    p.off_ctrl = (int)scratch;
-    p.env_smem = (int)(scratch + 32);
-    e->smem = (size_t)e->E * p.env_smem;
+    p.img_words = (int)((p.PB + 31) / 32 + 1);  // + pad word for the 2-word funnel shift
+
+    e->geo = pick_geo(H, W);
+    if (e->geo == 1) {
+        // one env per thread; per-env shared slot (in 32-bit words): bit image +
+        // 8 control floats, >= 33 words (union-find scratch), odd stride so the
+        // 32 lanes of a warp hit 32 different banks.
+        int slot = p.img_words + 8;
+        if (slot < 33) slot = 33;
+        if (!(slot & 1)) slot++;
+        p.env_smem = slot;
+        e->threads = 64;
+        e->team = 1;
+        e->E = 64;
+        e->smem = (size_t)64 * slot * 4;
+        if (e->OW > 64 || e->smem > 200 * 1024) e->geo = pick_geo(17, W);  // too wide: lane teams
+    }
+    if (e->geo != 1) {
+        e->team = e->geo == 16 ? 16 : 32;
+        e->threads = 256;
+        e->E = e->threads / e->team;
+        int rows = e->geo == 16 ? 16 : e->geo == 32 ? 32 : 64;
+        int runs = e->geo == 64 ? 32 : 16;
+        size_t uf_bytes = (size_t)rows * runs * 2;
+        size_t scratch = uf_bytes > (size_t)p.img_words * 4 ? uf_bytes : (size_t)p.img_words * 4;
+        scratch = (scratch + 15) & ~(size_t)15;
+        p.off_ctrl = (int)scratch;
+        p.env_smem = (int)(scratch + 32);
+        e->smem = (size_t)e->E * p.env_smem;
+        e->row_bytes = e->geo == 64 ? 8 : 4;
+        e->rows_per_env = (size_t)(e->NPL + 1) * rows;
+    } else {
+        e->row_bytes = 4;
+        e->rows_per_env = (size_t)(e->NPL + 1) * 8;
+    }
     if (e->smem > 200 * 1024) {
         set_err("observation window too large for shared memory staging");
         delete e;
@@ -729,6 +788,15 @@ extern "C" int lg_metrics(int domain, int H, int W, int64_t n, const uint8_t *ti
     if (n == 0) return LG_OK;
     cudaStream_t s = (cudaStream_t)stream;
     int g = pick_geo(H, W);
+    if (g == 1) {
+        unsigned grid = (unsigned)((n + 127) / 128);
+        size_t smem = 128 * 33 * 4;
+        if (domain == 0) solo_metrics_kernel<0><<<grid, 128, smem, s>>>(n, H, W, tiles, active, rng, values, unreach);
+        else if (domain == 1) solo_metrics_kernel<1><<<grid, 128, smem, s>>>(n, H, W, tiles, active, rng, values, unreach);
+        else solo_metrics_kernel<2><<<grid, 128, smem, s>>>(n, H, W, tiles, active, rng, values, unreach);
+        CU(cudaGetLastError());
+        return LG_OK;
+    }
 #define LGM(GG, D) launch_metrics_t<GG, D>(n, H, W, tiles, active, rng, values, unreach, s)
     if (g == 16) return domain == 0 ? LGM(G16, 0) : domain == 1 ? LGM(G16, 1) : LGM(G16, 2);
     if (g == 32) return domain == 0 ? LGM(G32, 0) : domain == 1 ? LGM(G32, 1) : LGM(G32, 2);

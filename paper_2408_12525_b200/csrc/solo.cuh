@@ -1,0 +1,218 @@
+// solo.cuh -- one environment per THREAD for maps up to 16 x 16.
+//
+// A 16x16 bit-plane is eight 32-bit registers: word k holds row 2k in bits
+// 0..15 and row 2k+1 in bits 16..31, so the bit index word*32+bit equals the
+// row-major cell index r*16+c (np.argmax / flatnonzero order). A BFS layer is
+// ~9 integer ops per word with no shuffles or votes: horizontal neighbours are
+// in-word shifts (masked at the 16-bit row seam), vertical neighbours are one
+// funnel shift with the adjacent word. 32 environments advance per warp with
+// fully coalesced state loads; divergence (only ~1/3 of env-steps recompute
+// metrics) costs far less than the collective traffic of a lane team.
+#pragma once
+#include <stdint.h>
+
+#include "team.cuh"
+
+namespace lg {
+
+struct SB {
+    uint32_t w[8];
+    __device__ __forceinline__ static SB zero() {
+        SB b;
+#pragma unroll
+        for (int k = 0; k < 8; k++) b.w[k] = 0;
+        return b;
+    }
+    __device__ __forceinline__ bool nz() const {
+        uint32_t x = 0;
+#pragma unroll
+        for (int k = 0; k < 8; k++) x |= w[k];
+        return x != 0;
+    }
+    __device__ __forceinline__ int count() const {
+        int c = 0;
+#pragma unroll
+        for (int k = 0; k < 8; k++) c += __popc(w[k]);
+        return c;
+    }
+    // 16-bit row r (r static after unrolling, or dynamic via a select chain)
+    __device__ __forceinline__ uint32_t row(int r) const {
+        uint32_t x = 0;
+#pragma unroll
+        for (int k = 0; k < 8; k++) x = (k == (r >> 1)) ? w[k] : x;
+        return (r & 1) ? (x >> 16) : (x & 0xFFFFu);
+    }
+};
+
+__device__ __forceinline__ SB operator&(const SB &a, const SB &b) {
+    SB o;
+#pragma unroll
+    for (int k = 0; k < 8; k++) o.w[k] = a.w[k] & b.w[k];
+    return o;
+}
+__device__ __forceinline__ SB operator|(const SB &a, const SB &b) {
+    SB o;
+#pragma unroll
+    for (int k = 0; k < 8; k++) o.w[k] = a.w[k] | b.w[k];
+    return o;
+}
+__device__ __forceinline__ SB andnot(const SB &a, const SB &b) {
+    SB o;
+#pragma unroll
+    for (int k = 0; k < 8; k++) o.w[k] = a.w[k] & ~b.w[k];
+    return o;
+}
+
+__device__ __forceinline__ uint32_t mask16(int n) { return n >= 16 ? 0xFFFFu : ((1u << n) - 1u); }
+
+// active rectangle h x w anchored top-left (apply_shape, grid.py:129-142)
+__device__ __forceinline__ SB rect_sb(int h, int w) {
+    SB b;
+    uint32_t m = mask16(w);
+#pragma unroll
+    for (int k = 0; k < 8; k++) b.w[k] = ((2 * k < h) ? m : 0u) | ((2 * k + 1 < h) ? (m << 16) : 0u);
+    return b;
+}
+
+__device__ __forceinline__ SB dilate_sb(const SB &f) {
+    SB o;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        uint32_t x = f.w[k];
+        uint32_t up = __funnelshift_l(k > 0 ? f.w[k - 1] : 0u, x, 16);  // row above
+        uint32_t dn = __funnelshift_r(x, k < 7 ? f.w[k + 1] : 0u, 16);  // row below
+        o.w[k] = x | ((x << 1) & 0xFFFEFFFEu) | ((x >> 1) & 0x7FFF7FFFu) | up | dn;
+    }
+    return o;
+}
+
+// Backend of the generic metric code (env_kernels.cuh) for one env per thread.
+struct SoloK {
+    using B = SB;
+    __device__ __forceinline__ int count(const SB &b) const { return b.count(); }
+    __device__ __forceinline__ SB cell(int flat) const {
+        SB b;
+#pragma unroll
+        for (int k = 0; k < 8; k++) b.w[k] = (k == (flat >> 5)) ? (1u << (flat & 31)) : 0u;
+        return b;
+    }
+    __device__ int kth(const SB &m, int kk) const {
+        int res = 0;
+        bool found = false;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            int c = __popc(m.w[k]);
+            if (!found && kk < c) {
+                uint32_t x = m.w[k];
+                for (int i = 0; i < kk; i++) x &= x - 1;
+                res = k * 32 + __ffs((int)x) - 1;
+                found = true;
+            }
+            kk -= c;
+        }
+        return res;
+    }
+    __device__ int lowest(const SB &m) const {
+        int res = 0;
+        bool found = false;
+#pragma unroll
+        for (int k = 0; k < 8; k++)
+            if (!found && m.w[k]) {
+                res = k * 32 + __ffs((int)m.w[k]) - 1;
+                found = true;
+            }
+        return res;
+    }
+    __device__ int bfs_last(SB &f, const SB &pass) const {
+        SB vis = f;
+        int depth = 0;
+        while (true) {
+            SB nx = andnot(dilate_sb(f) & pass, vis);
+            if (!nx.nz()) return depth;
+            vis = vis | nx;
+            f = nx;
+            depth++;
+        }
+    }
+    template <bool ENDPOINT>
+    __device__ void touch(SB f, const SB &pass, const SB &ta, const SB &tb, bool want_b, int &da,
+                          int &db) const {
+        da = -1;
+        db = -1;
+        bool need_a = ta.nz();
+        bool need_b = want_b && tb.nz();
+        SB vis = f;
+        int depth = 0;
+        while (need_a || need_b) {
+            SB d = dilate_sb(f);
+            if (ENDPOINT) {
+                if (need_a && (d & ta).nz()) {
+                    da = depth + 1;
+                    need_a = false;
+                }
+                if (need_b && (d & tb).nz()) {
+                    db = depth + 1;
+                    need_b = false;
+                }
+            } else {
+                if (need_a && (f & ta).nz()) {
+                    da = depth;
+                    need_a = false;
+                }
+                if (need_b && (f & tb).nz()) {
+                    db = depth;
+                    need_b = false;
+                }
+            }
+            if (!need_a && !need_b) break;
+            SB nx = andnot(d & pass, vis);
+            if (!nx.nz()) break;
+            vis = vis | nx;
+            f = nx;
+            depth++;
+        }
+    }
+    // count_regions (pathfind.py:116-130) as a sequential run union-find:
+    // nodes are runs of a row (id = row*8 + run index); a run touching a run
+    // of the previous row is united with it; regions = runs - merges.
+    __device__ int regions(const SB &pass, void *scratch) const {
+        uint8_t *par = reinterpret_cast<uint8_t *>(scratch);
+        int runs = 0, merges = 0;
+        uint32_t prevR = 0, prevS = 0;
+#pragma unroll
+        for (int r = 0; r < 16; r++) {
+            uint32_t R = (r & 1) ? (pass.w[r >> 1] >> 16) : (pass.w[r >> 1] & 0xFFFFu);
+            uint32_t S = R & ~(R << 1);
+            int nr = __popc(S);
+            for (int i = 0; i < nr; i++) par[r * 8 + i] = (uint8_t)(r * 8 + i);
+            runs += nr;
+            uint32_t C = R & prevR;
+            uint32_t CS = C & ~(C << 1);
+            while (CS) {
+                int c = __ffs((int)CS) - 1;
+                CS &= CS - 1;
+                uint32_t upto = (2u << c) - 1u;
+                int a = r * 8 + __popc(S & upto) - 1;
+                int b = (r - 1) * 8 + __popc(prevS & upto) - 1;
+                while (par[a] != a) {
+                    par[a] = par[par[a]];
+                    a = par[a];
+                }
+                while (par[b] != b) {
+                    par[b] = par[par[b]];
+                    b = par[b];
+                }
+                if (a != b) {
+                    if (a < b) par[b] = (uint8_t)a;
+                    else par[a] = (uint8_t)b;
+                    merges++;
+                }
+            }
+            prevR = R;
+            prevS = S;
+        }
+        return runs - merges;
+    }
+};
+
+}  // namespace lg

@@ -1,0 +1,742 @@
+// solo_kernel.cuh -- fused env step, one environment per thread (maps <= 16x16).
+//
+// Warp w of a block owns 32 consecutive environments. Each lane steps its own
+// environment entirely in registers (reference _Core.step, env.py:355-393, with
+// in-kernel auto-reset, env.py:391-392), then streams that environment's 0/1
+// observation planes (build_observation, env.py:186-233) into its slot of the
+// warp's shared-memory bit image as one sequential bit stream (no atomics, no
+// zero fill). After __syncwarp the whole warp expands the 32 images -- whose
+// outputs are contiguous in HBM -- into float32 with coalesced 256-bit
+// streaming stores (STG.E.EF.256): each lane turns 8 bits into 8 floats per
+// store. There is no block-wide barrier, so warps of the same SM interleave
+// their step phases with other warps' store phases.
+#pragma once
+#include "env_kernels.cuh"
+#include "solo.cuh"
+
+namespace lg {
+
+template <int DOM>
+struct SoloEnv {
+    SB pl[Dom<DOM>::NPL];
+    SB frz;
+    int h, w, pr, pc, pos_idx, order_len, changes;
+    long long t, max_steps;
+    int val[8], lo[8], hi[8];
+    int unr;
+    double prev_loss, ep_reward, ep_start_loss;
+    Pcg g;
+    long long mseed;
+};
+
+template <int DOM>
+__device__ __forceinline__ uint32_t *solo_rows(const Params &p, long long env) {
+    return reinterpret_cast<uint32_t *>(p.rows) + (size_t)env * (Dom<DOM>::NPL + 1) * 8;
+}
+
+template <int DOM>
+__device__ void solo_load(const Params &p, long long env, SoloEnv<DOM> &e) {
+    constexpr int NPL = Dom<DOM>::NPL;
+    const uint4 *rw = reinterpret_cast<const uint4 *>(solo_rows<DOM>(p, env));
+#pragma unroll
+    for (int q = 0; q <= NPL; q++) {
+        uint4 a = rw[2 * q], b = rw[2 * q + 1];
+        SB &d = q < NPL ? e.pl[q] : e.frz;
+        d.w[0] = a.x; d.w[1] = a.y; d.w[2] = a.z; d.w[3] = a.w;
+        d.w[4] = b.x; d.w[5] = b.y; d.w[6] = b.z; d.w[7] = b.w;
+    }
+    Hot hv = p.hot[env];
+    e.h = hv.geo & 255;
+    e.w = (hv.geo >> 8) & 255;
+    e.pr = (hv.geo >> 16) & 255;
+    e.pc = hv.geo >> 24;
+    e.pos_idx = hv.pos_idx;
+    e.order_len = hv.order_len;
+    e.changes = hv.changes;
+    e.t = hv.t;
+    e.max_steps = hv.max_steps;
+    const int4 *mv = reinterpret_cast<const int4 *>(p.mv + env * 24);
+    int4 a = mv[0], b = mv[1], c = mv[2], d = mv[3], f = mv[4], h2 = mv[5];
+    e.val[0] = a.x; e.val[1] = a.y; e.val[2] = a.z; e.val[3] = a.w;
+    e.val[4] = b.x; e.val[5] = b.y; e.val[6] = b.z; e.unr = b.w; e.val[7] = 0;
+    e.lo[0] = c.x; e.lo[1] = c.y; e.lo[2] = c.z; e.lo[3] = c.w;
+    e.lo[4] = d.x; e.lo[5] = d.y; e.lo[6] = d.z; e.lo[7] = d.w;
+    e.hi[0] = f.x; e.hi[1] = f.y; e.hi[2] = f.z; e.hi[3] = f.w;
+    e.hi[4] = h2.x; e.hi[5] = h2.y; e.hi[6] = h2.z; e.hi[7] = h2.w;
+    const double2 *lv = reinterpret_cast<const double2 *>(p.lossv + env * 4);
+    double2 l0 = lv[0], l1 = lv[1];
+    e.prev_loss = l0.x;
+    e.ep_reward = l0.y;
+    e.ep_start_loss = l1.x;
+    ulonglong2 s = p.rs[env], inc = p.ri[env];
+    uint2 bf = p.rb[env];
+    e.g.s = ((u128)s.x << 64) | s.y;
+    e.g.inc = ((u128)inc.x << 64) | inc.y;
+    e.g.has = bf.x;
+    e.g.u = bf.y;
+    e.mseed = p.det ? p.mseed[env] : 0;
+}
+
+template <int DOM>
+__device__ void solo_store(const Params &p, long long env, const SoloEnv<DOM> &e, bool rows_dirty,
+                           bool planes_dirty, bool metrics_dirty, bool rng_dirty) {
+    constexpr int NPL = Dom<DOM>::NPL;
+    if (rows_dirty || planes_dirty) {
+        uint4 *rw = reinterpret_cast<uint4 *>(solo_rows<DOM>(p, env));
+#pragma unroll
+        for (int q = 0; q <= NPL; q++) {
+            if (q == NPL && !rows_dirty) break;
+            const SB &d = q < NPL ? e.pl[q] : e.frz;
+            rw[2 * q] = make_uint4(d.w[0], d.w[1], d.w[2], d.w[3]);
+            rw[2 * q + 1] = make_uint4(d.w[4], d.w[5], d.w[6], d.w[7]);
+        }
+    }
+    Hot hv;
+    hv.geo = (uint32_t)e.h | ((uint32_t)e.w << 8) | ((uint32_t)e.pr << 16) | ((uint32_t)e.pc << 24);
+    hv.pos_idx = e.pos_idx;
+    hv.order_len = e.order_len;
+    hv.changes = e.changes;
+    hv.t = e.t;
+    hv.max_steps = e.max_steps;
+    p.hot[env] = hv;
+    if (metrics_dirty) {
+        int4 *mv = reinterpret_cast<int4 *>(p.mv + env * 24);
+        mv[0] = make_int4(e.val[0], e.val[1], e.val[2], e.val[3]);
+        mv[1] = make_int4(e.val[4], e.val[5], e.val[6], e.unr);
+        mv[2] = make_int4(e.lo[0], e.lo[1], e.lo[2], e.lo[3]);
+        mv[3] = make_int4(e.lo[4], e.lo[5], e.lo[6], e.lo[7]);
+        mv[4] = make_int4(e.hi[0], e.hi[1], e.hi[2], e.hi[3]);
+        mv[5] = make_int4(e.hi[4], e.hi[5], e.hi[6], e.hi[7]);
+    }
+    double2 *lv = reinterpret_cast<double2 *>(p.lossv + env * 4);
+    lv[0] = make_double2(e.prev_loss, e.ep_reward);
+    if (metrics_dirty) lv[1] = make_double2(e.ep_start_loss, 0.0);
+    if (rng_dirty) {
+        p.rs[env] = make_ulonglong2((unsigned long long)(e.g.s >> 64), (unsigned long long)e.g.s);
+        p.rb[env] = make_uint2(e.g.has, e.g.u);
+        if (p.det) p.mseed[env] = e.mseed;
+    }
+}
+
+template <int DOM>
+__device__ void solo_recompute(const Params &p, SoloEnv<DOM> &e, void *uf, bool reset) {
+    SoloK k;
+    SB act = rect_sb(e.h, e.w);
+    if (p.det) {  // _metric_rngs (env.py:327-330)
+        Pcg mg;
+        seedseq_pcg((uint64_t)e.mseed, false, 0, mg);
+        compute_metrics<SoloK, DOM>(k, e.pl, act, mg, uf, e.val, e.unr);
+    } else {
+        compute_metrics<SoloK, DOM>(k, e.pl, act, e.g, uf, e.val, e.unr);
+    }
+    double l = loss_of<DOM>(p, e.val, e.unr, e.lo, e.hi);
+    e.prev_loss = l;
+    if (reset) {
+        e.ep_reward = 0.0;
+        e.ep_start_loss = l;
+    }
+}
+
+// first editable cell (row-major r*16+c) in boustrophedon order at or after row r0; -1 if none
+__device__ __forceinline__ int solo_serp_first(const SB &ed, int r0) {
+    int res = -1;
+#pragma unroll
+    for (int r = 15; r >= 0; r--) {
+        uint32_t x = (r & 1) ? (ed.w[r >> 1] >> 16) : (ed.w[r >> 1] & 0xFFFFu);
+        if (r >= r0 && x) res = r * 16 + ((r & 1) ? (31 - __clz((int)x)) : (__ffs((int)x) - 1));
+    }
+    return res;
+}
+
+__device__ __forceinline__ int solo_serp_next(const SB &ed, int r, int c) {
+    uint32_t x = ed.row(r);
+    if (r & 1) {
+        x &= (1u << c) - 1u;
+        if (x) return r * 16 + 31 - __clz((int)x);
+    } else {
+        x &= ~((2u << c) - 1u);
+        if (x) return r * 16 + __ffs((int)x) - 1;
+    }
+    return solo_serp_first(ed, r + 1);
+}
+
+// set tile id `tile` (0..N-1) at (r, c) in the stored planes
+template <int DOM>
+__device__ __forceinline__ void solo_set_tile(SoloEnv<DOM> &e, int r, int c, int tile) {
+    constexpr int NPL = Dom<DOM>::NPL;
+    const int wi = r >> 1;
+    const uint32_t bit = 1u << ((r & 1) * 16 + c);
+#pragma unroll
+    for (int q = 0; q < NPL; q++)
+#pragma unroll
+        for (int k = 0; k < 8; k++)
+            if (k == wi) e.pl[q].w[k] = (e.pl[q].w[k] & ~bit) | (q == tile - 1 ? bit : 0u);
+}
+
+template <int DOM>
+__device__ void solo_reset(const Params &p, SoloEnv<DOM> &e, void *uf) {
+    constexpr int N = Dom<DOM>::N, NPL = Dom<DOM>::NPL, M = Dom<DOM>::M;
+    Pcg &g = e.g;
+    int h = p.H, w = p.W;
+    if (p.randomize) {  // sample_shape: width then height (grid.py:124-125)
+        w = (int)pcg_integers(g, 3, p.W + 1);
+        h = (int)pcg_integers(g, 3, p.H + 1);
+    }
+    e.h = h;
+    e.w = w;
+    SB act = rect_sb(h, w);
+#pragma unroll
+    for (int q = 0; q < NPL; q++) e.pl[q] = SB::zero();
+    e.frz = andnot(rect_sb(p.H, p.W), act);
+    if (p.weighted) {  // init_random: choice(n_tiles, (h, w), p), row-major (grid.py:169-191)
+#pragma unroll
+        for (int r = 0; r < 16; r++) {
+            if (r < h) {
+                uint32_t rowbits[NPL];
+#pragma unroll
+                for (int q = 0; q < NPL; q++) rowbits[q] = 0;
+                for (int c = 0; c < w; c++) {
+                    double u = pcg_double(g);
+                    int idx = 0;
+#pragma unroll
+                    for (int q = 0; q < N; q++) idx += (p.cdf[q] <= u) ? 1 : 0;  // searchsorted right
+                    idx = idx < N - 1 ? idx : N - 1;
+#pragma unroll
+                    for (int q = 0; q < NPL; q++) rowbits[q] |= (q == idx - 1) ? (1u << c) : 0u;
+                }
+#pragma unroll
+                for (int q = 0; q < NPL; q++) e.pl[q].w[r >> 1] |= rowbits[q] << ((r & 1) * 16);
+            }
+        }
+    }
+    if (p.n_pins > 0) {  // place_pinpoints: Floyd over the h*w free cells (grid.py:194-225)
+        int pop = h * w, k = p.n_pins;
+        if (pop < k) {
+            atomicOr(p.err, (unsigned)FLAG_PINPOINTS);
+        } else {
+            int picks[16];
+            for (int j = pop - k; j < pop; j++) {
+                int val = (int)pcg_bounded(g, (uint64_t)j);
+                bool seen = false;
+                for (int i = 0; i < j - (pop - k); i++) seen |= picks[i] == val;
+                picks[j - (pop - k)] = seen ? j : val;
+            }
+            for (int i = k - 1; i > 0; i--) {
+                int j = (int)pcg_bounded(g, (uint64_t)i);
+                int tmp = picks[i];
+                picks[i] = picks[j];
+                picks[j] = tmp;
+            }
+            for (int i = 0; i < k; i++) {
+                int r = picks[i] / w, c = picks[i] - (picks[i] / w) * w;
+                solo_set_tile<DOM>(e, r, c, p.pins[i]);
+                const int wi = r >> 1;
+                const uint32_t bit = 1u << ((r & 1) * 16 + c);
+#pragma unroll
+                for (int kk = 0; kk < 8; kk++)
+                    if (kk == wi) e.frz.w[kk] |= bit;
+            }
+        }
+    }
+    int cap = h * w;  // default_targets + sample_control_targets (problems.py:48-90)
+#pragma unroll
+    for (int m = 0; m < M; m++) {
+        int lo = 1, hi = 1;
+        if (m == 0) lo = hi = cap;
+        if (DOM == 2 && m == 5) {
+            lo = 2;
+            hi = 5;
+        }
+        if (DOM == 2 && m == 6) {
+            lo = 4;
+            hi = cap;
+        }
+        for (int j = 0; j < p.n_ctrl; j++)
+            if (p.ctrl[j] == m) lo = hi = (int)pcg_integers(g, 0, (int64_t)cap + 1);
+        e.lo[m] = lo;
+        e.hi[m] = hi;
+    }
+    if (p.det) e.mseed = (long long)pcg_bounded(g, 0x7FFFFFFFFFFFFFFFULL);  // env.py:302-303
+    SB ed = andnot(act, e.frz);  // _install_row (env.py:307-325)
+    e.order_len = ed.count();
+    int first = solo_serp_first(ed, 0);
+    if (first < 0) {
+        atomicOr(p.err, (unsigned)FLAG_NO_EDITABLE);
+        first = 0;
+    }
+    e.pr = first >> 4;
+    e.pc = first & 15;
+    e.pos_idx = 0;
+    e.t = 0;
+    e.changes = 0;
+    e.max_steps = p.max_steps > 0 ? p.max_steps : 3LL * cap;
+    solo_recompute<DOM>(p, e, uf, true);
+}
+
+// Sequential bit writer into one env's image slot.
+struct BitW {
+    uint32_t *dst;
+    uint32_t widx;
+    uint64_t acc;
+    int n;
+    __device__ __forceinline__ void put32(uint32_t v, int cnt) {  // cnt <= 32, v < 2^cnt
+        acc |= (uint64_t)v << n;
+        n += cnt;
+        if (n >= 32) {
+            dst[widx++] = (uint32_t)acc;
+            acc >>= 32;
+            n -= 32;
+        }
+    }
+    __device__ __forceinline__ void put(uint64_t v, int cnt) {  // cnt <= 64
+        if (cnt > 32) {
+            put32((uint32_t)v, 32);
+            put32((uint32_t)(v >> 32), cnt - 32);
+        } else {
+            put32((uint32_t)v, cnt);
+        }
+    }
+    __device__ __forceinline__ void fill(bool one, int cnt) {
+        while (cnt > 0) {
+            int take = cnt < 32 ? cnt : 32;
+            put32(one ? (take == 32 ? 0xFFFFFFFFu : ((1u << take) - 1u)) : 0u, take);
+            cnt -= take;
+        }
+    }
+    __device__ __forceinline__ void flush() {
+        if (n > 0) dst[widx++] = (uint32_t)acc;
+        dst[widx++] = 0u;  // pad word read by the 2-word funnel shift
+    }
+};
+
+template <int DOM>
+__device__ void solo_render(const Params &p, const SoloEnv<DOM> &e, uint32_t *slot) {
+    constexpr int N = Dom<DOM>::N, NPL = Dom<DOM>::NPL;
+    const int OH = p.OH, OW = p.OW, H = p.H, W = p.W;
+    int r0 = 0, c0 = 0;
+    if (p.rep != REP_WIDE) {
+        r0 = e.pr - p.half;
+        c0 = e.pc - p.half;
+    }
+    const int jlo = c0 < 0 ? -c0 : 0;
+    const int jhi = (W - c0) < OW ? (W - c0) : OW;
+    const uint64_t full = OW >= 64 ? ~0ull : ((1ull << OW) - 1ull);
+    const uint64_t inside = (jhi > jlo ? (jhi >= 64 ? ~0ull : ((1ull << jhi) - 1ull)) : 0ull) &
+                            ~((1ull << jlo) - 1ull);
+    int before = -r0;
+    before = before < 0 ? 0 : (before > OH ? OH : before);
+    int g_lo = r0 > 0 ? r0 : 0, g_hi = (r0 + OH) < H ? (r0 + OH) : H;
+    int n_in = g_hi > g_lo ? g_hi - g_lo : 0;
+    int after = OH - before - n_in;
+    BitW bw{slot, 0, 0, 0};
+    const uint32_t wm = mask16(W), am = mask16(e.w);
+#pragma unroll
+    for (int pl = 0; pl < N + 2; pl++) {
+        const bool fill = pl >= N;  // border and frozen planes read 1 outside the max grid
+        bw.fill(fill, before * OW);
+#pragma unroll
+        for (int gr = 0; gr < 16; gr++) {
+            int i = gr - r0;
+            if (gr < H && i >= 0 && i < OH) {
+                uint32_t act = gr < e.h ? am : 0u;
+                uint32_t m;
+                if (pl == 0) {
+                    uint32_t any = 0;
+#pragma unroll
+                    for (int q = 0; q < NPL; q++) any |= (gr & 1) ? (e.pl[q].w[gr >> 1] >> 16) : e.pl[q].w[gr >> 1];
+                    m = act & ~any;
+                } else if (pl < N) {
+                    m = ((gr & 1) ? (e.pl[pl - 1].w[gr >> 1] >> 16) : e.pl[pl - 1].w[gr >> 1]) & 0xFFFFu;
+                } else if (pl == N) {
+                    m = ~act & wm;
+                } else {
+                    m = ((gr & 1) ? (e.frz.w[gr >> 1] >> 16) : e.frz.w[gr >> 1]) & 0xFFFFu;
+                }
+                uint64_t win = c0 >= 0 ? ((uint64_t)m >> c0) : ((uint64_t)m << (-c0));
+                win = (win & inside) | (fill ? (full & ~inside) : 0ull);
+                bw.put(win, OW);
+            }
+        }
+        bw.fill(fill, after * OW);
+    }
+    bw.flush();
+    // control planes: (value - (lo+hi)/2) / cap, float64 -> float32 (env.py:224-232)
+    float *ctrl = reinterpret_cast<float *>(slot + p.img_words);
+    for (int j = 0; j < p.n_ctrl; j++) {
+        int m = p.ctrl[j];
+        int vm = 0, lm = 0, hm = 0;
+#pragma unroll
+        for (int q = 0; q < 8; q++)
+            if (q == m) {
+                vm = e.val[q];
+                lm = e.lo[q];
+                hm = e.hi[q];
+            }
+        double tgt = __ddiv_rn(__dadd_rn((double)lm, (double)hm), 2.0);
+        ctrl[j] = __double2float_rn(__ddiv_rn(__dsub_rn((double)vm, tgt), (double)(e.h * e.w)));
+    }
+}
+
+__device__ __forceinline__ float solo_elem(const Params &p, const uint32_t *wimg, uint32_t el, uint32_t le) {
+    const uint32_t *slot = wimg + (size_t)el * p.env_smem;
+    if (le < p.PB) return ((slot[le >> 5] >> (le & 31)) & 1u) ? 1.0f : 0.0f;
+    return reinterpret_cast<const float *>(slot + p.img_words)[fdiv(p.divOO, le - p.PB)];
+}
+
+__device__ __forceinline__ void st_cs_v8(float *ptr, const float *v) {
+    asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(ptr), "f"(v[0]), "f"(v[1]),
+                 "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                 : "memory");
+}
+
+// Expand the warp's 32 images to float32. VEC = 8 (32-byte stores) or 4.
+template <int VEC>
+__device__ void solo_write_warp(const Params &p, const uint32_t *wimg, long long env0, int nenv, int lane) {
+    float *out = p.obs + (size_t)env0 * p.PE;
+    const uint32_t total = (uint32_t)nenv * p.PE;
+    const uint32_t nv = total / VEC;
+    uint32_t e = (uint32_t)lane * VEC;
+    uint32_t el = fdiv(p.divPE, e);
+    uint32_t le = e - el * p.PE;
+    for (uint32_t q = lane; q < nv; q += 32) {
+        float v[VEC];
+        if (le + (VEC - 1) < p.PB) {
+            const uint32_t *slot = wimg + (size_t)el * p.env_smem;
+            uint32_t wi = le >> 5;
+            uint32_t x = __funnelshift_r(slot[wi], slot[wi + 1], le & 31);
+#pragma unroll
+            for (int k = 0; k < VEC; k++) v[k] = ((x >> k) & 1u) ? 1.0f : 0.0f;
+        } else {
+#pragma unroll
+            for (int k = 0; k < VEC; k++) {
+                uint32_t l2 = le + k, e2 = el;
+                if (l2 >= p.PE) {
+                    l2 -= p.PE;
+                    e2++;
+                }
+                v[k] = solo_elem(p, wimg, e2, l2);
+            }
+        }
+        if constexpr (VEC == 8) {
+            st_cs_v8(out + (size_t)q * 8, v);
+        } else {
+            __stcs(reinterpret_cast<float4 *>(out) + q, make_float4(v[0], v[1], v[2], v[3]));
+        }
+        le += 32 * VEC;
+        while (le >= p.PE) {
+            le -= p.PE;
+            el++;
+        }
+    }
+    for (uint32_t t = nv * VEC + lane; t < total; t += 32) {
+        uint32_t e2 = fdiv(p.divPE, t);
+        out[t] = solo_elem(p, wimg, e2, t - e2 * p.PE);
+    }
+}
+
+template <int DOM>
+__global__ void __launch_bounds__(64) env_solo_kernel(const Params p, int mode) {
+    extern __shared__ __align__(16) uint32_t smem_w[];
+    constexpr int N = Dom<DOM>::N;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long env = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long env0 = env - lane;
+    uint32_t *wimg = smem_w + (size_t)warp * 32 * p.env_smem;
+    uint32_t *slot = wimg + (size_t)lane * p.env_smem;
+    if (env < p.B) {
+        SoloEnv<DOM> e;
+        solo_load<DOM>(p, env, e);
+        bool rows_dirty = false, planes_dirty = false, metrics_dirty = false, rng_dirty = false;
+        if (mode == MODE_STEP) {
+            long long a = p.actions[env];
+            bool ok = a >= 0 && a < p.n_actions;
+            if (!ok) atomicOr(p.err, (unsigned)FLAG_BAD_ACTION);
+            int r = e.pr, c = e.pc, tile = -1;
+            if (p.rep == REP_NARROW) {
+                if (ok && a != 0) tile = (int)a - 1;
+            } else if (p.rep == REP_TURTLE) {
+                if (ok && a < 4) {
+                    if (a == 0) r = r > 0 ? r - 1 : 0;
+                    else if (a == 1) r = r < e.h - 1 ? r + 1 : e.h - 1;
+                    else if (a == 2) c = c > 0 ? c - 1 : 0;
+                    else c = c < e.w - 1 ? c + 1 : e.w - 1;
+                    e.pr = r;
+                    e.pc = c;
+                } else if (ok) {
+                    tile = (int)a - 4;
+                }
+            } else if (ok) {  // wide
+                int cell = (int)(a / N);
+                tile = (int)(a - (long long)cell * N);
+                r = cell / p.W;
+                c = cell - r * p.W;
+            }
+            bool wrote = false;
+            if (tile >= 0) {
+                const uint32_t sh = (r & 1) * 16 + c;
+                const int wi = r >> 1;
+                bool act = r < e.h && c < e.w;
+                int cur = act ? 0 : N;
+                uint32_t fz = 0;
+#pragma unroll
+                for (int k = 0; k < 8; k++) {
+                    if (k == wi) {
+#pragma unroll
+                        for (int q = 0; q < Dom<DOM>::NPL; q++)
+                            if ((e.pl[q].w[k] >> sh) & 1u) cur = q + 1;
+                        fz = (e.frz.w[k] >> sh) & 1u;
+                    }
+                }
+                bool editable = act && !fz;
+                wrote = tile != cur && (p.rep == REP_NARROW || editable);
+            }
+            double reward = 0.0;
+            if (wrote) {
+                solo_set_tile<DOM>(e, r, c, tile);
+                planes_dirty = true;
+                e.changes += 1;
+                double before = e.prev_loss;
+                solo_recompute<DOM>(p, e, slot, false);
+                reward = __dsub_rn(before, e.prev_loss);
+                metrics_dirty = true;
+                rng_dirty = true;
+            }
+            e.ep_reward = __dadd_rn(e.ep_reward, reward);
+            if (p.rep == REP_NARROW) {  // pos_idx = (pos_idx + 1) % order_len
+                SB ed = andnot(rect_sb(e.h, e.w), e.frz);
+                int nidx = e.pos_idx + 1, nxt;
+                if (nidx >= e.order_len) {
+                    nidx = 0;
+                    nxt = solo_serp_first(ed, 0);
+                } else {
+                    nxt = solo_serp_next(ed, e.pr, e.pc);
+                }
+                e.pos_idx = nidx;
+                e.pr = nxt >> 4;
+                e.pc = nxt & 15;
+            }
+            e.t += 1;
+            bool done = e.t >= e.max_steps;
+            if (p.budget > 0) done |= e.changes >= p.budget;
+            p.reward[env] = reward;
+            p.done[env] = done;
+            if (p.terminal) p.terminal[env] = done;
+            if (p.ep_rew) p.ep_rew[env] = done ? e.ep_reward : 0.0;
+            if (p.ep_len) p.ep_len[env] = done ? e.t : 0;
+            if (p.ep_start) p.ep_start[env] = done ? e.ep_start_loss : 0.0;
+            if (p.fin_loss) p.fin_loss[env] = done ? e.prev_loss : 0.0;
+            if (done && p.stats) {
+                atomicAdd(p.stats + 0, 1.0);
+                atomicAdd(p.stats + 1, e.ep_reward);
+                atomicAdd(p.stats + 2, (double)e.t);
+                atomicAdd(p.stats + 3, e.ep_start_loss);
+                atomicAdd(p.stats + 4, e.prev_loss);
+            }
+            if (done) {
+                solo_reset<DOM>(p, e, slot);
+                rows_dirty = metrics_dirty = rng_dirty = true;
+            }
+        } else if (mode == MODE_RESET) {
+            if (!p.reset_mask || p.reset_mask[env]) {
+                solo_reset<DOM>(p, e, slot);
+                rows_dirty = metrics_dirty = rng_dirty = true;
+            }
+        }
+        if (mode != MODE_OBSERVE) solo_store<DOM>(p, env, e, rows_dirty, planes_dirty, metrics_dirty, rng_dirty);
+        if (p.obs) solo_render<DOM>(p, e, slot);
+    }
+    if (p.obs) {
+        __syncwarp();
+        long long rem = (long long)p.B - env0;
+        int nenv = rem < 32 ? (int)rem : 32;
+        if (nenv > 0) {
+            if ((reinterpret_cast<uintptr_t>(p.obs) & 31) == 0)
+                solo_write_warp<8>(p, wimg, env0, nenv, lane);
+            else
+                solo_write_warp<4>(p, wimg, env0, nenv, lane);
+        }
+    }
+}
+
+// ---- state export / import / metrics for the solo layout -------------------
+
+template <int DOM>
+__global__ void solo_export_kernel(const Params p, lg_state dst) {
+    constexpr int N = Dom<DOM>::N, NPL = Dom<DOM>::NPL, M = Dom<DOM>::M;
+    const long long env = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (env >= p.B) return;
+    SoloEnv<DOM> e;
+    solo_load<DOM>(p, env, e);
+    const int H = p.H, W = p.W, HW = H * W;
+    SB act = rect_sb(e.h, e.w);
+    SB ed = andnot(act, e.frz);
+    int32_t *ord = dst.order + (size_t)env * HW;
+    int n = 0;
+    for (int r = 0; r < H; r++) {
+        uint32_t arow = act.row(r), frow = e.frz.row(r), erow = ed.row(r);
+        uint32_t prow[NPL];
+#pragma unroll
+        for (int q = 0; q < NPL; q++) prow[q] = e.pl[q].row(r);
+        for (int c = 0; c < W; c++) {
+            bool a = (arow >> c) & 1u;
+            int tile = a ? 0 : N;
+#pragma unroll
+            for (int q = 0; q < NPL; q++)
+                if ((prow[q] >> c) & 1u) tile = q + 1;
+            size_t o = ((size_t)env * H + r) * W + c;
+            dst.tiles[o] = (uint8_t)tile;
+            dst.active[o] = a;
+            dst.frozen[o] = (frow >> c) & 1u;
+        }
+        for (int k = 0; k < W; k++) {
+            int c = (r & 1) ? W - 1 - k : k;
+            if ((erow >> c) & 1u) ord[n++] = r * W + c;
+        }
+    }
+    for (int i = n; i < HW; i++) ord[i] = -1;
+    dst.shape_hw[2 * env] = e.h;
+    dst.shape_hw[2 * env + 1] = e.w;
+    dst.order_len[env] = e.order_len;
+    dst.pos_idx[env] = e.pos_idx;
+    dst.pos[2 * env] = e.pr;
+    dst.pos[2 * env + 1] = e.pc;
+    dst.t[env] = e.t;
+    dst.changes[env] = e.changes;
+    dst.max_steps[env] = e.max_steps;
+    for (int m = 0; m < M; m++) {
+        dst.lo[(size_t)m * p.B + env] = e.lo[m];
+        dst.hi[(size_t)m * p.B + env] = e.hi[m];
+        dst.values[(size_t)m * p.B + env] = e.val[m];
+        dst.unreach[(size_t)m * p.B + env] = (e.unr >> m) & 1;
+    }
+    dst.prev_loss[env] = e.prev_loss;
+    dst.ep_reward[env] = e.ep_reward;
+    dst.ep_start_loss[env] = e.ep_start_loss;
+    dst.metric_seeds[env] = p.mseed[env];
+    uint64_t *rg = dst.rng + 6 * env;
+    rg[0] = (uint64_t)(e.g.s >> 64);
+    rg[1] = (uint64_t)e.g.s;
+    rg[2] = (uint64_t)(e.g.inc >> 64);
+    rg[3] = (uint64_t)e.g.inc;
+    rg[4] = e.g.has;
+    rg[5] = e.g.u;
+}
+
+template <int DOM>
+__global__ void solo_import_kernel(const Params p, lg_state src) {
+    constexpr int NPL = Dom<DOM>::NPL, M = Dom<DOM>::M;
+    const long long env = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (env >= p.B) return;
+    const int H = p.H, W = p.W;
+    uint32_t wq[NPL + 1][8];
+#pragma unroll
+    for (int q = 0; q <= NPL; q++)
+#pragma unroll
+        for (int k = 0; k < 8; k++) wq[q][k] = 0;
+    for (int r = 0; r < H; r++)
+        for (int c = 0; c < W; c++) {
+            size_t o = ((size_t)env * H + r) * W + c;
+            int tile = src.tiles[o];
+            uint32_t bit = 1u << ((r & 1) * 16 + c);
+            bool a = src.active[o] != 0;
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                if (k != (r >> 1)) continue;
+#pragma unroll
+                for (int q = 0; q < NPL; q++)
+                    if (a && tile == q + 1) wq[q][k] |= bit;
+                if (src.frozen[o]) wq[NPL][k] |= bit;
+            }
+        }
+    uint32_t *rw = solo_rows<DOM>(p, env);
+#pragma unroll
+    for (int q = 0; q <= NPL; q++)
+#pragma unroll
+        for (int k = 0; k < 8; k++) rw[q * 8 + k] = wq[q][k];
+    Hot hv;
+    uint32_t h = (uint32_t)src.shape_hw[2 * env], w = (uint32_t)src.shape_hw[2 * env + 1];
+    uint32_t pr = (uint32_t)src.pos[2 * env], pc = (uint32_t)src.pos[2 * env + 1];
+    hv.geo = h | (w << 8) | (pr << 16) | (pc << 24);
+    hv.pos_idx = (int32_t)src.pos_idx[env];
+    hv.order_len = (int32_t)src.order_len[env];
+    hv.changes = (int32_t)src.changes[env];
+    hv.t = src.t[env];
+    hv.max_steps = src.max_steps[env];
+    p.hot[env] = hv;
+    int *mv = p.mv + env * 24;
+    int unr = 0;
+    for (int m = 0; m < 8; m++) {
+        bool in = m < M;
+        mv[m] = in ? (int)src.values[(size_t)m * p.B + env] : 0;
+        mv[8 + m] = in ? (int)src.lo[(size_t)m * p.B + env] : 0;
+        mv[16 + m] = in ? (int)src.hi[(size_t)m * p.B + env] : 0;
+        if (in && src.unreach[(size_t)m * p.B + env]) unr |= 1 << m;
+    }
+    mv[7] = unr;
+    double *lv = p.lossv + env * 4;
+    lv[0] = src.prev_loss[env];
+    lv[1] = src.ep_reward[env];
+    lv[2] = src.ep_start_loss[env];
+    lv[3] = 0.0;
+    p.mseed[env] = src.metric_seeds[env];
+    const uint64_t *rg = src.rng + 6 * env;
+    p.rs[env] = make_ulonglong2(rg[0], rg[1]);
+    p.ri[env] = make_ulonglong2(rg[2], rg[3]);
+    p.rb[env] = make_uint2((unsigned)rg[4], (unsigned)rg[5]);
+}
+
+// compute_metrics_batch on raw stacks for maps <= 16x16, one grid per thread.
+template <int DOM>
+__global__ void __launch_bounds__(128) solo_metrics_kernel(long long n, int H, int W, const uint8_t *tiles,
+                                                           const uint8_t *active, uint64_t *rng,
+                                                           int64_t *values, uint8_t *unreach) {
+    extern __shared__ __align__(16) uint32_t smem_w[];
+    constexpr int NPL = Dom<DOM>::NPL, M = Dom<DOM>::M;
+    const long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= n) return;
+    void *uf = smem_w + threadIdx.x * 33;
+    SB pl[NPL], act = SB::zero();
+#pragma unroll
+    for (int q = 0; q < NPL; q++) pl[q] = SB::zero();
+    for (int r = 0; r < H; r++)
+        for (int c = 0; c < W; c++) {
+            size_t o = ((size_t)b * H + r) * W + c;
+            if (!active[o]) continue;
+            uint32_t bit = 1u << ((r & 1) * 16 + c);
+            int tile = tiles[o];
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                if (k != (r >> 1)) continue;
+                act.w[k] |= bit;
+#pragma unroll
+                for (int q = 0; q < NPL; q++)
+                    if (tile == q + 1) pl[q].w[k] |= bit;
+            }
+        }
+    Pcg g;
+    g.s = g.inc = 0;
+    g.has = g.u = 0;
+    if (rng) {
+        const uint64_t *rg = rng + 6 * b;
+        g.s = ((u128)rg[0] << 64) | rg[1];
+        g.inc = ((u128)rg[2] << 64) | rg[3];
+        g.has = (uint32_t)rg[4];
+        g.u = (uint32_t)rg[5];
+    }
+    int val[8] = {0, 0, 0, 0, 0, 0, 0, 0}, unr = 0;
+    SoloK k;
+    compute_metrics<SoloK, DOM>(k, pl, act, g, uf, val, unr);
+    for (int m = 0; m < M; m++) {
+        values[(size_t)m * n + b] = val[m];
+        unreach[(size_t)m * n + b] = (unr >> m) & 1;
+    }
+    if (rng) {
+        uint64_t *rg = rng + 6 * b;
+        rg[0] = (uint64_t)(g.s >> 64);
+        rg[1] = (uint64_t)g.s;
+        rg[4] = g.has;
+        rg[5] = g.u;
+    }
+}
+
+}  // namespace lg

@@ -34,6 +34,18 @@ def _cmp_state(sd, want, prefix, rep):
     assert np.array_equal(sd["prev_loss"], want[f"{prefix}prev_loss"])
 
 
+SMALL_CASES = ["c1_binary16_narrow_o31", "c2_maze16_turtle_o31", "c3_dungeon16_wide_pins_rand",
+               "dungeon6_c5_like", "maze_ctrl_weights", "binary_ctrl_det_budget"]
+
+
+@pytest.mark.parametrize("name", SMALL_CASES)
+def test_golden_env_case_lane_team_path(name, monkeypatch):
+    """Maps <= 16x16 normally run one env per thread; force the lane-team
+    kernel so both code paths are pinned on the same fixtures."""
+    monkeypatch.setenv("LG_FORCE_TEAM", "1")
+    test_golden_env_case(name)
+
+
 @pytest.mark.parametrize("name", env_case_names())
 def test_golden_env_case(name):
     cfg, z = load_env_case(name)
