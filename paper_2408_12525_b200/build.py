@@ -6,6 +6,7 @@ git-ignored but travels with the repo snapshot to the GPU box.
 """
 from __future__ import annotations
 
+import glob
 import os
 import shutil
 import subprocess
@@ -14,7 +15,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SRC = os.path.join(PKG, "csrc", "pcgrl_b200.cu")
-DEPS = [os.path.join(PKG, "csrc", f) for f in ("pcgrl_b200.cu", "env_kernels.cuh", "team.cuh", "rng.cuh")] + [
+DEPS = sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu")) + glob.glob(os.path.join(PKG, "csrc", "*.cuh"))) + [
     os.path.join(ROOT, "include", "pcgrl_b200.h")]
 LIB = os.path.join(PKG, "libpcgrl_b200.so")
 

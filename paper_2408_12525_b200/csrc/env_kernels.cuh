@@ -97,7 +97,8 @@ struct Params {
     uint32_t PE, PB, OO;  // floats per env, bit-plane elements per env, OH*OW
     FastDiv divPE, divOO;
     int img_words;  // u32 words of one env's bit image (incl. 1 pad word)
-    int env_smem;   // bytes of shared memory per env
+    int env_smem;   // shared memory per env: bytes (team kernel) or 32-bit words (solo)
+    int solo_E;     // solo kernel: envs per block (== blockDim: warp mode)
     int off_ctrl;   // byte offset of the control floats within an env's smem
 };
 

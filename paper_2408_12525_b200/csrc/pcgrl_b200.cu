@@ -336,7 +336,7 @@ static int launch_solo_t(lg_env *e, const Params &p, int mode, cudaStream_t s) {
                                         200 * 1024);
     });
     CU(attr_err);
-    long long grid = (e->B + e->threads - 1) / e->threads;
+    long long grid = (e->B + e->E - 1) / e->E;
     env_solo_kernel<DOM><<<(unsigned)grid, e->threads, e->smem, s>>>(p, mode);
     CU(cudaGetLastError());
     return LG_OK;
@@ -518,14 +518,23 @@ extern "C" int lg_create(const lg_config *cfg, int64_t n_envs, int64_t global_of
         // one env per thread; per-env shared slot (in 32-bit words): bit image +
         // 8 control floats, >= 33 words (union-find scratch), odd stride so the
         // 32 lanes of a warp hit 32 different banks.
-        int slot = p.img_words + 8;
+        int slot = p.img_words + (p.n_ctrl > 0 ? 8 : 0);
         if (slot < 33) slot = 33;
         if (!(slot & 1)) slot++;
         p.env_smem = slot;
-        e->threads = 64;
         e->team = 1;
-        e->E = 64;
-        e->smem = (size_t)64 * slot * 4;
+        if (n_envs >= 148LL * 8 * 64) {  // enough warps: each warp writes its own 32 envs
+            e->threads = 64;
+            e->E = 64;
+        } else {  // small batch: E envs per block, the whole block writes
+            long long per = n_envs / (148 * 4);
+            int E = 8;
+            while (E < 32 && E * 2 <= per) E *= 2;
+            e->E = E;
+            e->threads = 128;
+        }
+        p.solo_E = e->E;
+        e->smem = (size_t)e->E * slot * 4;
         if (e->OW > 64 || e->smem > 200 * 1024) e->geo = pick_geo(17, W);  // too wide: lane teams
     }
     if (e->geo != 1) {

@@ -390,172 +390,197 @@ __device__ __forceinline__ void st_cs_v8(float *ptr, const float *v) {
 }
 
 // Expand the warp's 32 images to float32. VEC = 8 (32-byte stores) or 4.
-template <int VEC>
-__device__ void solo_write_warp(const Params &p, const uint32_t *wimg, long long env0, int nenv, int lane) {
+// Each lane keeps U independent (env, element) cursors so that U stores and
+// their shared-memory reads are in flight per lane (the store's source
+// registers stay locked until the LSU has read them).
+template <int VEC, int U>
+__device__ void solo_write(const Params &p, const uint32_t *wimg, long long env0, int nenv, int lane,
+                           int nthr) {
     float *out = p.obs + (size_t)env0 * p.PE;
     const uint32_t total = (uint32_t)nenv * p.PE;
     const uint32_t nv = total / VEC;
-    uint32_t e = (uint32_t)lane * VEC;
-    uint32_t el = fdiv(p.divPE, e);
-    uint32_t le = e - el * p.PE;
-    for (uint32_t q = lane; q < nv; q += 32) {
-        float v[VEC];
-        if (le + (VEC - 1) < p.PB) {
-            const uint32_t *slot = wimg + (size_t)el * p.env_smem;
-            uint32_t wi = le >> 5;
-            uint32_t x = __funnelshift_r(slot[wi], slot[wi + 1], le & 31);
+    uint32_t el[U], le[U];
 #pragma unroll
-            for (int k = 0; k < VEC; k++) v[k] = ((x >> k) & 1u) ? 1.0f : 0.0f;
-        } else {
+    for (int u = 0; u < U; u++) {
+        uint32_t e = (uint32_t)(lane + nthr * u) * VEC;
+        el[u] = fdiv(p.divPE, e);
+        le[u] = e - el[u] * p.PE;
+    }
+    const uint32_t STEP = (uint32_t)nthr * U * VEC;
+    for (uint32_t q0 = lane; q0 < nv; q0 += nthr * U) {
 #pragma unroll
-            for (int k = 0; k < VEC; k++) {
-                uint32_t l2 = le + k, e2 = el;
-                if (l2 >= p.PE) {
-                    l2 -= p.PE;
-                    e2++;
+        for (int u = 0; u < U; u++) {
+            const uint32_t q = q0 + nthr * u;
+            if (q < nv) {
+                float v[VEC];
+                if (le[u] + (VEC - 1) < p.PB) {
+                    const uint32_t *slot = wimg + (size_t)el[u] * p.env_smem;
+                    uint32_t wi = le[u] >> 5;
+                    uint32_t x = __funnelshift_r(slot[wi], slot[wi + 1], le[u] & 31);
+#pragma unroll
+                    for (int k = 0; k < VEC; k++) v[k] = ((x >> k) & 1u) ? 1.0f : 0.0f;
+                } else {
+#pragma unroll
+                    for (int k = 0; k < VEC; k++) {
+                        uint32_t l2 = le[u] + k, e2 = el[u];
+                        if (l2 >= p.PE) {
+                            l2 -= p.PE;
+                            e2++;
+                        }
+                        v[k] = solo_elem(p, wimg, e2, l2);
+                    }
                 }
-                v[k] = solo_elem(p, wimg, e2, l2);
+                if constexpr (VEC == 8) {
+                    st_cs_v8(out + (size_t)q * 8, v);
+                } else {
+                    __stcs(reinterpret_cast<float4 *>(out) + q, make_float4(v[0], v[1], v[2], v[3]));
+                }
             }
-        }
-        if constexpr (VEC == 8) {
-            st_cs_v8(out + (size_t)q * 8, v);
-        } else {
-            __stcs(reinterpret_cast<float4 *>(out) + q, make_float4(v[0], v[1], v[2], v[3]));
-        }
-        le += 32 * VEC;
-        while (le >= p.PE) {
-            le -= p.PE;
-            el++;
+            uint32_t l = le[u] + STEP;
+            uint32_t k = fdiv(p.divPE, l);
+            el[u] += k;
+            le[u] = l - k * p.PE;
         }
     }
-    for (uint32_t t = nv * VEC + lane; t < total; t += 32) {
+    for (uint32_t t = nv * VEC + lane; t < total; t += nthr) {
         uint32_t e2 = fdiv(p.divPE, t);
         out[t] = solo_elem(p, wimg, e2, t - e2 * p.PE);
     }
 }
 
+// One env, one thread: step / reset / observe, then render its image into `slot`.
 template <int DOM>
-__global__ void __launch_bounds__(64) env_solo_kernel(const Params p, int mode) {
-    extern __shared__ __align__(16) uint32_t smem_w[];
+__device__ __forceinline__ void solo_env(const Params &p, int mode, long long env, uint32_t *slot) {
     constexpr int N = Dom<DOM>::N;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const long long env = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long env0 = env - lane;
-    uint32_t *wimg = smem_w + (size_t)warp * 32 * p.env_smem;
-    uint32_t *slot = wimg + (size_t)lane * p.env_smem;
-    if (env < p.B) {
-        SoloEnv<DOM> e;
-        solo_load<DOM>(p, env, e);
-        bool rows_dirty = false, planes_dirty = false, metrics_dirty = false, rng_dirty = false;
-        if (mode == MODE_STEP) {
-            long long a = p.actions[env];
-            bool ok = a >= 0 && a < p.n_actions;
-            if (!ok) atomicOr(p.err, (unsigned)FLAG_BAD_ACTION);
-            int r = e.pr, c = e.pc, tile = -1;
-            if (p.rep == REP_NARROW) {
-                if (ok && a != 0) tile = (int)a - 1;
-            } else if (p.rep == REP_TURTLE) {
-                if (ok && a < 4) {
-                    if (a == 0) r = r > 0 ? r - 1 : 0;
-                    else if (a == 1) r = r < e.h - 1 ? r + 1 : e.h - 1;
-                    else if (a == 2) c = c > 0 ? c - 1 : 0;
-                    else c = c < e.w - 1 ? c + 1 : e.w - 1;
-                    e.pr = r;
-                    e.pc = c;
-                } else if (ok) {
-                    tile = (int)a - 4;
-                }
-            } else if (ok) {  // wide
-                int cell = (int)(a / N);
-                tile = (int)(a - (long long)cell * N);
-                r = cell / p.W;
-                c = cell - r * p.W;
+    SoloEnv<DOM> e;
+    solo_load<DOM>(p, env, e);
+    bool rows_dirty = false, planes_dirty = false, metrics_dirty = false, rng_dirty = false;
+    if (mode == MODE_STEP) {
+        long long a = p.actions[env];
+        bool ok = a >= 0 && a < p.n_actions;
+        if (!ok) atomicOr(p.err, (unsigned)FLAG_BAD_ACTION);
+        int r = e.pr, c = e.pc, tile = -1;
+        if (p.rep == REP_NARROW) {
+            if (ok && a != 0) tile = (int)a - 1;
+        } else if (p.rep == REP_TURTLE) {
+            if (ok && a < 4) {
+                if (a == 0) r = r > 0 ? r - 1 : 0;
+                else if (a == 1) r = r < e.h - 1 ? r + 1 : e.h - 1;
+                else if (a == 2) c = c > 0 ? c - 1 : 0;
+                else c = c < e.w - 1 ? c + 1 : e.w - 1;
+                e.pr = r;
+                e.pc = c;
+            } else if (ok) {
+                tile = (int)a - 4;
             }
-            bool wrote = false;
-            if (tile >= 0) {
-                const uint32_t sh = (r & 1) * 16 + c;
-                const int wi = r >> 1;
-                bool act = r < e.h && c < e.w;
-                int cur = act ? 0 : N;
-                uint32_t fz = 0;
-#pragma unroll
-                for (int k = 0; k < 8; k++) {
-                    if (k == wi) {
-#pragma unroll
-                        for (int q = 0; q < Dom<DOM>::NPL; q++)
-                            if ((e.pl[q].w[k] >> sh) & 1u) cur = q + 1;
-                        fz = (e.frz.w[k] >> sh) & 1u;
-                    }
-                }
-                bool editable = act && !fz;
-                wrote = tile != cur && (p.rep == REP_NARROW || editable);
-            }
-            double reward = 0.0;
-            if (wrote) {
-                solo_set_tile<DOM>(e, r, c, tile);
-                planes_dirty = true;
-                e.changes += 1;
-                double before = e.prev_loss;
-                solo_recompute<DOM>(p, e, slot, false);
-                reward = __dsub_rn(before, e.prev_loss);
-                metrics_dirty = true;
-                rng_dirty = true;
-            }
-            e.ep_reward = __dadd_rn(e.ep_reward, reward);
-            if (p.rep == REP_NARROW) {  // pos_idx = (pos_idx + 1) % order_len
-                SB ed = andnot(rect_sb(e.h, e.w), e.frz);
-                int nidx = e.pos_idx + 1, nxt;
-                if (nidx >= e.order_len) {
-                    nidx = 0;
-                    nxt = solo_serp_first(ed, 0);
-                } else {
-                    nxt = solo_serp_next(ed, e.pr, e.pc);
-                }
-                e.pos_idx = nidx;
-                e.pr = nxt >> 4;
-                e.pc = nxt & 15;
-            }
-            e.t += 1;
-            bool done = e.t >= e.max_steps;
-            if (p.budget > 0) done |= e.changes >= p.budget;
-            p.reward[env] = reward;
-            p.done[env] = done;
-            if (p.terminal) p.terminal[env] = done;
-            if (p.ep_rew) p.ep_rew[env] = done ? e.ep_reward : 0.0;
-            if (p.ep_len) p.ep_len[env] = done ? e.t : 0;
-            if (p.ep_start) p.ep_start[env] = done ? e.ep_start_loss : 0.0;
-            if (p.fin_loss) p.fin_loss[env] = done ? e.prev_loss : 0.0;
-            if (done && p.stats) {
-                atomicAdd(p.stats + 0, 1.0);
-                atomicAdd(p.stats + 1, e.ep_reward);
-                atomicAdd(p.stats + 2, (double)e.t);
-                atomicAdd(p.stats + 3, e.ep_start_loss);
-                atomicAdd(p.stats + 4, e.prev_loss);
-            }
-            if (done) {
-                solo_reset<DOM>(p, e, slot);
-                rows_dirty = metrics_dirty = rng_dirty = true;
-            }
-        } else if (mode == MODE_RESET) {
-            if (!p.reset_mask || p.reset_mask[env]) {
-                solo_reset<DOM>(p, e, slot);
-                rows_dirty = metrics_dirty = rng_dirty = true;
-            }
+        } else if (ok) {  // wide
+            int cell = (int)(a / N);
+            tile = (int)(a - (long long)cell * N);
+            r = cell / p.W;
+            c = cell - r * p.W;
         }
-        if (mode != MODE_OBSERVE) solo_store<DOM>(p, env, e, rows_dirty, planes_dirty, metrics_dirty, rng_dirty);
-        if (p.obs) solo_render<DOM>(p, e, slot);
-    }
-    if (p.obs) {
-        __syncwarp();
-        long long rem = (long long)p.B - env0;
-        int nenv = rem < 32 ? (int)rem : 32;
-        if (nenv > 0) {
-            if ((reinterpret_cast<uintptr_t>(p.obs) & 31) == 0)
-                solo_write_warp<8>(p, wimg, env0, nenv, lane);
-            else
-                solo_write_warp<4>(p, wimg, env0, nenv, lane);
+        bool wrote = false;
+        if (tile >= 0) {
+            const uint32_t sh = (r & 1) * 16 + c;
+            const int wi = r >> 1;
+            bool act = r < e.h && c < e.w;
+            int cur = act ? 0 : N;
+            uint32_t fz = 0;
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                if (k == wi) {
+#pragma unroll
+                    for (int q = 0; q < Dom<DOM>::NPL; q++)
+                        if ((e.pl[q].w[k] >> sh) & 1u) cur = q + 1;
+                    fz = (e.frz.w[k] >> sh) & 1u;
+                }
+            }
+            bool editable = act && !fz;
+            wrote = tile != cur && (p.rep == REP_NARROW || editable);
+        }
+        double reward = 0.0;
+        if (wrote) {
+            solo_set_tile<DOM>(e, r, c, tile);
+            planes_dirty = true;
+            e.changes += 1;
+            double before = e.prev_loss;
+            solo_recompute<DOM>(p, e, slot, false);
+            reward = __dsub_rn(before, e.prev_loss);
+            metrics_dirty = true;
+            rng_dirty = true;
+        }
+        e.ep_reward = __dadd_rn(e.ep_reward, reward);
+        if (p.rep == REP_NARROW) {  // pos_idx = (pos_idx + 1) % order_len
+            SB ed = andnot(rect_sb(e.h, e.w), e.frz);
+            int nidx = e.pos_idx + 1, nxt;
+            if (nidx >= e.order_len) {
+                nidx = 0;
+                nxt = solo_serp_first(ed, 0);
+            } else {
+                nxt = solo_serp_next(ed, e.pr, e.pc);
+            }
+            e.pos_idx = nidx;
+            e.pr = nxt >> 4;
+            e.pc = nxt & 15;
+        }
+        e.t += 1;
+        bool done = e.t >= e.max_steps;
+        if (p.budget > 0) done |= e.changes >= p.budget;
+        p.reward[env] = reward;
+        p.done[env] = done;
+        if (p.terminal) p.terminal[env] = done;
+        if (p.ep_rew) p.ep_rew[env] = done ? e.ep_reward : 0.0;
+        if (p.ep_len) p.ep_len[env] = done ? e.t : 0;
+        if (p.ep_start) p.ep_start[env] = done ? e.ep_start_loss : 0.0;
+        if (p.fin_loss) p.fin_loss[env] = done ? e.prev_loss : 0.0;
+        if (done && p.stats) {
+            atomicAdd(p.stats + 0, 1.0);
+            atomicAdd(p.stats + 1, e.ep_reward);
+            atomicAdd(p.stats + 2, (double)e.t);
+            atomicAdd(p.stats + 3, e.ep_start_loss);
+            atomicAdd(p.stats + 4, e.prev_loss);
+        }
+        if (done) {
+            solo_reset<DOM>(p, e, slot);
+            rows_dirty = metrics_dirty = rng_dirty = true;
+        }
+    } else if (mode == MODE_RESET) {
+        if (!p.reset_mask || p.reset_mask[env]) {
+            solo_reset<DOM>(p, e, slot);
+            rows_dirty = metrics_dirty = rng_dirty = true;
         }
     }
+    if (mode != MODE_OBSERVE) solo_store<DOM>(p, env, e, rows_dirty, planes_dirty, metrics_dirty, rng_dirty);
+    if (p.obs) solo_render<DOM>(p, e, slot);
+    }
+
+template <int DOM>
+__global__ void __launch_bounds__(128, 1) env_solo_kernel(const Params p, int mode) {
+    extern __shared__ __align__(16) uint32_t smem_w[];
+    const int E = p.solo_E, T = blockDim.x, tid = threadIdx.x;
+    const bool warp_mode = E == T;  // uniform over the launch
+    // warp mode (large batches): warp w owns 32 consecutive envs and writes
+    // their outputs; block mode (small batches): E < T envs per block and all
+    // T threads write them.
+    const int lane = tid & 31, warp = tid >> 5;
+    const long long env0 = warp_mode ? (long long)blockIdx.x * T + warp * 32 : (long long)blockIdx.x * E;
+    const int local = warp_mode ? lane : tid;
+    uint32_t *img = smem_w + (warp_mode ? (size_t)warp * 32 * p.env_smem : 0);
+    const long long env = env0 + local;
+    if (local < (warp_mode ? 32 : E) && env < p.B) solo_env<DOM>(p, mode, env, img + (size_t)local * p.env_smem);
+    if (!p.obs) return;
+    long long rem = (long long)p.B - env0;
+    const int cap = warp_mode ? 32 : E;
+    const int nenv = rem < cap ? (rem > 0 ? (int)rem : 0) : cap;
+    if (warp_mode) __syncwarp();
+    else __syncthreads();
+    if (nenv <= 0) return;
+    const int wl = warp_mode ? lane : tid, nthr = warp_mode ? 32 : T;
+    const size_t first = (size_t)env0 * p.PE;
+    // obs base is 16-byte aligned (checked on the host) and env0 is a multiple
+    // of 8, so every block's output starts 32-byte aligned when the base is.
+    if ((reinterpret_cast<uintptr_t>(p.obs + first) & 31) == 0) solo_write<8, 2>(p, img, env0, nenv, wl, nthr);
+    else solo_write<4, 2>(p, img, env0, nenv, wl, nthr);
 }
 
 // ---- state export / import / metrics for the solo layout -------------------
