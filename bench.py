@@ -213,16 +213,16 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     from paper_2408_12525_b200.env import INFO_KEYS, BatchEnv, NumpyBatchEnv
 
-    if global_b % world:
-        raise SystemExit("global env count must divide by the number of GPUs")
-    B = global_b // world
-    env = BatchEnv(cfg, B, seed=0, device=dev, global_offset=rank * B, validate=False)
+    from paper_2408_12525_b200.sharding import EpisodeStats, max_over_ranks, shard
+    offset, B = shard(global_b, world, rank)
+    env = BatchEnv(cfg, B, seed=0, device=dev, global_offset=offset, validate=False)
     obs = env.new_obs()
     acts = torch.empty(B, dtype=torch.int64, device=dev)
     reward = torch.empty(B, dtype=torch.float64, device=dev)
     done = torch.empty(B, dtype=torch.bool, device=dev)
     info = env._info_buffers()
-    stats = torch.zeros(5, dtype=torch.float64, device=dev)
+    ep_stats = EpisodeStats(dev)
+    stats = ep_stats.t
     env.reset(out=obs)
     stream = torch.cuda.current_stream(dev)
 
@@ -257,11 +257,9 @@ def main():
     clocks = clk.stop()
     elapsed_ms = t_start.elapsed_time(t_end)
     step_ms = sum(a.elapsed_time(b) for a, b in ev) / K
-    if world > 1:
-        t = torch.tensor([elapsed_ms, step_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms, step_ms = float(t[0]), float(t[1])
-        dist.all_reduce(stats)  # the episode-stats reduce over NVLink
+    elapsed_ms = max_over_ranks(elapsed_ms, dev)
+    step_ms = max_over_ranks(step_ms, dev)
+    ep_stats.all_reduce()  # the episode-stats reduce (NCCL over NVLink when N > 1)
     errs = env.errors()
     if errs:
         raise SystemExit(f"device error flags {errs}")
@@ -277,7 +275,7 @@ def main():
     if not args.no_e2e:
         del obs
         torch.cuda.empty_cache()
-        nenv = NumpyBatchEnv(cfg, B, seed=0, device=dev, global_offset=rank * B, pinned=True, copy=False)
+        nenv = NumpyBatchEnv(cfg, B, seed=0, device=dev, global_offset=offset, pinned=True, copy=False)
         nenv.reset()
         import numpy as np
         rng = np.random.default_rng(1)
@@ -288,11 +286,7 @@ def main():
         t0 = time.perf_counter()
         for a in host_acts[1:]:
             nenv.step(a)
-        dt = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([dt], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t[0])
+        dt = max_over_ranks(time.perf_counter() - t0, dev)
         obs_b = 4 * int(np.prod(env.observation_shape))
         e2e = {"value": global_b * args.e2e_steps / dt, "unit": UNIT,
                "h2d_bytes_per_step": B * 8,
