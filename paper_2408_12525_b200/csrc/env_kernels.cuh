@@ -99,6 +99,7 @@ struct Params {
     int img_words;  // u32 words of one env's bit image (incl. 1 pad word)
     int env_smem;   // shared memory per env: bytes (team kernel) or 32-bit words (solo)
     int solo_E;     // solo kernel: envs per block (== blockDim: warp mode)
+    int solo_u;     // solo kernel: stores in flight per lane in the obs writer (2 or 4)
     int off_ctrl;   // byte offset of the control floats within an env's smem
 };
 

@@ -523,9 +523,14 @@ extern "C" int lg_create(const lg_config *cfg, int64_t n_envs, int64_t global_of
         if (!(slot & 1)) slot++;
         p.env_smem = slot;
         e->team = 1;
-        if (n_envs >= 148LL * 8 * 64) {  // enough warps: each warp writes its own 32 envs
-            e->threads = 64;
-            e->E = 64;
+        const char *tb = getenv("LG_SOLO_THREADS");
+        int warp_threads = tb ? atoi(tb) : 64;
+        if (warp_threads != 32 && warp_threads != 64 && warp_threads != 128) warp_threads = 64;
+        const char *su = getenv("LG_SOLO_U");
+        p.solo_u = su && atoi(su) == 4 ? 4 : 2;
+        if (n_envs >= 148LL * 4 * 32) {  // >= 4 warps per SM: each warp writes its own 32 envs
+            e->threads = warp_threads;
+            e->E = warp_threads;
         } else {  // small batch: E envs per block, the whole block writes
             long long per = n_envs / (148 * 4);
             int E = 8;
@@ -539,7 +544,9 @@ extern "C" int lg_create(const lg_config *cfg, int64_t n_envs, int64_t global_of
     }
     if (e->geo != 1) {
         e->team = e->geo == 16 ? 16 : 32;
-        e->threads = 256;
+        const char *tt = getenv("LG_TEAM_THREADS");
+        e->threads = tt ? atoi(tt) : 64;
+        if (e->threads != 32 && e->threads != 64 && e->threads != 128 && e->threads != 256) e->threads = 64;
         e->E = e->threads / e->team;
         int rows = e->geo == 16 ? 16 : e->geo == 32 ? 32 : 64;
         int runs = e->geo == 64 ? 32 : 16;

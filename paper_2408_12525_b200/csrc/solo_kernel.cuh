@@ -579,8 +579,12 @@ __global__ void __launch_bounds__(128, 1) env_solo_kernel(const Params p, int mo
     const size_t first = (size_t)env0 * p.PE;
     // obs base is 16-byte aligned (checked on the host) and env0 is a multiple
     // of 8, so every block's output starts 32-byte aligned when the base is.
-    if ((reinterpret_cast<uintptr_t>(p.obs + first) & 31) == 0) solo_write<8, 2>(p, img, env0, nenv, wl, nthr);
-    else solo_write<4, 2>(p, img, env0, nenv, wl, nthr);
+    if ((reinterpret_cast<uintptr_t>(p.obs + first) & 31) == 0) {
+        if (p.solo_u == 4) solo_write<8, 4>(p, img, env0, nenv, wl, nthr);
+        else solo_write<8, 2>(p, img, env0, nenv, wl, nthr);
+    } else {
+        solo_write<4, 2>(p, img, env0, nenv, wl, nthr);
+    }
 }
 
 // ---- state export / import / metrics for the solo layout -------------------
