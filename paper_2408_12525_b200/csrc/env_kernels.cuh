@@ -100,6 +100,7 @@ struct Params {
     int env_smem;   // shared memory per env: bytes (team kernel) or 32-bit words (solo)
     int solo_E;     // solo kernel: envs per block (== blockDim: warp mode)
     int solo_u;     // solo kernel: stores in flight per lane in the obs writer (2 or 4)
+    int ws_producers, ws_consumers, ws_slots;  // warp-specialised solo kernel (0 = off)
     int off_ctrl;   // byte offset of the control floats within an env's smem
 };
 
@@ -212,7 +213,7 @@ struct TeamK {
 // board backend K (lane team or single thread). pl: stored tile planes
 // (tile p+1), act: active mask, g: metric generator (binary draw only).
 template <class K, int DOM>
-__device__ void compute_metrics(const K &k, const typename K::B *pl, const typename K::B &act, Pcg &g,
+__device__ __forceinline__ void compute_metrics(const K &k, const typename K::B *pl, const typename K::B &act, Pcg &g,
                                 void *uf, int *val, int &unr) {
     using B = typename K::B;
     unr = 0;
@@ -294,13 +295,11 @@ __device__ void recompute(const Params &p, const Team<G> &t, EnvRegs<G, DOM> &e,
     using Row = typename G::Row;
     TeamK<G> k{t, low_mask<Row>(p.W)};
     Bd<G> act = rect_board(t, e.h, e.w);
-    if (p.det) {  // _metric_rngs: fresh default_rng(metric_seed) (env.py:327-330)
-        Pcg mg;
-        seedseq_pcg((uint64_t)e.mseed, false, 0, mg);
-        compute_metrics<TeamK<G>, DOM>(k, e.pl, act, mg, uf, e.val, e.unr);
-    } else {
-        compute_metrics<TeamK<G>, DOM>(k, e.pl, act, e.g, uf, e.val, e.unr);
-    }
+    // _metric_rngs (env.py:327-330): the env stream, or a fresh default_rng(metric_seed)
+    Pcg mg = e.g;
+    if (p.det) seedseq_pcg((uint64_t)e.mseed, false, 0, mg);
+    compute_metrics<TeamK<G>, DOM>(k, e.pl, act, mg, uf, e.val, e.unr);
+    if (!p.det) e.g = mg;
     double l = loss_of<DOM>(p, e.val, e.unr, e.lo, e.hi);
     e.prev_loss = l;
     if (reset) {

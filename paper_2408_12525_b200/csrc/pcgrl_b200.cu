@@ -282,6 +282,7 @@ struct lg_env {
     int team, threads, E;
     int N, M, NPL, C, OH, OW;
     long long n_actions;
+    int ws_grid = 0;
     size_t row_bytes, rows_per_env;
     Params base;
     size_t smem;
@@ -328,7 +329,24 @@ static int launch_env_t(lg_env *e, const Params &p, int mode, cudaStream_t s) {
 }
 
 template <int DOM>
+static int launch_solo_ws_t(lg_env *e, const Params &p, int mode, cudaStream_t s) {
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [] {
+        attr_err = cudaFuncSetAttribute(env_solo_ws_kernel<DOM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        227 * 1024);
+    });
+    CU(attr_err);
+    int threads = 32 * (p.ws_producers + p.ws_consumers);
+    size_t smem = (size_t)p.ws_slots * 32 * p.env_smem * 4 + (size_t)p.ws_slots * 16;
+    env_solo_ws_kernel<DOM><<<e->ws_grid, threads, smem, s>>>(p, mode);
+    CU(cudaGetLastError());
+    return LG_OK;
+}
+
+template <int DOM>
 static int launch_solo_t(lg_env *e, const Params &p, int mode, cudaStream_t s) {
+    if (p.ws_slots > 0 && p.obs) return launch_solo_ws_t<DOM>(e, p, mode, s);
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [] {
@@ -540,6 +558,23 @@ extern "C" int lg_create(const lg_config *cfg, int64_t n_envs, int64_t global_of
         }
         p.solo_E = e->E;
         e->smem = (size_t)e->E * slot * 4;
+        // warp-specialised persistent variant (LG_WS=producers,consumers[,slots])
+        const char *ws = getenv("LG_WS");
+        if (ws && n_envs >= 148LL * 32 * 4) {
+            int P = 0, C = 0, S = 0;
+            if (sscanf(ws, "%d,%d,%d", &P, &C, &S) < 2) P = C = 0;
+            size_t slot_bytes = (size_t)32 * slot * 4;
+            int smax = (int)((225 * 1024) / (slot_bytes + 16));
+            if (S <= 0 || S > smax) S = smax;
+            if (P > 0 && C > 0 && P + C <= 16 && S >= 2) {
+                p.ws_producers = P;
+                p.ws_consumers = C;
+                p.ws_slots = S;
+                int dev_sms = 148;
+                cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
+                e->ws_grid = dev_sms;
+            }
+        }
         if (e->OW > 64 || e->smem > 200 * 1024) e->geo = pick_geo(17, W);  // too wide: lane teams
     }
     if (e->geo != 1) {

@@ -96,7 +96,7 @@ struct SoloK {
         for (int k = 0; k < 8; k++) b.w[k] = (k == (flat >> 5)) ? (1u << (flat & 31)) : 0u;
         return b;
     }
-    __device__ int kth(const SB &m, int kk) const {
+    __device__ __forceinline__ int kth(const SB &m, int kk) const {
         int res = 0;
         bool found = false;
 #pragma unroll
@@ -112,7 +112,7 @@ struct SoloK {
         }
         return res;
     }
-    __device__ int lowest(const SB &m) const {
+    __device__ __forceinline__ int lowest(const SB &m) const {
         int res = 0;
         bool found = false;
 #pragma unroll
@@ -123,7 +123,7 @@ struct SoloK {
             }
         return res;
     }
-    __device__ int bfs_last(SB &f, const SB &pass) const {
+    __device__ __forceinline__ int bfs_last(SB &f, const SB &pass) const {
         SB vis = f;
         int depth = 0;
         while (true) {
@@ -135,7 +135,7 @@ struct SoloK {
         }
     }
     template <bool ENDPOINT>
-    __device__ void touch(SB f, const SB &pass, const SB &ta, const SB &tb, bool want_b, int &da,
+    __device__ __forceinline__ void touch(SB f, const SB &pass, const SB &ta, const SB &tb, bool want_b, int &da,
                           int &db) const {
         da = -1;
         db = -1;
@@ -175,7 +175,7 @@ struct SoloK {
     // count_regions (pathfind.py:116-130) as a sequential run union-find:
     // nodes are runs of a row (id = row*8 + run index); a run touching a run
     // of the previous row is united with it; regions = runs - merges.
-    __device__ int regions(const SB &pass, void *scratch) const {
+    __device__ __forceinline__ int regions(const SB &pass, void *scratch) const {
         uint8_t *par = reinterpret_cast<uint8_t *>(scratch);
         int runs = 0, merges = 0;
         uint32_t prevR = 0, prevS = 0;

@@ -119,16 +119,14 @@ __device__ void solo_store(const Params &p, long long env, const SoloEnv<DOM> &e
 }
 
 template <int DOM>
-__device__ void solo_recompute(const Params &p, SoloEnv<DOM> &e, void *uf, bool reset) {
+__device__ __forceinline__ void solo_recompute(const Params &p, SoloEnv<DOM> &e, void *uf, bool reset) {
     SoloK k;
     SB act = rect_sb(e.h, e.w);
-    if (p.det) {  // _metric_rngs (env.py:327-330)
-        Pcg mg;
-        seedseq_pcg((uint64_t)e.mseed, false, 0, mg);
-        compute_metrics<SoloK, DOM>(k, e.pl, act, mg, uf, e.val, e.unr);
-    } else {
-        compute_metrics<SoloK, DOM>(k, e.pl, act, e.g, uf, e.val, e.unr);
-    }
+    // _metric_rngs (env.py:327-330): the env stream, or a fresh default_rng(metric_seed)
+    Pcg mg = e.g;
+    if (p.det) seedseq_pcg((uint64_t)e.mseed, false, 0, mg);
+    compute_metrics<SoloK, DOM>(k, e.pl, act, mg, uf, e.val, e.unr);
+    if (!p.det) e.g = mg;
     double l = loss_of<DOM>(p, e.val, e.unr, e.lo, e.hi);
     e.prev_loss = l;
     if (reset) {
@@ -174,7 +172,7 @@ __device__ __forceinline__ void solo_set_tile(SoloEnv<DOM> &e, int r, int c, int
 }
 
 template <int DOM>
-__device__ void solo_reset(const Params &p, SoloEnv<DOM> &e, void *uf) {
+__device__ __forceinline__ void solo_reset(const Params &p, SoloEnv<DOM> &e, void *uf) {
     constexpr int N = Dom<DOM>::N, NPL = Dom<DOM>::NPL, M = Dom<DOM>::M;
     Pcg &g = e.g;
     int h = p.H, w = p.W;
@@ -205,7 +203,10 @@ __device__ void solo_reset(const Params &p, SoloEnv<DOM> &e, void *uf) {
                     for (int q = 0; q < NPL; q++) rowbits[q] |= (q == idx - 1) ? (1u << c) : 0u;
                 }
 #pragma unroll
-                for (int q = 0; q < NPL; q++) e.pl[q].w[r >> 1] |= rowbits[q] << ((r & 1) * 16);
+                for (int q = 0; q < NPL; q++)
+#pragma unroll
+                    for (int k = 0; k < 8; k++)  // select chain keeps the register index static
+                        e.pl[q].w[k] |= (k == (r >> 1)) ? (rowbits[q] << ((r & 1) * 16)) : 0u;
             }
         }
     }
@@ -253,8 +254,11 @@ __device__ void solo_reset(const Params &p, SoloEnv<DOM> &e, void *uf) {
         }
         for (int j = 0; j < p.n_ctrl; j++)
             if (p.ctrl[j] == m) lo = hi = (int)pcg_integers(g, 0, (int64_t)cap + 1);
-        e.lo[m] = lo;
-        e.hi[m] = hi;
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            e.lo[q] = (q == m) ? lo : e.lo[q];
+            e.hi[q] = (q == m) ? hi : e.hi[q];
+        }
     }
     if (p.det) e.mseed = (long long)pcg_bounded(g, 0x7FFFFFFFFFFFFFFFULL);  // env.py:302-303
     SB ed = andnot(act, e.frz);  // _install_row (env.py:307-325)
@@ -330,28 +334,30 @@ __device__ void solo_render(const Params &p, const SoloEnv<DOM> &e, uint32_t *sl
     int after = OH - before - n_in;
     BitW bw{slot, 0, 0, 0};
     const uint32_t wm = mask16(W), am = mask16(e.w);
-#pragma unroll
+    // plane loop kept rolled (instruction-cache footprint); the stored plane
+    // for `pl` is picked with selects so register indexing stays static.
+#pragma unroll 1
     for (int pl = 0; pl < N + 2; pl++) {
         const bool fill = pl >= N;  // border and frozen planes read 1 outside the max grid
         bw.fill(fill, before * OW);
+        SB cur;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            uint32_t any = 0, sel = 0;
+#pragma unroll
+            for (int q = 0; q < NPL; q++) {
+                any |= e.pl[q].w[k];
+                sel = (q == pl - 1) ? e.pl[q].w[k] : sel;
+            }
+            const uint32_t act2 = ((2 * k < e.h) ? am : 0u) | ((2 * k + 1 < e.h) ? (am << 16) : 0u);
+            const uint32_t wm2 = wm | (wm << 16);
+            cur.w[k] = pl == 0 ? (act2 & ~any) : pl < N ? sel : pl == N ? (~act2 & wm2) : e.frz.w[k];
+        }
 #pragma unroll
         for (int gr = 0; gr < 16; gr++) {
             int i = gr - r0;
             if (gr < H && i >= 0 && i < OH) {
-                uint32_t act = gr < e.h ? am : 0u;
-                uint32_t m;
-                if (pl == 0) {
-                    uint32_t any = 0;
-#pragma unroll
-                    for (int q = 0; q < NPL; q++) any |= (gr & 1) ? (e.pl[q].w[gr >> 1] >> 16) : e.pl[q].w[gr >> 1];
-                    m = act & ~any;
-                } else if (pl < N) {
-                    m = ((gr & 1) ? (e.pl[pl - 1].w[gr >> 1] >> 16) : e.pl[pl - 1].w[gr >> 1]) & 0xFFFFu;
-                } else if (pl == N) {
-                    m = ~act & wm;
-                } else {
-                    m = ((gr & 1) ? (e.frz.w[gr >> 1] >> 16) : e.frz.w[gr >> 1]) & 0xFFFFu;
-                }
+                uint32_t m = ((gr & 1) ? (cur.w[gr >> 1] >> 16) : cur.w[gr >> 1]) & 0xFFFFu;
                 uint64_t win = c0 >= 0 ? ((uint64_t)m >> c0) : ((uint64_t)m << (-c0));
                 win = (win & inside) | (fill ? (full & ~inside) : 0ull);
                 bw.put(win, OW);
@@ -445,6 +451,71 @@ __device__ void solo_write(const Params &p, const uint32_t *wimg, long long env0
     for (uint32_t t = nv * VEC + lane; t < total; t += nthr) {
         uint32_t e2 = fdiv(p.divPE, t);
         out[t] = solo_elem(p, wimg, e2, t - e2 * p.PE);
+    }
+}
+
+// Branch-light writer for observations without control planes (PB == PE),
+// 32-byte aligned output: U independent 256-bit stores per lane per round.
+// A group of 8 elements that straddles an env boundary takes its high bits
+// from the first word of the next env's image.
+template <int U>
+__device__ void solo_write_noctrl(const Params &p, const uint32_t *wimg, long long env0, int nenv, int lane,
+                                  int nthr) {
+    float *out = p.obs + (size_t)env0 * p.PE;
+    const uint32_t PE = p.PE, stride = (uint32_t)p.env_smem;
+    const uint32_t total = (uint32_t)nenv * PE;
+    const uint32_t nv = total / 8;
+    const uint32_t STEP = (uint32_t)nthr * U * 8;  // elements per round per lane
+    uint32_t el[U], le[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        uint32_t e = (uint32_t)(lane + nthr * u) * 8;
+        el[u] = fdiv(p.divPE, e);
+        le[u] = e - el[u] * PE;
+    }
+    const bool small_env = PE <= STEP;  // more than one wrap per round: use the divider
+    uint32_t q0 = lane;
+    for (; q0 + (uint32_t)nthr * (U - 1) < nv; q0 += (uint32_t)nthr * U) {
+        uint32_t x[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const uint32_t *sl = wimg + el[u] * stride;
+            const uint32_t wi = le[u] >> 5;
+            uint32_t v = __funnelshift_r(sl[wi], sl[wi + 1], le[u] & 31);
+            const uint32_t k = PE - le[u];
+            if (k < 8) {
+                uint32_t m = (1u << k) - 1u;
+                v = (v & m) | ((sl[stride] << k) & ~m);
+            }
+            x[u] = v;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            float f[8];
+#pragma unroll
+            for (int j = 0; j < 8; j++) f[j] = ((x[u] >> j) & 1u) ? 1.0f : 0.0f;
+            st_cs_v8(out + (size_t)(q0 + (uint32_t)nthr * u) * 8, f);
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            uint32_t l = le[u] + STEP;
+            if (small_env) {
+                uint32_t kk = fdiv(p.divPE, l);
+                el[u] += kk;
+                le[u] = l - kk * PE;
+            } else if (l >= PE) {
+                el[u] += 1;
+                le[u] = l - PE;
+            } else {
+                le[u] = l;
+            }
+        }
+    }
+    for (uint32_t t = q0 * 8; t < total; t += (uint32_t)nthr * 8) {  // ragged end, element by element
+        for (uint32_t j = 0; j < 8 && t + j < total; j++) {
+            uint32_t e2 = fdiv(p.divPE, t + j);
+            out[t + j] = solo_elem(p, wimg, e2, t + j - e2 * PE);
+        }
     }
 }
 
@@ -580,8 +651,12 @@ __global__ void __launch_bounds__(128, 1) env_solo_kernel(const Params p, int mo
     // obs base is 16-byte aligned (checked on the host) and env0 is a multiple
     // of 8, so every block's output starts 32-byte aligned when the base is.
     if ((reinterpret_cast<uintptr_t>(p.obs + first) & 31) == 0) {
-        if (p.solo_u == 4) solo_write<8, 4>(p, img, env0, nenv, wl, nthr);
-        else solo_write<8, 2>(p, img, env0, nenv, wl, nthr);
+        if (p.PB == p.PE) {
+            if (p.solo_u == 4) solo_write_noctrl<4>(p, img, env0, nenv, wl, nthr);
+            else solo_write_noctrl<2>(p, img, env0, nenv, wl, nthr);
+        } else {
+            solo_write<8, 2>(p, img, env0, nenv, wl, nthr);
+        }
     } else {
         solo_write<4, 2>(p, img, env0, nenv, wl, nthr);
     }
@@ -765,6 +840,90 @@ __global__ void __launch_bounds__(128) solo_metrics_kernel(long long n, int H, i
         rg[1] = (uint64_t)g.s;
         rg[4] = g.has;
         rg[5] = g.u;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Warp-specialised persistent variant: P producer warps step 32 envs each and
+// render their images into a ring of S shared-memory slots; C consumer warps
+// stream every filled slot to HBM. full/empty mbarriers hand slots over, so
+// stores never wait for a slow environment and steps never wait for stores.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+                 "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile(
+        "{\n\t.reg .b64 st;\n\tmbarrier.arrive.release.cta.shared::cta.b64 st, [%0];\n\t}" ::"r"(
+            (unsigned)__cvta_generic_to_shared(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+    unsigned addr = (unsigned)__cvta_generic_to_shared(bar);
+    unsigned done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(addr), "r"(parity)
+            : "memory");
+    }
+}
+
+template <int DOM>
+__global__ void __launch_bounds__(512, 1) env_solo_ws_kernel(const Params p, int mode) {
+    extern __shared__ __align__(16) uint32_t smem_w[];
+    const int P = p.ws_producers, C = p.ws_consumers, S = p.ws_slots;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const size_t slot_words = (size_t)32 * p.env_smem;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem_w + (size_t)S * slot_words);
+    uint64_t *empty = full + S;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; s++) {
+            mbar_init(&full[s], 32);
+            mbar_init(&empty[s], C);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const long long ntiles = ((long long)p.B + 31) / 32;
+    const long long G = gridDim.x, b = blockIdx.x;
+    const long long mine = b < ntiles ? (ntiles - b + G - 1) / G : 0;  // tiles b, b+G, ...
+    if (warp < P) {
+        for (long long k = warp; k < mine; k += P) {
+            const int s = (int)(k % S);
+            const unsigned round = (unsigned)(k / S);
+            if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
+            const long long env = (b + k * G) * 32 + lane;
+            uint32_t *slot = smem_w + (size_t)s * slot_words + (size_t)lane * p.env_smem;
+            if (env < p.B) solo_env<DOM>(p, mode, env, slot);
+            __syncwarp();
+            mbar_arrive(&full[s]);
+        }
+    } else {
+        const int cw = warp - P;
+        for (long long k = 0; k < mine; k++) {
+            const int s = (int)(k % S);
+            mbar_wait(&full[s], (unsigned)(k / S) & 1);
+            const long long env0 = (b + k * G) * 32;
+            long long rem = (long long)p.B - env0;
+            const int nenv = rem < 32 ? (int)rem : 32;
+            const uint32_t *img = smem_w + (size_t)s * slot_words;
+            if (p.obs && nenv > 0) {
+                if ((reinterpret_cast<uintptr_t>(p.obs + (size_t)env0 * p.PE) & 31) == 0 && p.PB == p.PE)
+                    solo_write_noctrl<4>(p, img, env0, nenv, cw * 32 + lane, C * 32);
+                else if ((reinterpret_cast<uintptr_t>(p.obs + (size_t)env0 * p.PE) & 31) == 0)
+                    solo_write<8, 2>(p, img, env0, nenv, cw * 32 + lane, C * 32);
+                else
+                    solo_write<4, 2>(p, img, env0, nenv, cw * 32 + lane, C * 32);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
     }
 }
 
