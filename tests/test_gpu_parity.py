@@ -228,3 +228,58 @@ def test_pinpoint_overflow_flags_error():
     env = BatchEnv(cfg, 2)
     with pytest.raises(ValueError):
         env.reset()
+
+
+WARP_MODE_CASES = [
+    (dict(domain="binary"), 40000, 4),
+    (dict(domain="maze", representation="turtle"), 20000, 4),
+    (dict(domain="dungeon", representation="wide", pinpoints=("player", "key", "door"),
+          randomize_shape=True), 20000, 4),
+    (dict(domain="maze", controllable=("path_length", "regions")), 20000, 3),
+]
+
+
+@pytest.mark.parametrize("case", range(len(WARP_MODE_CASES)))
+def test_large_batch_warp_mode_against_oracle(case):
+    """Batches >= 4 warps/SM take the warp-mode store path; pin it to the oracle."""
+    kw, n, steps = WARP_MODE_CASES[case]
+    cfg = EnvConfig(**kw)
+    env = BatchEnv(cfg, n, seed=21)
+    ref = O.OracleBatchEnv(cfg, n, seed=21)
+    assert np.array_equal(_np(env.reset()), ref.reset())
+    act = np.random.default_rng(5)
+    for t in range(steps):
+        a = act.integers(0, cfg.n_actions, size=n)
+        o1, r1, d1, _ = env.step(a)
+        o2, r2, d2, _ = ref.step(a)
+        assert np.array_equal(_np(r1), r2), t
+        assert np.array_equal(_np(d1), d2), t
+        assert np.array_equal(_np(o1), o2), t
+
+
+def test_full_size_c5_properties():
+    """2^20 envs (config c5): size-independent invariants of the outputs, and a
+    shard built with global_offset reproduces its slice of the full batch."""
+    cfg = EnvConfig(domain="binary")
+    n = 1 << 20
+    env = BatchEnv(cfg, n, seed=0, validate=False)
+    obs = env.reset()
+    for t in range(3):
+        obs, r, d, info = env.step(env.random_actions(t))
+    n_tiles = cfg.domain_obj.n_tiles
+    one_hot = obs[:, : n_tiles + 1].sum(dim=1)
+    assert bool((one_hot == 1.0).all())                       # tile planes are one-hot
+    border, frozen = obs[:, n_tiles], obs[:, n_tiles + 1]
+    assert bool((frozen >= border).all())                     # border cells read frozen
+    assert bool((r == torch.round(r)).all())                  # unit weights: integer losses
+    assert env.errors() == 0
+    lo, cnt = 123456, 4096
+    part = BatchEnv(cfg, cnt, seed=0, global_offset=lo, validate=False)
+    part.reset()
+    for t in range(3):
+        # the same per-env actions the full batch received
+        full_a = torch.empty(n, dtype=torch.int64, device="cuda")
+        env2_a = env.random_actions(t, out=full_a)
+        po, pr, _, _ = part.step(env2_a[lo:lo + cnt].contiguous())
+    assert torch.equal(po, obs[lo:lo + cnt])
+    assert torch.equal(pr, r[lo:lo + cnt])
