@@ -278,16 +278,35 @@ __device__ __forceinline__ void solo_reset(const Params &p, SoloEnv<DOM> &e, voi
 }
 
 // Sequential bit writer into one env's image slot.
+// Stream-mode shared-memory index: one pad word after every 32 words so that
+// the 32 lanes of a warp, each writing its own env's stretch of the stream,
+// spread over the banks instead of colliding (env stretches are ~PE/32 words).
+__device__ __forceinline__ uint32_t sidx(uint32_t w) { return w + (w >> 5); }
+
 struct BitW {
     uint32_t *dst;
     uint32_t widx;
     uint64_t acc;
     int n;
+    // stream mode: this env's bits start mid-word inside a warp-wide bit
+    // stream; the first and a partial last word are shared with neighbouring
+    // envs (rendered by other lanes) and are merged with atomicOr.
+    bool stream, first, last;
+    __device__ __forceinline__ void emit(uint32_t word) {
+        if (stream) {
+            if (first) atomicOr(&dst[sidx(widx)], word);
+            else dst[sidx(widx)] = word;
+        } else {
+            dst[widx] = word;
+        }
+        first = false;
+        widx++;
+    }
     __device__ __forceinline__ void put32(uint32_t v, int cnt) {  // cnt <= 32, v < 2^cnt
         acc |= (uint64_t)v << n;
         n += cnt;
         if (n >= 32) {
-            dst[widx++] = (uint32_t)acc;
+            emit((uint32_t)acc);
             acc >>= 32;
             n -= 32;
         }
@@ -308,13 +327,24 @@ struct BitW {
         }
     }
     __device__ __forceinline__ void flush() {
+        if (stream) {
+            if (n > 0) {
+                if (first || !last) atomicOr(&dst[sidx(widx)], (uint32_t)acc);
+                else dst[sidx(widx)] = (uint32_t)acc;
+            }
+            return;
+        }
         if (n > 0) dst[widx++] = (uint32_t)acc;
         dst[widx++] = 0u;  // pad word read by the 2-word funnel shift
     }
 };
 
+// Render one env's 0/1 observation planes as a bit stream: into its private
+// slot (slot mode), or at bit offset `bit0` of the warp/block stream whose
+// bits are the concatenated outputs of consecutive envs (stream mode).
 template <int DOM>
-__device__ void solo_render(const Params &p, const SoloEnv<DOM> &e, uint32_t *slot) {
+__device__ void solo_render(const Params &p, const SoloEnv<DOM> &e, uint32_t *slot, bool stream, uint32_t bit0,
+                            bool last) {
     constexpr int N = Dom<DOM>::N, NPL = Dom<DOM>::NPL;
     const int OH = p.OH, OW = p.OW, H = p.H, W = p.W;
     int r0 = 0, c0 = 0;
@@ -332,7 +362,7 @@ __device__ void solo_render(const Params &p, const SoloEnv<DOM> &e, uint32_t *sl
     int g_lo = r0 > 0 ? r0 : 0, g_hi = (r0 + OH) < H ? (r0 + OH) : H;
     int n_in = g_hi > g_lo ? g_hi - g_lo : 0;
     int after = OH - before - n_in;
-    BitW bw{slot, 0, 0, 0};
+    BitW bw{slot, stream ? (bit0 >> 5) : 0u, 0, stream ? (int)(bit0 & 31) : 0, stream, true, last};
     const uint32_t wm = mask16(W), am = mask16(e.w);
     // plane loop kept rolled (instruction-cache footprint); the stored plane
     // for `pl` is picked with selects so register indexing stays static.
@@ -366,6 +396,7 @@ __device__ void solo_render(const Params &p, const SoloEnv<DOM> &e, uint32_t *sl
         bw.fill(fill, after * OW);
     }
     bw.flush();
+    if (stream) return;  // stream mode is only used without control planes
     // control planes: (value - (lo+hi)/2) / cap, float64 -> float32 (env.py:224-232)
     float *ctrl = reinterpret_cast<float *>(slot + p.img_words);
     for (int j = 0; j < p.n_ctrl; j++) {
@@ -519,9 +550,46 @@ __device__ void solo_write_noctrl(const Params &p, const uint32_t *wimg, long lo
     }
 }
 
+// Writer for the stream layout: the group's outputs are one bit stream, so a
+// VEC-element group q is bits [q*VEC, q*VEC+VEC) -- one shared-memory word,
+// a lane-constant shift, VEC selects and one store. No env bookkeeping.
+template <int VEC, int U>
+__device__ void solo_write_stream(const Params &p, const uint32_t *st, long long env0, int nenv, int lane,
+                                  int nthr) {
+    float *out = p.obs + (size_t)env0 * p.PE;
+    const uint32_t total = (uint32_t)nenv * p.PE;
+    const uint32_t nv = total / VEC;
+    const uint32_t sh = ((uint32_t)lane * VEC) & 31;  // nthr * VEC is a multiple of 32
+    uint32_t q0 = lane;
+    for (; q0 + (uint32_t)nthr * (U - 1) < nv; q0 += (uint32_t)nthr * U) {
+        uint32_t x[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) x[u] = st[sidx(((q0 + (uint32_t)nthr * u) * VEC) >> 5)] >> sh;
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            float f[8];
+#pragma unroll
+            for (int j = 0; j < VEC; j++) f[j] = ((x[u] >> j) & 1u) ? 1.0f : 0.0f;
+            const size_t q = q0 + (size_t)nthr * u;
+            if constexpr (VEC == 8) st_cs_v8(out + q * 8, f);
+            else __stcs(reinterpret_cast<float4 *>(out) + q, make_float4(f[0], f[1], f[2], f[3]));
+        }
+    }
+    for (uint32_t q = q0; q < nv; q += nthr) {
+        uint32_t x = st[sidx((q * VEC) >> 5)] >> sh;
+        float f[8];
+#pragma unroll
+        for (int j = 0; j < VEC; j++) f[j] = ((x >> j) & 1u) ? 1.0f : 0.0f;
+        if constexpr (VEC == 8) st_cs_v8(out + (size_t)q * 8, f);
+        else __stcs(reinterpret_cast<float4 *>(out) + q, make_float4(f[0], f[1], f[2], f[3]));
+    }
+    for (uint32_t t = nv * VEC + lane; t < total; t += nthr) out[t] = ((st[sidx(t >> 5)] >> (t & 31)) & 1u) ? 1.0f : 0.0f;
+}
+
 // One env, one thread: step / reset / observe, then render its image into `slot`.
 template <int DOM>
-__device__ __forceinline__ void solo_env(const Params &p, int mode, long long env, uint32_t *slot) {
+__device__ __forceinline__ void solo_env(const Params &p, int mode, long long env, uint32_t *slot, uint32_t *img,
+                                         bool stream, uint32_t bit0, bool last) {
     constexpr int N = Dom<DOM>::N;
     SoloEnv<DOM> e;
     solo_load<DOM>(p, env, e);
@@ -622,7 +690,7 @@ __device__ __forceinline__ void solo_env(const Params &p, int mode, long long en
         }
     }
     if (mode != MODE_OBSERVE) solo_store<DOM>(p, env, e, rows_dirty, planes_dirty, metrics_dirty, rng_dirty);
-    if (p.obs) solo_render<DOM>(p, e, slot);
+    if (p.obs) solo_render<DOM>(p, e, img, stream, bit0, last);
     }
 
 template <int DOM>
@@ -636,27 +704,49 @@ __global__ void __launch_bounds__(128, 1) env_solo_kernel(const Params p, int mo
     const int lane = tid & 31, warp = tid >> 5;
     const long long env0 = warp_mode ? (long long)blockIdx.x * T + warp * 32 : (long long)blockIdx.x * E;
     const int local = warp_mode ? lane : tid;
-    uint32_t *img = smem_w + (warp_mode ? (size_t)warp * 32 * p.env_smem : 0);
-    const long long env = env0 + local;
-    if (local < (warp_mode ? 32 : E) && env < p.B) solo_env<DOM>(p, mode, env, img + (size_t)local * p.env_smem);
-    if (!p.obs) return;
-    long long rem = (long long)p.B - env0;
     const int cap = warp_mode ? 32 : E;
+    long long rem = (long long)p.B - env0;
     const int nenv = rem < cap ? (rem > 0 ? (int)rem : 0) : cap;
+    const long long env = env0 + local;
+    const bool valid = local < nenv;
+    const int wl = warp_mode ? lane : tid, nthr = warp_mode ? 32 : T;
+    if (p.stream_mode) {
+        uint32_t *grp = smem_w + (warp_mode ? (size_t)warp * p.group_words : 0);
+        if (p.obs && valid) grp[sidx(((uint32_t)local * p.PE) >> 5)] = 0u;  // shared boundary words
+        if (warp_mode) __syncwarp();
+        else __syncthreads();
+        if (valid) {
+            // union-find scratch: the env's own interior stream words when they
+            // are large enough (written by nobody else before this env renders)
+            uint32_t *uf = p.stream_words == 0 ? grp + sidx((((uint32_t)local * p.PE) >> 5) + 1)
+                                               : grp + p.stream_words + (size_t)local * 33;
+            solo_env<DOM>(p, mode, env, uf, grp, true, (uint32_t)local * p.PE, local == nenv - 1);
+        }
+        if (!p.obs) return;
+        if (warp_mode) __syncwarp();
+        else __syncthreads();
+        if (nenv <= 0) return;
+        if ((reinterpret_cast<uintptr_t>(p.obs + (size_t)env0 * p.PE) & 31) == 0)
+            solo_write_stream<8, 2>(p, grp, env0, nenv, wl, nthr);
+        else
+            solo_write_stream<4, 2>(p, grp, env0, nenv, wl, nthr);
+        return;
+    }
+    uint32_t *img = smem_w + (warp_mode ? (size_t)warp * 32 * p.env_smem : 0);
+    if (valid) {
+        uint32_t *slot = img + (size_t)local * p.env_smem;
+        solo_env<DOM>(p, mode, env, slot, slot, false, 0, false);
+    }
+    if (!p.obs) return;
     if (warp_mode) __syncwarp();
     else __syncthreads();
     if (nenv <= 0) return;
-    const int wl = warp_mode ? lane : tid, nthr = warp_mode ? 32 : T;
     const size_t first = (size_t)env0 * p.PE;
     // obs base is 16-byte aligned (checked on the host) and env0 is a multiple
     // of 8, so every block's output starts 32-byte aligned when the base is.
     if ((reinterpret_cast<uintptr_t>(p.obs + first) & 31) == 0) {
-        if (p.PB == p.PE) {
-            if (p.solo_u == 4) solo_write_noctrl<4>(p, img, env0, nenv, wl, nthr);
-            else solo_write_noctrl<2>(p, img, env0, nenv, wl, nthr);
-        } else {
-            solo_write<8, 2>(p, img, env0, nenv, wl, nthr);
-        }
+        if (p.PB == p.PE) solo_write_noctrl<2>(p, img, env0, nenv, wl, nthr);
+        else solo_write<8, 2>(p, img, env0, nenv, wl, nthr);
     } else {
         solo_write<4, 2>(p, img, env0, nenv, wl, nthr);
     }
@@ -900,7 +990,7 @@ __global__ void __launch_bounds__(512, 1) env_solo_ws_kernel(const Params p, int
             if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
             const long long env = (b + k * G) * 32 + lane;
             uint32_t *slot = smem_w + (size_t)s * slot_words + (size_t)lane * p.env_smem;
-            if (env < p.B) solo_env<DOM>(p, mode, env, slot);
+            if (env < p.B) solo_env<DOM>(p, mode, env, slot, slot, false, 0, false);
             __syncwarp();
             mbar_arrive(&full[s]);
         }
