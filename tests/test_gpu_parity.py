@@ -239,9 +239,13 @@ WARP_MODE_CASES = [
 ]
 
 
+@pytest.mark.parametrize("layout", ["default", "stream", "slot"])
 @pytest.mark.parametrize("case", range(len(WARP_MODE_CASES)))
-def test_large_batch_warp_mode_against_oracle(case):
-    """Batches >= 4 warps/SM take the warp-mode store path; pin it to the oracle."""
+def test_large_batch_warp_mode_against_oracle(case, layout, monkeypatch):
+    """Batches >= 4 warps/SM take the warp-mode store path; pin it to the oracle
+    with both shared-memory layouts (per-env slots, warp-wide bit stream)."""
+    if layout != "default":
+        monkeypatch.setenv("LG_STREAM", "1" if layout == "stream" else "0")
     kw, n, steps = WARP_MODE_CASES[case]
     cfg = EnvConfig(**kw)
     env = BatchEnv(cfg, n, seed=21)
