@@ -171,8 +171,9 @@ __device__ __forceinline__ void solo_set_tile(SoloEnv<DOM> &e, int r, int c, int
             if (k == wi) e.pl[q].w[k] = (e.pl[q].w[k] & ~bit) | (q == tile - 1 ? bit : 0u);
 }
 
+// reset_rows for one env minus its final _recompute (env.py:284-325)
 template <int DOM>
-__device__ __forceinline__ void solo_reset(const Params &p, SoloEnv<DOM> &e, void *uf) {
+__device__ __forceinline__ void solo_reset_setup(const Params &p, SoloEnv<DOM> &e) {
     constexpr int N = Dom<DOM>::N, NPL = Dom<DOM>::NPL, M = Dom<DOM>::M;
     Pcg &g = e.g;
     int h = p.H, w = p.W;
@@ -187,7 +188,7 @@ __device__ __forceinline__ void solo_reset(const Params &p, SoloEnv<DOM> &e, voi
     for (int q = 0; q < NPL; q++) e.pl[q] = SB::zero();
     e.frz = andnot(rect_sb(p.H, p.W), act);
     if (p.weighted) {  // init_random: choice(n_tiles, (h, w), p), row-major (grid.py:169-191)
-#pragma unroll
+#pragma unroll 1
         for (int r = 0; r < 16; r++) {
             if (r < h) {
                 uint32_t rowbits[NPL];
@@ -274,7 +275,7 @@ __device__ __forceinline__ void solo_reset(const Params &p, SoloEnv<DOM> &e, voi
     e.t = 0;
     e.changes = 0;
     e.max_steps = p.max_steps > 0 ? p.max_steps : 3LL * cap;
-    solo_recompute<DOM>(p, e, uf, true);
+    // the caller runs _recompute(reset=True) (env.py:305)
 }
 
 // Sequential bit writer into one env's image slot.
@@ -594,6 +595,8 @@ __device__ __forceinline__ void solo_env(const Params &p, int mode, long long en
     SoloEnv<DOM> e;
     solo_load<DOM>(p, env, e);
     bool rows_dirty = false, planes_dirty = false, metrics_dirty = false, rng_dirty = false;
+    bool wrote = false, reset_now = false;
+    double before = 0.0;
     if (mode == MODE_STEP) {
         long long a = p.actions[env];
         bool ok = a >= 0 && a < p.n_actions;
@@ -618,7 +621,6 @@ __device__ __forceinline__ void solo_env(const Params &p, int mode, long long en
             r = cell / p.W;
             c = cell - r * p.W;
         }
-        bool wrote = false;
         if (tile >= 0) {
             const uint32_t sh = (r & 1) * 16 + c;
             const int wi = r >> 1;
@@ -637,61 +639,67 @@ __device__ __forceinline__ void solo_env(const Params &p, int mode, long long en
             bool editable = act && !fz;
             wrote = tile != cur && (p.rep == REP_NARROW || editable);
         }
-        double reward = 0.0;
-        if (wrote) {
+        if (wrote) {  // env.py:369-372
             solo_set_tile<DOM>(e, r, c, tile);
             planes_dirty = true;
             e.changes += 1;
-            double before = e.prev_loss;
-            solo_recompute<DOM>(p, e, slot, false);
-            reward = __dsub_rn(before, e.prev_loss);
-            metrics_dirty = true;
-            rng_dirty = true;
-        }
-        e.ep_reward = __dadd_rn(e.ep_reward, reward);
-        if (p.rep == REP_NARROW) {  // pos_idx = (pos_idx + 1) % order_len
-            SB ed = andnot(rect_sb(e.h, e.w), e.frz);
-            int nidx = e.pos_idx + 1, nxt;
-            if (nidx >= e.order_len) {
-                nidx = 0;
-                nxt = solo_serp_first(ed, 0);
-            } else {
-                nxt = solo_serp_next(ed, e.pr, e.pc);
-            }
-            e.pos_idx = nidx;
-            e.pr = nxt >> 4;
-            e.pc = nxt & 15;
-        }
-        e.t += 1;
-        bool done = e.t >= e.max_steps;
-        if (p.budget > 0) done |= e.changes >= p.budget;
-        p.reward[env] = reward;
-        p.done[env] = done;
-        if (p.terminal) p.terminal[env] = done;
-        if (p.ep_rew) p.ep_rew[env] = done ? e.ep_reward : 0.0;
-        if (p.ep_len) p.ep_len[env] = done ? e.t : 0;
-        if (p.ep_start) p.ep_start[env] = done ? e.ep_start_loss : 0.0;
-        if (p.fin_loss) p.fin_loss[env] = done ? e.prev_loss : 0.0;
-        if (done && p.stats) {
-            atomicAdd(p.stats + 0, 1.0);
-            atomicAdd(p.stats + 1, e.ep_reward);
-            atomicAdd(p.stats + 2, (double)e.t);
-            atomicAdd(p.stats + 3, e.ep_start_loss);
-            atomicAdd(p.stats + 4, e.prev_loss);
-        }
-        if (done) {
-            solo_reset<DOM>(p, e, slot);
-            rows_dirty = metrics_dirty = rng_dirty = true;
+            before = e.prev_loss;
         }
     } else if (mode == MODE_RESET) {
-        if (!p.reset_mask || p.reset_mask[env]) {
-            solo_reset<DOM>(p, e, slot);
-            rows_dirty = metrics_dirty = rng_dirty = true;
+        reset_now = !p.reset_mask || p.reset_mask[env];
+    }
+    // pass 0: the step's recompute + bookkeeping; pass 1: auto-reset. One
+    // call site for the metric code keeps the kernel's instruction footprint small.
+#pragma unroll 1
+    for (int pass = 0; pass < 2; pass++) {
+        if (pass == 1) {
+            if (!reset_now) break;
+            solo_reset_setup<DOM>(p, e);
+            rows_dirty = true;
+        }
+        if (pass == 1 || wrote) {
+            solo_recompute<DOM>(p, e, slot, pass == 1);  // _recompute (env.py:332-347)
+            metrics_dirty = rng_dirty = true;
+        }
+        if (pass == 0 && mode == MODE_STEP) {
+            double reward = wrote ? __dsub_rn(before, e.prev_loss) : 0.0;
+            e.ep_reward = __dadd_rn(e.ep_reward, reward);
+            if (p.rep == REP_NARROW) {  // pos_idx = (pos_idx + 1) % order_len
+                SB ed = andnot(rect_sb(e.h, e.w), e.frz);
+                int nidx = e.pos_idx + 1, nxt;
+                if (nidx >= e.order_len) {
+                    nidx = 0;
+                    nxt = solo_serp_first(ed, 0);
+                } else {
+                    nxt = solo_serp_next(ed, e.pr, e.pc);
+                }
+                e.pos_idx = nidx;
+                e.pr = nxt >> 4;
+                e.pc = nxt & 15;
+            }
+            e.t += 1;
+            bool done = e.t >= e.max_steps;
+            if (p.budget > 0) done |= e.changes >= p.budget;
+            p.reward[env] = reward;
+            p.done[env] = done;
+            if (p.terminal) p.terminal[env] = done;
+            if (p.ep_rew) p.ep_rew[env] = done ? e.ep_reward : 0.0;
+            if (p.ep_len) p.ep_len[env] = done ? e.t : 0;
+            if (p.ep_start) p.ep_start[env] = done ? e.ep_start_loss : 0.0;
+            if (p.fin_loss) p.fin_loss[env] = done ? e.prev_loss : 0.0;
+            if (done && p.stats) {
+                atomicAdd(p.stats + 0, 1.0);
+                atomicAdd(p.stats + 1, e.ep_reward);
+                atomicAdd(p.stats + 2, (double)e.t);
+                atomicAdd(p.stats + 3, e.ep_start_loss);
+                atomicAdd(p.stats + 4, e.prev_loss);
+            }
+            reset_now = done;
         }
     }
     if (mode != MODE_OBSERVE) solo_store<DOM>(p, env, e, rows_dirty, planes_dirty, metrics_dirty, rng_dirty);
     if (p.obs) solo_render<DOM>(p, e, img, stream, bit0, last);
-    }
+}
 
 template <int DOM>
 __global__ void __launch_bounds__(128, 1) env_solo_kernel(const Params p, int mode) {
@@ -703,25 +711,35 @@ __global__ void __launch_bounds__(128, 1) env_solo_kernel(const Params p, int mo
     // T threads write them.
     const int lane = tid & 31, warp = tid >> 5;
     const long long env0 = warp_mode ? (long long)blockIdx.x * T + warp * 32 : (long long)blockIdx.x * E;
-    const int local = warp_mode ? lane : tid;
+    // block mode deals envs round-robin over the warps (env j -> warp j % nw),
+    // so a warp steps few envs and their divergent paths serialise less.
+    const int nw = T >> 5;
+    const int local = warp_mode ? lane : lane * nw + warp;
     const int cap = warp_mode ? 32 : E;
     long long rem = (long long)p.B - env0;
     const int nenv = rem < cap ? (rem > 0 ? (int)rem : 0) : cap;
     const long long env = env0 + local;
-    const bool valid = local < nenv;
+    const bool valid = local < nenv && (warp_mode || lane < (E + nw - 1) / nw);
     const int wl = warp_mode ? lane : tid, nthr = warp_mode ? 32 : T;
+    uint32_t *grp = smem_w + (warp_mode ? (size_t)warp * (p.stream_mode ? (size_t)p.group_words
+                                                                        : (size_t)32 * p.env_smem)
+                                        : 0);
+    uint32_t *scratch, *img;
     if (p.stream_mode) {
-        uint32_t *grp = smem_w + (warp_mode ? (size_t)warp * p.group_words : 0);
         if (p.obs && valid) grp[sidx(((uint32_t)local * p.PE) >> 5)] = 0u;  // shared boundary words
         if (warp_mode) __syncwarp();
         else __syncthreads();
-        if (valid) {
-            // union-find scratch: the env's own interior stream words when they
-            // are large enough (written by nobody else before this env renders)
-            uint32_t *uf = p.stream_words == 0 ? grp + sidx((((uint32_t)local * p.PE) >> 5) + 1)
-                                               : grp + p.stream_words + (size_t)local * 33;
-            solo_env<DOM>(p, mode, env, uf, grp, true, (uint32_t)local * p.PE, local == nenv - 1);
-        }
+        // union-find scratch: the env's own interior stream words when they
+        // are large enough (written by nobody else before this env renders)
+        scratch = p.stream_words == 0 ? grp + sidx((((uint32_t)local * p.PE) >> 5) + 1)
+                                      : grp + p.stream_words + (size_t)local * 33;
+        img = grp;
+    } else {
+        scratch = img = grp + (size_t)local * p.env_smem;
+    }
+    if (valid)
+        solo_env<DOM>(p, mode, env, scratch, img, p.stream_mode != 0, (uint32_t)local * p.PE, local == nenv - 1);
+    if (p.stream_mode) {
         if (!p.obs) return;
         if (warp_mode) __syncwarp();
         else __syncthreads();
@@ -732,11 +750,7 @@ __global__ void __launch_bounds__(128, 1) env_solo_kernel(const Params p, int mo
             solo_write_stream<4, 2>(p, grp, env0, nenv, wl, nthr);
         return;
     }
-    uint32_t *img = smem_w + (warp_mode ? (size_t)warp * 32 * p.env_smem : 0);
-    if (valid) {
-        uint32_t *slot = img + (size_t)local * p.env_smem;
-        solo_env<DOM>(p, mode, env, slot, slot, false, 0, false);
-    }
+    img = grp;
     if (!p.obs) return;
     if (warp_mode) __syncwarp();
     else __syncthreads();
