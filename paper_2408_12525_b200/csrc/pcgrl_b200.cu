@@ -536,7 +536,7 @@ extern "C" int lg_create(const lg_config *cfg, int64_t n_envs, int64_t global_of
     // latency-bound work: splitting each env over a 16-lane team shortens the
     // per-env dependency chain (measured c2, 4096 envs: 92M vs 56M env-steps/s).
     if (e->geo == 1 && n_envs >= 1024 && n_envs < 148LL * 4 * 32 && !getenv("LG_SOLO_MID"))
-        e->geo = pick_geo(17, W);
+        e->geo = 16;  // lane team of 16, one row per lane (H <= 16)
     if (e->geo == 1) {
         // one env per thread; per-env shared slot (in 32-bit words): bit image +
         // 8 control floats, >= 33 words (union-find scratch), odd stride so the
