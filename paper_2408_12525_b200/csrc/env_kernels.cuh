@@ -100,7 +100,6 @@ struct Params {
     int env_smem;   // shared memory per env: bytes (team kernel) or 32-bit words (solo)
     int solo_E;     // solo kernel: envs per block (== blockDim: warp mode)
     int solo_u;     // solo kernel: stores in flight per lane in the obs writer (2 or 4)
-    int ws_producers, ws_consumers, ws_slots;  // warp-specialised solo kernel (0 = off)
     int stream_mode;   // solo: envs of a warp/block rendered into one contiguous bit stream
     int group_words;   // solo stream mode: shared words per warp (warp mode) or block
     int stream_words;  // solo stream mode: offset of the union-find scratch in a group

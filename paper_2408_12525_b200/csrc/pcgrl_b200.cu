@@ -282,7 +282,6 @@ struct lg_env {
     int team, threads, E;
     int N, M, NPL, C, OH, OW;
     long long n_actions;
-    int ws_grid = 0;
     size_t row_bytes, rows_per_env;
     Params base;
     size_t smem;
@@ -329,24 +328,7 @@ static int launch_env_t(lg_env *e, const Params &p, int mode, cudaStream_t s) {
 }
 
 template <int DOM>
-static int launch_solo_ws_t(lg_env *e, const Params &p, int mode, cudaStream_t s) {
-    static std::once_flag once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(once, [] {
-        attr_err = cudaFuncSetAttribute(env_solo_ws_kernel<DOM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        227 * 1024);
-    });
-    CU(attr_err);
-    int threads = 32 * (p.ws_producers + p.ws_consumers);
-    size_t smem = (size_t)p.ws_slots * 32 * p.env_smem * 4 + (size_t)p.ws_slots * 16;
-    env_solo_ws_kernel<DOM><<<e->ws_grid, threads, smem, s>>>(p, mode);
-    CU(cudaGetLastError());
-    return LG_OK;
-}
-
-template <int DOM>
 static int launch_solo_t(lg_env *e, const Params &p, int mode, cudaStream_t s) {
-    if (p.ws_slots > 0 && p.obs) return launch_solo_ws_t<DOM>(e, p, mode, s);
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [] {
@@ -563,6 +545,33 @@ extern "C" int lg_create(const lg_config *cfg, int64_t n_envs, int64_t global_of
         }
         p.solo_E = e->E;
         e->smem = (size_t)e->E * slot * 4;
+        // stream layout (no control planes): one bit stream per warp. Measured
+        // faster when env boundaries are word aligned (c3: +21%), slower
+        // otherwise (c5: -5%, c2 block mode: -30%); LG_STREAM=0/1 overrides.
+        const char *sm = getenv("LG_STREAM");
+        bool want_stream = (p.PE % 32 == 0) && e->E == e->threads;
+        if (sm) want_stream = sm[0] == '1';
+        if (p.PB == p.PE && want_stream) {
+            int G = e->E == e->threads ? 32 : e->E;
+            int sw = (int)(((long long)G * p.PE + 31) / 32 + 1);
+            sw = sw + sw / 32 + 1;  // swizzle pad words (sidx)
+            sw = (sw + 3) & ~3;
+            int gw;
+            if ((int)(p.PE / 32) - 2 >= 36) {  // union-find scratch fits in each env's own words
+                gw = sw;
+                sw = 0;
+            } else {
+                gw = sw + G * 33;
+            }
+            gw = (gw + 3) & ~3;
+            size_t bytes = (size_t)gw * 4 * (e->E == e->threads ? e->threads / 32 : 1);
+            if (bytes <= 200 * 1024) {
+                p.stream_mode = 1;
+                p.stream_words = sw;  // 0: scratch inside the env's own stream words
+                p.group_words = gw;
+                e->smem = bytes;
+            }
+        }
         // stream layout (no control planes): one bit stream per warp. Measured
         // faster when env boundaries are word aligned (c3: +21%), slower
         // otherwise (c5: -5%, c2 block mode: -30%); LG_STREAM=0/1 overrides.

@@ -947,88 +947,4 @@ __global__ void __launch_bounds__(128) solo_metrics_kernel(long long n, int H, i
     }
 }
 
-// ---------------------------------------------------------------------------
-// Warp-specialised persistent variant: P producer warps step 32 envs each and
-// render their images into a ring of S shared-memory slots; C consumer warps
-// stream every filled slot to HBM. full/empty mbarriers hand slots over, so
-// stores never wait for a slow environment and steps never wait for stores.
-// ---------------------------------------------------------------------------
-
-__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
-                 "r"(count)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile(
-        "{\n\t.reg .b64 st;\n\tmbarrier.arrive.release.cta.shared::cta.b64 st, [%0];\n\t}" ::"r"(
-            (unsigned)__cvta_generic_to_shared(bar))
-        : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
-    unsigned addr = (unsigned)__cvta_generic_to_shared(bar);
-    unsigned done = 0;
-    while (!done) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(addr), "r"(parity)
-            : "memory");
-    }
-}
-
-template <int DOM>
-__global__ void __launch_bounds__(512, 1) env_solo_ws_kernel(const Params p, int mode) {
-    extern __shared__ __align__(16) uint32_t smem_w[];
-    const int P = p.ws_producers, C = p.ws_consumers, S = p.ws_slots;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const size_t slot_words = (size_t)32 * p.env_smem;
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem_w + (size_t)S * slot_words);
-    uint64_t *empty = full + S;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < S; s++) {
-            mbar_init(&full[s], 32);
-            mbar_init(&empty[s], C);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    const long long ntiles = ((long long)p.B + 31) / 32;
-    const long long G = gridDim.x, b = blockIdx.x;
-    const long long mine = b < ntiles ? (ntiles - b + G - 1) / G : 0;  // tiles b, b+G, ...
-    if (warp < P) {
-        for (long long k = warp; k < mine; k += P) {
-            const int s = (int)(k % S);
-            const unsigned round = (unsigned)(k / S);
-            if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
-            const long long env = (b + k * G) * 32 + lane;
-            uint32_t *slot = smem_w + (size_t)s * slot_words + (size_t)lane * p.env_smem;
-            if (env < p.B) solo_env<DOM>(p, mode, env, slot, slot, false, 0, false);
-            __syncwarp();
-            mbar_arrive(&full[s]);
-        }
-    } else {
-        const int cw = warp - P;
-        for (long long k = 0; k < mine; k++) {
-            const int s = (int)(k % S);
-            mbar_wait(&full[s], (unsigned)(k / S) & 1);
-            const long long env0 = (b + k * G) * 32;
-            long long rem = (long long)p.B - env0;
-            const int nenv = rem < 32 ? (int)rem : 32;
-            const uint32_t *img = smem_w + (size_t)s * slot_words;
-            if (p.obs && nenv > 0) {
-                if ((reinterpret_cast<uintptr_t>(p.obs + (size_t)env0 * p.PE) & 31) == 0 && p.PB == p.PE)
-                    solo_write_noctrl<4>(p, img, env0, nenv, cw * 32 + lane, C * 32);
-                else if ((reinterpret_cast<uintptr_t>(p.obs + (size_t)env0 * p.PE) & 31) == 0)
-                    solo_write<8, 2>(p, img, env0, nenv, cw * 32 + lane, C * 32);
-                else
-                    solo_write<4, 2>(p, img, env0, nenv, cw * 32 + lane, C * 32);
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
-        }
-    }
-}
-
 }  // namespace lg
