@@ -99,7 +99,6 @@ struct Params {
     int img_words;  // u32 words of one env's bit image (incl. 1 pad word)
     int env_smem;   // shared memory per env: bytes (team kernel) or 32-bit words (solo)
     int solo_E;     // solo kernel: envs per block (== blockDim: warp mode)
-    int solo_u;     // solo kernel: stores in flight per lane in the obs writer (2 or 4)
     int stream_mode;   // solo: envs of a warp/block rendered into one contiguous bit stream
     int group_words;   // solo stream mode: shared words per warp (warp mode) or block
     int stream_words;  // solo stream mode: offset of the union-find scratch in a group

@@ -531,8 +531,6 @@ extern "C" int lg_create(const lg_config *cfg, int64_t n_envs, int64_t global_of
         const char *tb = getenv("LG_SOLO_THREADS");
         int warp_threads = tb ? atoi(tb) : 64;
         if (warp_threads != 32 && warp_threads != 64 && warp_threads != 128) warp_threads = 64;
-        const char *su = getenv("LG_SOLO_U");
-        p.solo_u = su && atoi(su) == 4 ? 4 : 2;
         if (n_envs >= 148LL * 4 * 32) {  // >= 4 warps per SM: each warp writes its own 32 envs
             e->threads = warp_threads;
             e->E = warp_threads;
@@ -570,50 +568,6 @@ extern "C" int lg_create(const lg_config *cfg, int64_t n_envs, int64_t global_of
                 p.stream_words = sw;  // 0: scratch inside the env's own stream words
                 p.group_words = gw;
                 e->smem = bytes;
-            }
-        }
-        // stream layout (no control planes): one bit stream per warp. Measured
-        // faster when env boundaries are word aligned (c3: +21%), slower
-        // otherwise (c5: -5%, c2 block mode: -30%); LG_STREAM=0/1 overrides.
-        const char *sm = getenv("LG_STREAM");
-        bool want_stream = (p.PE % 32 == 0) && e->E == e->threads;
-        if (sm) want_stream = sm[0] == '1';
-        if (p.PB == p.PE && want_stream) {
-            int G = e->E == e->threads ? 32 : e->E;
-            int sw = (int)(((long long)G * p.PE + 31) / 32 + 1);
-            sw = sw + sw / 32 + 1;  // swizzle pad words (sidx)
-            sw = (sw + 3) & ~3;
-            int gw;
-            if ((int)(p.PE / 32) - 2 >= 36) {  // union-find scratch fits in each env's own words
-                gw = sw;
-                sw = 0;
-            } else {
-                gw = sw + G * 33;
-            }
-            gw = (gw + 3) & ~3;
-            size_t bytes = (size_t)gw * 4 * (e->E == e->threads ? e->threads / 32 : 1);
-            if (bytes <= 200 * 1024) {
-                p.stream_mode = 1;
-                p.stream_words = sw;  // 0: scratch inside the env's own stream words
-                p.group_words = gw;
-                e->smem = bytes;
-            }
-        }
-        // warp-specialised persistent variant (LG_WS=producers,consumers[,slots])
-        const char *ws = getenv("LG_WS");
-        if (ws && n_envs >= 148LL * 32 * 4) {
-            int P = 0, C = 0, S = 0;
-            if (sscanf(ws, "%d,%d,%d", &P, &C, &S) < 2) P = C = 0;
-            size_t slot_bytes = (size_t)32 * slot * 4;
-            int smax = (int)((225 * 1024) / (slot_bytes + 16));
-            if (S <= 0 || S > smax) S = smax;
-            if (P > 0 && C > 0 && P + C <= 16 && S >= 2) {
-                p.ws_producers = P;
-                p.ws_consumers = C;
-                p.ws_slots = S;
-                int dev_sms = 148;
-                cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device);
-                e->ws_grid = dev_sms;
             }
         }
         if (e->OW > 64 || e->smem > 200 * 1024) e->geo = pick_geo(17, W);  // too wide: lane teams
