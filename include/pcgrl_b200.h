@@ -123,6 +123,11 @@ int lg_reset_masked(lg_env *env, const uint8_t *mask_dev, float *obs_dev, void *
  * sum final loss (the per-GPU input of the NCCL stats all-reduce). */
 int lg_step(lg_env *env, const int64_t *actions_dev, float *obs_dev, double *reward_dev,
             uint8_t *done_dev, const lg_info *info, double *stats_dev, void *stream);
+/* lg_step with flags: LG_STEP_NO_AUTO_RESET leaves finished envs as they are
+ * (the scalar facade's _Core.step(auto_reset=False), env.py:611-630). */
+#define LG_STEP_NO_AUTO_RESET 1u
+int lg_step_flags(lg_env *env, const int64_t *actions_dev, float *obs_dev, double *reward_dev,
+                  uint8_t *done_dev, const lg_info *info, double *stats_dev, uint32_t flags, void *stream);
 /* BatchEnv.observe (env.py:587-588). */
 int lg_observe(lg_env *env, float *obs_dev, void *stream);
 /* The same step with HOST buffers: H2D of actions and D2H of every output

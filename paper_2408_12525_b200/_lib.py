@@ -13,6 +13,7 @@ LIB_PATH = os.path.join(_PKG, "libpcgrl_b200.so")
 
 LG_OK, LG_EINVAL, LG_ECUDA = 0, 1, 2
 FLAG_BAD_ACTION, FLAG_NO_EDITABLE, FLAG_PINPOINTS = 1, 2, 4
+STEP_NO_AUTO_RESET = 1
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
@@ -64,6 +65,8 @@ SIGNATURES = {
     "lg_reset": (ctypes.c_int, [_P, _P, _P]),
     "lg_reset_masked": (ctypes.c_int, [_P, _P, _P, _P]),
     "lg_step": (ctypes.c_int, [_P, _P, _P, _P, _P, ctypes.POINTER(LgInfo), _P, _P]),
+    "lg_step_flags": (ctypes.c_int, [_P, _P, _P, _P, _P, ctypes.POINTER(LgInfo), _P, ctypes.c_uint32,
+                                     _P]),
     "lg_observe": (ctypes.c_int, [_P, _P, _P]),
     "lg_step_host": (ctypes.c_int, [_P, _P, _P, _P, _P, ctypes.POINTER(LgInfo), _P]),
     "lg_export_state": (ctypes.c_int, [_P, ctypes.POINTER(LgState), _P]),

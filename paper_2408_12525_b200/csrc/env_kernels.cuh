@@ -99,6 +99,7 @@ struct Params {
     int img_words;  // u32 words of one env's bit image (incl. 1 pad word)
     int env_smem;   // shared memory per env: bytes (team kernel) or 32-bit words (solo)
     int solo_E;     // solo kernel: envs per block (== blockDim: warp mode)
+    int no_auto_reset;  // scalar step (env.py:611-630): finished envs are not reset
     int stream_mode;   // solo: envs of a warp/block rendered into one contiguous bit stream
     int group_words;   // solo stream mode: shared words per warp (warp mode) or block
     int stream_words;  // solo stream mode: offset of the union-find scratch in a group
@@ -852,7 +853,7 @@ __global__ void __launch_bounds__(256) env_kernel(const Params p, int mode) {
                     atomicAdd(p.stats + 4, e.prev_loss);
                 }
             }
-            if (done) {
+            if (done && !p.no_auto_reset) {
                 reset_env<G, DOM>(p, t, e, uf);
                 rows_dirty = metrics_dirty = rng_dirty = true;
             }

@@ -669,7 +669,8 @@ static int check_obs_ptr(const float *obs) {
 }
 
 static int run_mode(lg_env *e, int mode, const long long *actions, float *obs, double *reward,
-                    uint8_t *done, const lg_info *info, double *stats, const uint8_t *mask, void *stream) {
+                    uint8_t *done, const lg_info *info, double *stats, const uint8_t *mask, void *stream,
+                    unsigned flags = 0) {
     if (!e) {
         set_err("null env");
         return LG_EINVAL;
@@ -694,6 +695,7 @@ static int run_mode(lg_env *e, int mode, const long long *actions, float *obs, d
     }
     p.stats = stats;
     p.reset_mask = mask;
+    p.no_auto_reset = (flags & LG_STEP_NO_AUTO_RESET) ? 1 : 0;
     return launch_env(e, p, mode, (cudaStream_t)stream);
 }
 
@@ -714,6 +716,12 @@ extern "C" int lg_step(lg_env *e, const int64_t *actions, float *obs, double *re
                        const lg_info *info, double *stats, void *stream) {
     return run_mode(e, MODE_STEP, (const long long *)actions, obs, reward, done, info, stats, nullptr,
                     stream);
+}
+
+extern "C" int lg_step_flags(lg_env *e, const int64_t *actions, float *obs, double *reward, uint8_t *done,
+                             const lg_info *info, double *stats, uint32_t flags, void *stream) {
+    return run_mode(e, MODE_STEP, (const long long *)actions, obs, reward, done, info, stats, nullptr,
+                    stream, flags);
 }
 
 extern "C" int lg_step_host(lg_env *e, const int64_t *actions_host, float *obs_host, double *reward_host,

@@ -694,7 +694,7 @@ __device__ __forceinline__ void solo_env(const Params &p, int mode, long long en
                 atomicAdd(p.stats + 3, e.ep_start_loss);
                 atomicAdd(p.stats + 4, e.prev_loss);
             }
-            reset_now = done;
+            reset_now = done && !p.no_auto_reset;
         }
     }
     if (mode != MODE_OBSERVE) solo_store<DOM>(p, env, e, rows_dirty, planes_dirty, metrics_dirty, rng_dirty);

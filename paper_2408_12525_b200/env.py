@@ -307,9 +307,29 @@ class BatchEnv:
         else:
             self._started = True
 
+    def snapshot(self, i: int):
+        """``EnvState`` of env ``i`` (reference env.py:527-528)."""
+        from .scalar import _state_from_row
+        return _state_from_row(self._cfg, _row(self.state_dict(), i), done=False)
+
     def grid_view(self, i: int):
-        sd = self.state_dict()
-        return {"tiles": sd["tiles"][i], "active": sd["active"][i], "frozen": sd["frozen"][i]}
+        """``TileGrid`` of env ``i`` (reference env.py:530-531)."""
+        return self.snapshot(i).grid
+
+
+def _row(sd: dict, i: int) -> dict:
+    """Slice a batch state_dict down to env ``i`` (B = 1)."""
+    out = {}
+    for k, v in sd.items():
+        if k == "rng_states":
+            out[k] = [v[i]]
+        elif k == "started":
+            out[k] = v
+        elif k in ("lo", "hi", "values", "unreach"):
+            out[k] = v[:, i:i + 1]
+        else:
+            out[k] = v[i:i + 1]
+    return out
 
 
 def _np_of():
