@@ -135,6 +135,12 @@ int lg_observe(lg_env *env, float *obs_dev, void *stream);
 int lg_step_host(lg_env *env, const int64_t *actions_host, float *obs_host, double *reward_host,
                  uint8_t *done_host, const lg_info *info_host, void *stream);
 
+/* Designer edits on imported states: recompute metrics + loss of the masked
+ * envs (mask NULL = all) after their tiles/frozen planes changed (with_pin /
+ * without_pin, env.py:657-667,684-715), or with reprice_only=1 only the loss
+ * after a target change (with_target, env.py:670-681). */
+int lg_recompute(lg_env *env, const uint8_t *mask_dev, int reprice_only, void *stream);
+
 /* BatchEnv.state_dict / load_state_dict (env.py:535-585), device buffers. */
 int lg_export_state(lg_env *env, const lg_state *dst_dev, void *stream);
 int lg_import_state(lg_env *env, const lg_state *src_dev, void *stream);

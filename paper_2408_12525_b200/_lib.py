@@ -68,6 +68,7 @@ SIGNATURES = {
     "lg_step_flags": (ctypes.c_int, [_P, _P, _P, _P, _P, ctypes.POINTER(LgInfo), _P, ctypes.c_uint32,
                                      _P]),
     "lg_observe": (ctypes.c_int, [_P, _P, _P]),
+    "lg_recompute": (ctypes.c_int, [_P, _P, ctypes.c_int, _P]),
     "lg_step_host": (ctypes.c_int, [_P, _P, _P, _P, _P, ctypes.POINTER(LgInfo), _P]),
     "lg_export_state": (ctypes.c_int, [_P, ctypes.POINTER(LgState), _P]),
     "lg_import_state": (ctypes.c_int, [_P, ctypes.POINTER(LgState), _P]),

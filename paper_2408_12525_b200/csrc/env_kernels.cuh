@@ -25,7 +25,9 @@
 
 namespace lg {
 
-enum { MODE_STEP = 0, MODE_RESET = 1, MODE_OBSERVE = 2 };
+// MODE_RECOMPUTE: metrics + loss after a designer edit (env.py:684-715);
+// MODE_REPRICE: loss only, after a target change (env.py:670-681).
+enum { MODE_STEP = 0, MODE_RESET = 1, MODE_OBSERVE = 2, MODE_RECOMPUTE = 3, MODE_REPRICE = 4 };
 enum { REP_NARROW = 0, REP_TURTLE = 1, REP_WIDE = 2 };
 enum { FLAG_BAD_ACTION = 1, FLAG_NO_EDITABLE = 2, FLAG_PINPOINTS = 4 };
 
@@ -862,6 +864,13 @@ __global__ void __launch_bounds__(256) env_kernel(const Params p, int mode) {
                 reset_env<G, DOM>(p, t, e, uf);
                 rows_dirty = metrics_dirty = rng_dirty = true;
             }
+        } else if (mode == MODE_RECOMPUTE) {
+            if (!p.reset_mask || p.reset_mask[env]) {
+                recompute<G, DOM>(p, t, e, uf, false);
+                metrics_dirty = rng_dirty = true;
+            }
+        } else if (mode == MODE_REPRICE) {
+            if (!p.reset_mask || p.reset_mask[env]) e.prev_loss = loss_of<DOM>(p, e.val, e.unr, e.lo, e.hi);
         }
         if (mode != MODE_OBSERVE) store_env<G, DOM>(p, t, env, e, rows_dirty, dirty_row, metrics_dirty, rng_dirty);
         if (p.obs) {

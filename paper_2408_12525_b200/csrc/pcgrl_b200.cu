@@ -705,6 +705,11 @@ extern "C" int lg_reset(lg_env *e, float *obs, void *stream) {
 extern "C" int lg_reset_masked(lg_env *e, const uint8_t *mask, float *obs, void *stream) {
     return run_mode(e, MODE_RESET, nullptr, obs, nullptr, nullptr, nullptr, nullptr, mask, stream);
 }
+extern "C" int lg_recompute(lg_env *e, const uint8_t *mask, int reprice_only, void *stream) {
+    return run_mode(e, reprice_only ? MODE_REPRICE : MODE_RECOMPUTE, nullptr, nullptr, nullptr, nullptr, nullptr,
+                    nullptr, mask, stream);
+}
+
 extern "C" int lg_observe(lg_env *e, float *obs, void *stream) {
     if (!obs) {
         set_err("observe needs an output buffer");

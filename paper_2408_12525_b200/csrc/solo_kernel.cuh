@@ -647,6 +647,10 @@ __device__ __forceinline__ void solo_env(const Params &p, int mode, long long en
         }
     } else if (mode == MODE_RESET) {
         reset_now = !p.reset_mask || p.reset_mask[env];
+    } else if (mode == MODE_RECOMPUTE) {
+        wrote = !p.reset_mask || p.reset_mask[env];  // recompute without a write
+    } else if (mode == MODE_REPRICE) {
+        if (!p.reset_mask || p.reset_mask[env]) e.prev_loss = loss_of<DOM>(p, e.val, e.unr, e.lo, e.hi);
     }
     // pass 0: the step's recompute + bookkeeping; pass 1: auto-reset. One
     // call site for the metric code keeps the kernel's instruction footprint small.

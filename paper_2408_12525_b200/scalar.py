@@ -238,3 +238,96 @@ def next_pos(state: EnvState) -> tuple[int, int]:
         raise ValueError("episode is done")
     nxt = int(state.order[(state.pos_idx + 1) % state.order.size])
     return divmod(nxt, state.grid.tiles.shape[1])
+
+
+# ---------------------------------------------------------------------------
+# designer edits (reference env.py:657-715): host bookkeeping of the scan
+# order, metrics and loss recomputed by the CUDA kernels (lg_recompute)
+# ---------------------------------------------------------------------------
+
+
+def _scan_order(active: np.ndarray, frozen: np.ndarray) -> np.ndarray:
+    """Editable cells in boustrophedon order (reference env.py:155-178)."""
+    h, w = active.shape
+    out = []
+    for r in range(h):
+        cols = range(w) if r % 2 == 0 else range(w - 1, -1, -1)
+        out.extend(r * w + c for c in cols if active[r, c] and not frozen[r, c])
+    return np.array(out, dtype=np.int32)
+
+
+def _serp_rank(h: int, w: int) -> np.ndarray:
+    rank = np.empty(h * w, dtype=np.int64)
+    k = 0
+    for r in range(h):
+        for c in (range(w) if r % 2 == 0 else range(w - 1, -1, -1)):
+            rank[r * w + c] = k
+            k += 1
+    return rank
+
+
+def _device_recompute(state: EnvState, reprice_only: bool) -> EnvState:
+    env = _env_for(state.config)
+    env.load_state_dict(_row_from_state(state))
+    t = env._torch
+    with t.cuda.device(env.device):
+        _lib.check(_lib.load().lg_recompute(env.handle, None, int(reprice_only),
+                                            ctypes.c_void_p(t.cuda.current_stream(env.device).cuda_stream)))
+    return _state_from_row(state.config, env.state_dict(), done=state.done)
+
+
+def _after_grid_edit(state: EnvState, tiles: np.ndarray, frozen: np.ndarray) -> EnvState:
+    active = state.grid.active
+    order = _scan_order(active, frozen)
+    if order.size == 0:
+        raise ValueError("edit would leave no editable cells")
+    h, w = tiles.shape
+    rank = _serp_rank(h, w)
+    old_cell = int(state.order[state.pos_idx])
+    pos_idx = int(np.searchsorted(rank[order], rank[old_cell])) % order.size  # same cell or next
+    flat = int(order[pos_idx])
+    edited = EnvState(**{**state.__dict__, "grid": TileGrid(state.grid.domain, tiles, active, frozen),
+                         "order": order, "pos_idx": pos_idx, "pos": divmod(flat, w)})
+    return _device_recompute(edited, reprice_only=False)
+
+
+def _pin_checks(state: EnvState, row: int, col: int):
+    g = state.grid
+    if not (0 <= row < g.tiles.shape[0] and 0 <= col < g.tiles.shape[1]) or not g.active[row, col]:
+        raise ValueError(f"cell ({row}, {col}) is not inside the active map")
+
+
+def with_pin(state: EnvState, row: int, col: int, tile) -> EnvState:
+    """Pin a tile mid-episode (reference env.py:657-661, grid.pin_cell)."""
+    d = state.config.domain_obj
+    tid = d.tile_id(tile) if isinstance(tile, str) else int(tile)
+    if d.tile_name(tid) not in d.pivotal:
+        raise ValueError(f"tile {d.tile_name(tid)!r} is not pinnable in domain {d.name!r}")
+    _pin_checks(state, row, col)
+    tiles, frozen = state.grid.tiles.copy(), state.grid.frozen.copy()
+    tiles[row, col] = tid
+    frozen[row, col] = True
+    return _after_grid_edit(state, tiles, frozen)
+
+
+def without_pin(state: EnvState, row: int, col: int) -> EnvState:
+    """Release a pinned cell back into the scan (reference env.py:664-667)."""
+    _pin_checks(state, row, col)
+    if not state.grid.frozen[row, col]:
+        raise ValueError(f"cell ({row}, {col}) is not pinned")
+    frozen = state.grid.frozen.copy()
+    frozen[row, col] = False
+    return _after_grid_edit(state, state.grid.tiles.copy(), frozen)
+
+
+def with_target(state: EnvState, metric: str, value: int) -> EnvState:
+    """Point target for one metric, loss repriced (reference env.py:670-681)."""
+    d = state.config.domain_obj
+    if metric not in d.metric_names:
+        raise ValueError(f"unknown metric {metric!r}")
+    cap = state.shape.area
+    if not 0 <= value <= cap:
+        raise ValueError(f"target {value} outside [0, {cap}]")
+    targets = dict(state.targets)
+    targets[metric] = (int(value), int(value))
+    return _device_recompute(EnvState(**{**state.__dict__, "targets": targets}), reprice_only=True)
