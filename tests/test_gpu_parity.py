@@ -287,3 +287,64 @@ def test_full_size_c5_properties():
         po, pr, _, _ = part.step(env2_a[lo:lo + cnt].contiguous())
     assert torch.equal(po, obs[lo:lo + cnt])
     assert torch.equal(pr, r[lo:lo + cnt])
+
+
+def _random_config(rng):
+    domain = ["binary", "maze", "dungeon"][int(rng.integers(3))]
+    d = {"binary": ("diameter", "regions"),
+         "maze": ("path_length", "regions", "n_player", "n_door"),
+         "dungeon": ("pkd_path", "regions", "n_player", "n_key", "n_door", "n_enemy", "nearest_enemy")}[domain]
+    piv = {"binary": (), "maze": ("player", "door"), "dungeon": ("player", "key", "door")}[domain]
+    H, W = int(rng.integers(3, 65)), int(rng.integers(3, 65))
+    if rng.random() < 0.5:
+        H, W = int(rng.integers(3, 17)), int(rng.integers(3, 17))
+    kw = dict(domain=domain, max_height=H, max_width=W,
+              obs_size=int(rng.integers(3, min(128, 2 * max(H, W) - 1) + 1)),
+              randomize_shape=bool(rng.random() < 0.5),
+              representation=["narrow", "turtle", "wide"][int(rng.integers(3))],
+              deterministic_metrics=bool(rng.random() < 0.3))
+    if piv and rng.random() < 0.6:
+        kw["pinpoints"] = tuple(rng.choice(piv, size=int(rng.integers(1, 4))))
+    if rng.random() < 0.4:
+        kw["controllable"] = tuple(sorted(set(rng.choice(d, size=int(rng.integers(1, 3))))))
+    if rng.random() < 0.3:
+        kw["init_mode"] = "weighted"
+    if rng.random() < 0.3:
+        kw["change_budget"] = int(rng.integers(1, 20))
+    if rng.random() < 0.3:
+        kw["max_steps"] = int(rng.integers(1, 60))
+    if rng.random() < 0.3:
+        kw["loss_weights"] = {m: float(rng.choice([0.5, 2.0, 0.25, 3.0])) for m in d[:2]}
+    return EnvConfig(**kw)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_config_fuzz_against_oracle(seed):
+    """Random EnvConfigs (all domains/representations, 3..64 sides, windows up
+    to 128, pins, controls, budgets, weights, deterministic metrics)."""
+    rng = np.random.default_rng(1000 + seed)
+    cfg = _random_config(rng)
+    n = int(rng.integers(1, 300))
+    env = BatchEnv(cfg, n, seed=seed)
+    ref = O.OracleBatchEnv(cfg, n, seed=seed)
+    try:
+        o2 = ref.reset()
+    except ValueError:
+        with pytest.raises(ValueError):
+            env.reset()
+        return
+    assert np.array_equal(_np(env.reset()), o2), cfg
+    act = np.random.default_rng(seed)
+    for t in range(40):
+        a = act.integers(0, cfg.n_actions, size=n)
+        try:
+            o2, r2, d2, i2 = ref.step(a)
+        except ValueError:  # e.g. an auto-reset that cannot place its pinpoints
+            return
+        o1, r1, d1, i1 = env.step(a)
+        assert np.array_equal(_np(r1), r2), (cfg, t)
+        assert np.array_equal(_np(d1), d2), (cfg, t)
+        assert np.array_equal(_np(o1), o2), (cfg, t)
+    s1, s2 = env.state_dict(), ref.state_dict()
+    for k in ("tiles", "frozen", "values", "unreach", "prev_loss", "rng", "t", "pos_idx"):
+        assert np.array_equal(s1[k], s2[k]), (cfg, k)
