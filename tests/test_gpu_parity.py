@@ -318,7 +318,7 @@ def _random_config(rng):
     return EnvConfig(**kw)
 
 
-@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("seed", range(64))
 def test_random_config_fuzz_against_oracle(seed):
     """Random EnvConfigs (all domains/representations, 3..64 sides, windows up
     to 128, pins, controls, budgets, weights, deterministic metrics)."""
