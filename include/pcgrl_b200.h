@@ -41,6 +41,10 @@ extern "C" {
 
 enum { LG_BINARY = 0, LG_MAZE = 1, LG_DUNGEON = 2 };
 enum { LG_NARROW = 0, LG_TURTLE = 1, LG_WIDE = 2 };
+/* Observation buffers are float32 [B][C][OH][OW] as in the reference
+ * (env.py:186-233); LG_OBS_U8 writes the same 0/1 planes as uint8 (4x fewer
+ * bytes for GPU-side consumers; configs without control planes only). */
+enum { LG_OBS_F32 = 0, LG_OBS_U8 = 1 };
 
 /* EnvConfig (env.py:42-124) flattened; built by the Python mirror. */
 typedef struct {
@@ -57,7 +61,7 @@ typedef struct {
     int64_t max_steps;       /* 0: 3 * episode area */
     int64_t change_budget;   /* 0: unlimited */
     int32_t det_metrics;     /* deterministic_metrics */
-    int32_t _pad;
+    int32_t obs_format;      /* LG_OBS_F32 (reference) | LG_OBS_U8 (opt-in, no controls) */
     double init_cdf[8];      /* numpy choice cdf over the writable tiles */
     double weights[8];       /* loss weight per metric, canonical order */
 } lg_config;
@@ -113,26 +117,26 @@ int lg_destroy(lg_env *env);
 int lg_describe(const lg_env *env, lg_desc *out);
 
 /* BatchEnv.reset (env.py:516-519). obs_dev may be NULL. */
-int lg_reset(lg_env *env, float *obs_dev, void *stream);
+int lg_reset(lg_env *env, void *obs_dev, void *stream);
 /* _Core.reset_rows on a subset: mask_dev[b] != 0 resets env b (env.py:284-305). */
-int lg_reset_masked(lg_env *env, const uint8_t *mask_dev, float *obs_dev, void *stream);
-/* BatchEnv.step (env.py:521-525): actions_dev int64[B]; obs_dev f32[B,C,OH,OW]
+int lg_reset_masked(lg_env *env, const uint8_t *mask_dev, void *obs_dev, void *stream);
+/* BatchEnv.step (env.py:521-525): actions_dev int64[B]; obs_dev [B,C,OH,OW]
  * (may be NULL to skip the observation), reward_dev f64[B], done_dev u8[B];
  * info may be NULL; stats_dev (NULL or f64[5]) accumulates, over finished
  * episodes: count, sum episode_reward, sum episode_length, sum start loss,
  * sum final loss (the per-GPU input of the NCCL stats all-reduce). */
-int lg_step(lg_env *env, const int64_t *actions_dev, float *obs_dev, double *reward_dev,
+int lg_step(lg_env *env, const int64_t *actions_dev, void *obs_dev, double *reward_dev,
             uint8_t *done_dev, const lg_info *info, double *stats_dev, void *stream);
 /* lg_step with flags: LG_STEP_NO_AUTO_RESET leaves finished envs as they are
  * (the scalar facade's _Core.step(auto_reset=False), env.py:611-630). */
 #define LG_STEP_NO_AUTO_RESET 1u
-int lg_step_flags(lg_env *env, const int64_t *actions_dev, float *obs_dev, double *reward_dev,
+int lg_step_flags(lg_env *env, const int64_t *actions_dev, void *obs_dev, double *reward_dev,
                   uint8_t *done_dev, const lg_info *info, double *stats_dev, uint32_t flags, void *stream);
 /* BatchEnv.observe (env.py:587-588). */
-int lg_observe(lg_env *env, float *obs_dev, void *stream);
+int lg_observe(lg_env *env, void *obs_dev, void *stream);
 /* The same step with HOST buffers: H2D of actions and D2H of every output
  * happen inside the call, which returns after the stream synchronises. */
-int lg_step_host(lg_env *env, const int64_t *actions_host, float *obs_host, double *reward_host,
+int lg_step_host(lg_env *env, const int64_t *actions_host, void *obs_host, double *reward_host,
                  uint8_t *done_host, const lg_info *info_host, void *stream);
 
 /* Designer edits on imported states: recompute metrics + loss of the masked

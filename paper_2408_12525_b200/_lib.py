@@ -28,7 +28,7 @@ class LgConfig(ctypes.Structure):
         ("pins", ctypes.c_int32 * 16), ("n_ctrl", ctypes.c_int32),
         ("ctrl", ctypes.c_int32 * 8), ("max_steps", ctypes.c_int64),
         ("change_budget", ctypes.c_int64), ("det_metrics", ctypes.c_int32),
-        ("_pad", ctypes.c_int32), ("init_cdf", ctypes.c_double * 8),
+        ("obs_format", ctypes.c_int32), ("init_cdf", ctypes.c_double * 8),
         ("weights", ctypes.c_double * 8),
     ]
 

@@ -102,6 +102,7 @@ struct Params {
     int env_smem;   // shared memory per env: bytes (team kernel) or 32-bit words (solo)
     int solo_E;     // solo kernel: envs per block (== blockDim: warp mode)
     int no_auto_reset;  // scalar step (env.py:611-630): finished envs are not reset
+    int obs_u8;         // observation format: 0 = float32 (reference), 1 = uint8 0/1 planes
     int stream_mode;   // solo: envs of a warp/block rendered into one contiguous bit stream
     int group_words;   // solo stream mode: shared words per warp (warp mode) or block
     int stream_words;  // solo stream mode: offset of the union-find scratch in a group
@@ -701,6 +702,30 @@ __device__ __forceinline__ float team_elem(const Params &p, const unsigned char 
     return reinterpret_cast<const float *>(es + p.off_ctrl)[fdiv(p.divOO, le - p.PB)];
 }
 
+// 4 bits -> 4 bytes of 0/1 (bit k lands in byte k).
+__device__ __forceinline__ uint32_t bits_to_bytes4(uint32_t x) { return ((x & 0xFu) * 0x00204081u) & 0x01010101u; }
+
+// uint8 observation (opt-in, no control planes): 16 elements per 16-byte store.
+template <class G>
+__device__ void write_obs_team_u8(const Params &p, const Team<G> &t, long long env, const unsigned char *es) {
+    const uint32_t *img = reinterpret_cast<const uint32_t *>(es);
+    const size_t base = (size_t)env * p.PE;
+    uint8_t *out = reinterpret_cast<uint8_t *>(p.obs) + base;
+    uint32_t head = (uint32_t)((16 - (base & 15)) & 15);
+    if (head > p.PE) head = p.PE;
+    for (uint32_t e = t.lane; e < head; e += G::TEAM) out[e] = (img[e >> 5] >> (e & 31)) & 1u;
+    const uint32_t n16 = (p.PE - head) >> 4;
+    uint4 *o16 = reinterpret_cast<uint4 *>(out + head);
+    for (uint32_t q = t.lane; q < n16; q += G::TEAM) {
+        uint32_t le = head + (q << 4);
+        uint32_t x = __funnelshift_r(img[le >> 5], img[(le >> 5) + 1], le & 31);
+        __stcs(o16 + q, make_uint4(bits_to_bytes4(x), bits_to_bytes4(x >> 4), bits_to_bytes4(x >> 8),
+                                   bits_to_bytes4(x >> 12)));
+    }
+    for (uint32_t e = head + (n16 << 4) + t.lane; e < p.PE; e += G::TEAM)
+        out[e] = (img[e >> 5] >> (e & 31)) & 1u;
+}
+
 template <class G>
 __device__ void write_obs_team(const Params &p, const Team<G> &t, long long env, const unsigned char *es) {
     const uint32_t *img = reinterpret_cast<const uint32_t *>(es);
@@ -877,7 +902,8 @@ __global__ void __launch_bounds__(256) env_kernel(const Params p, int mode) {
             t.sync();  // union-find scratch is reused for the image
             render_env<G, DOM>(p, t, e, es);
             t.sync();
-            write_obs_team<G>(p, t, env, es);
+            if (p.obs_u8) write_obs_team_u8<G>(p, t, env, es);
+            else write_obs_team<G>(p, t, env, es);
         }
     }
 }

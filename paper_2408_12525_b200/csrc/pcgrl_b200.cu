@@ -287,7 +287,7 @@ struct lg_env {
     size_t smem;
     // e2e staging (lazy)
     long long *d_act = nullptr;
-    float *d_obs = nullptr;
+    void *d_obs = nullptr;
     double *d_rew = nullptr;
     unsigned char *d_done = nullptr, *d_term = nullptr;
     double *d_er = nullptr, *d_es = nullptr, *d_fl = nullptr;
@@ -438,6 +438,10 @@ static int validate_cfg(const lg_config *c) {
         set_err("obs_size must be within 3..128 on device");
         return LG_EINVAL;
     }
+    if (c->obs_format != 0 && c->obs_format != 1) {
+        set_err("unknown observation format %d", c->obs_format);
+        return LG_EINVAL;
+    }
     if (c->n_pins < 0 || c->n_pins > 16 || c->n_ctrl < 0 || c->n_ctrl > 7) {
         set_err("too many pinpoints or controls");
         return LG_EINVAL;
@@ -505,6 +509,12 @@ extern "C" int lg_create(const lg_config *cfg, int64_t n_envs, int64_t global_of
         p.ctrl[i] = cfg->ctrl[i];
         p.cdf[i] = cfg->init_cdf[i];
         p.w[i] = cfg->weights[i];
+    }
+    p.obs_u8 = cfg->obs_format == 1;
+    if (p.obs_u8 && cfg->n_ctrl > 0) {
+        set_err("uint8 observations need a config without controllable metrics");
+        delete e;
+        return LG_EINVAL;
     }
     p.OO = (uint32_t)(e->OH * e->OW);
     p.PB = (uint32_t)(e->N + 2) * p.OO;
@@ -654,13 +664,13 @@ extern "C" int lg_describe(const lg_env *e, lg_desc *out) {
     out->obs_h = e->OH;
     out->obs_w = e->OW;
     out->team = e->team;
-    out->obs_bytes_per_env = (int64_t)e->C * e->OH * e->OW * 4;
+    out->obs_bytes_per_env = (int64_t)e->C * e->OH * e->OW * (e->base.obs_u8 ? 1 : 4);
     out->state_bytes_per_env =
         (int64_t)(e->rows_per_env * e->row_bytes + sizeof(Hot) + 24 * 4 + 32 + 16 + 16 + 8 + 8);
     return LG_OK;
 }
 
-static int check_obs_ptr(const float *obs) {
+static int check_obs_ptr(const void *obs) {
     if (obs && ((uintptr_t)obs & 15)) {
         set_err("observation buffer must be 16-byte aligned");
         return LG_EINVAL;
@@ -668,7 +678,7 @@ static int check_obs_ptr(const float *obs) {
     return LG_OK;
 }
 
-static int run_mode(lg_env *e, int mode, const long long *actions, float *obs, double *reward,
+static int run_mode(lg_env *e, int mode, const long long *actions, void *obs, double *reward,
                     uint8_t *done, const lg_info *info, double *stats, const uint8_t *mask, void *stream,
                     unsigned flags = 0) {
     if (!e) {
@@ -683,7 +693,7 @@ static int run_mode(lg_env *e, int mode, const long long *actions, float *obs, d
     CU(cudaSetDevice(e->device));
     Params p = e->base;
     p.actions = actions;
-    p.obs = obs;
+    p.obs = reinterpret_cast<float *>(obs);  // uint8 bytes when obs_u8
     p.reward = reward;
     p.done = done;
     if (info) {
@@ -699,10 +709,10 @@ static int run_mode(lg_env *e, int mode, const long long *actions, float *obs, d
     return launch_env(e, p, mode, (cudaStream_t)stream);
 }
 
-extern "C" int lg_reset(lg_env *e, float *obs, void *stream) {
+extern "C" int lg_reset(lg_env *e, void *obs, void *stream) {
     return run_mode(e, MODE_RESET, nullptr, obs, nullptr, nullptr, nullptr, nullptr, nullptr, stream);
 }
-extern "C" int lg_reset_masked(lg_env *e, const uint8_t *mask, float *obs, void *stream) {
+extern "C" int lg_reset_masked(lg_env *e, const uint8_t *mask, void *obs, void *stream) {
     return run_mode(e, MODE_RESET, nullptr, obs, nullptr, nullptr, nullptr, nullptr, mask, stream);
 }
 extern "C" int lg_recompute(lg_env *e, const uint8_t *mask, int reprice_only, void *stream) {
@@ -710,26 +720,26 @@ extern "C" int lg_recompute(lg_env *e, const uint8_t *mask, int reprice_only, vo
                     nullptr, mask, stream);
 }
 
-extern "C" int lg_observe(lg_env *e, float *obs, void *stream) {
+extern "C" int lg_observe(lg_env *e, void *obs, void *stream) {
     if (!obs) {
         set_err("observe needs an output buffer");
         return LG_EINVAL;
     }
     return run_mode(e, MODE_OBSERVE, nullptr, obs, nullptr, nullptr, nullptr, nullptr, nullptr, stream);
 }
-extern "C" int lg_step(lg_env *e, const int64_t *actions, float *obs, double *reward, uint8_t *done,
+extern "C" int lg_step(lg_env *e, const int64_t *actions, void *obs, double *reward, uint8_t *done,
                        const lg_info *info, double *stats, void *stream) {
     return run_mode(e, MODE_STEP, (const long long *)actions, obs, reward, done, info, stats, nullptr,
                     stream);
 }
 
-extern "C" int lg_step_flags(lg_env *e, const int64_t *actions, float *obs, double *reward, uint8_t *done,
+extern "C" int lg_step_flags(lg_env *e, const int64_t *actions, void *obs, double *reward, uint8_t *done,
                              const lg_info *info, double *stats, uint32_t flags, void *stream) {
     return run_mode(e, MODE_STEP, (const long long *)actions, obs, reward, done, info, stats, nullptr,
                     stream, flags);
 }
 
-extern "C" int lg_step_host(lg_env *e, const int64_t *actions_host, float *obs_host, double *reward_host,
+extern "C" int lg_step_host(lg_env *e, const int64_t *actions_host, void *obs_host, double *reward_host,
                             uint8_t *done_host, const lg_info *info_host, void *stream) {
     if (!e || !actions_host || !reward_host || !done_host) {
         set_err("step_host needs actions, reward and done buffers");
@@ -737,7 +747,7 @@ extern "C" int lg_step_host(lg_env *e, const int64_t *actions_host, float *obs_h
     }
     CU(cudaSetDevice(e->device));
     size_t B = (size_t)e->B;
-    size_t obs_bytes = B * (size_t)e->C * e->OH * e->OW * sizeof(float);
+    size_t obs_bytes = B * (size_t)e->C * e->OH * e->OW * (e->base.obs_u8 ? 1 : sizeof(float));
     if (!e->d_act) {
         CU(cudaMalloc((void **)&e->d_act, B * 8));
         CU(cudaMalloc((void **)&e->d_rew, B * 8));

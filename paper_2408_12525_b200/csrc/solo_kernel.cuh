@@ -551,6 +551,63 @@ __device__ void solo_write_noctrl(const Params &p, const uint32_t *wimg, long lo
     }
 }
 
+__device__ __forceinline__ void st_cs_v8u(uint8_t *ptr, const uint32_t *v) {
+    asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(ptr), "r"(v[0]), "r"(v[1]),
+                 "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+
+// uint8 observation writer (opt-in, no control planes), slot layout: 32
+// elements -> 32 bytes per lane per 256-bit store, 16 with 16-byte stores.
+template <int GRP>
+__device__ void solo_write_u8(const Params &p, const uint32_t *wimg, long long env0, int nenv, int lane,
+                              int nthr) {
+    uint8_t *out = reinterpret_cast<uint8_t *>(p.obs) + (size_t)env0 * p.PE;
+    const uint32_t PE = p.PE, stride = (uint32_t)p.env_smem;
+    const uint32_t total = (uint32_t)nenv * PE;
+    const uint32_t ng = total / GRP;
+    uint32_t e0 = (uint32_t)lane * GRP;
+    uint32_t el = fdiv(p.divPE, e0), le = e0 - el * PE;
+    for (uint32_t q = lane; q < ng; q += nthr) {
+        const uint32_t *sl = wimg + el * stride;
+        uint32_t x = __funnelshift_r(sl[le >> 5], sl[(le >> 5) + 1], le & 31);
+        const uint32_t k = PE - le;
+        if (k < GRP) {  // group runs into the next env's image
+            uint32_t m = (1u << k) - 1u;
+            x = (x & m) | ((sl[stride] << k) & ~m);
+        }
+        uint32_t w[8];
+#pragma unroll
+        for (int i = 0; i < GRP / 4; i++) w[i] = bits_to_bytes4(x >> (4 * i));
+        if constexpr (GRP == 32) st_cs_v8u(out + (size_t)q * 32, w);
+        else __stcs(reinterpret_cast<uint4 *>(out) + q, make_uint4(w[0], w[1], w[2], w[3]));
+        uint32_t l = le + (uint32_t)nthr * GRP;
+        uint32_t kk = fdiv(p.divPE, l);
+        el += kk;
+        le = l - kk * PE;
+    }
+    for (uint32_t t = ng * GRP + lane; t < total; t += nthr) {
+        uint32_t e2 = fdiv(p.divPE, t), l2 = t - e2 * PE;
+        out[t] = (wimg[e2 * stride + (l2 >> 5)] >> (l2 & 31)) & 1u;
+    }
+}
+
+// uint8 writer for the stream layout: stream word q is elements [32q, 32q+32).
+__device__ void solo_write_stream_u8(const Params &p, const uint32_t *st, long long env0, int nenv, int lane,
+                                     int nthr) {
+    uint8_t *out = reinterpret_cast<uint8_t *>(p.obs) + (size_t)env0 * p.PE;
+    const uint32_t total = (uint32_t)nenv * p.PE;
+    const uint32_t ng = total / 32;
+    for (uint32_t q = lane; q < ng; q += nthr) {
+        uint32_t x = st[sidx(q)];
+        uint32_t w[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) w[i] = bits_to_bytes4(x >> (4 * i));
+        st_cs_v8u(out + (size_t)q * 32, w);
+    }
+    for (uint32_t t = ng * 32 + lane; t < total; t += nthr) out[t] = (st[sidx(t >> 5)] >> (t & 31)) & 1u;
+}
+
 // Writer for the stream layout: the group's outputs are one bit stream, so a
 // VEC-element group q is bits [q*VEC, q*VEC+VEC) -- one shared-memory word,
 // a lane-constant shift, VEC selects and one store. No env bookkeeping.
@@ -748,10 +805,14 @@ __global__ void __launch_bounds__(128, 1) env_solo_kernel(const Params p, int mo
         if (warp_mode) __syncwarp();
         else __syncthreads();
         if (nenv <= 0) return;
-        if ((reinterpret_cast<uintptr_t>(p.obs + (size_t)env0 * p.PE) & 31) == 0)
+        if (p.obs_u8) {
+            // env0 is a multiple of 32, so the warp's byte range is 32-byte aligned
+            solo_write_stream_u8(p, grp, env0, nenv, wl, nthr);
+        } else if ((reinterpret_cast<uintptr_t>(p.obs + (size_t)env0 * p.PE) & 31) == 0) {
             solo_write_stream<8, 2>(p, grp, env0, nenv, wl, nthr);
-        else
+        } else {
             solo_write_stream<4, 2>(p, grp, env0, nenv, wl, nthr);
+        }
         return;
     }
     img = grp;
@@ -760,6 +821,19 @@ __global__ void __launch_bounds__(128, 1) env_solo_kernel(const Params p, int mo
     else __syncthreads();
     if (nenv <= 0) return;
     const size_t first = (size_t)env0 * p.PE;
+    if (p.obs_u8) {
+        const uintptr_t a = reinterpret_cast<uintptr_t>(reinterpret_cast<uint8_t *>(p.obs) + first);
+        if ((a & 31) == 0) solo_write_u8<32>(p, img, env0, nenv, wl, nthr);
+        else if ((a & 15) == 0) solo_write_u8<16>(p, img, env0, nenv, wl, nthr);
+        else {
+            uint8_t *out = reinterpret_cast<uint8_t *>(p.obs) + first;
+            for (uint32_t t = wl; t < (uint32_t)nenv * p.PE; t += nthr) {
+                uint32_t e2 = fdiv(p.divPE, t), l2 = t - e2 * p.PE;
+                out[t] = (img[e2 * (uint32_t)p.env_smem + (l2 >> 5)] >> (l2 & 31)) & 1u;
+            }
+        }
+        return;
+    }
     // obs base is 16-byte aligned (checked on the host) and env0 is a multiple
     // of 8, so every block's output starts 32-byte aligned when the base is.
     if ((reinterpret_cast<uintptr_t>(p.obs + first) & 31) == 0) {

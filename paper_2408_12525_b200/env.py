@@ -27,9 +27,15 @@ from .tiles import get_domain
 INFO_KEYS = ("terminal", "episode_reward", "episode_length", "episode_start_loss", "final_loss")
 
 
-def make_lg_config(cfg: EnvConfig) -> _lib.LgConfig:
+OBS_FORMATS = {"float32": 0, "uint8": 1}
+
+
+def make_lg_config(cfg: EnvConfig, obs_dtype: str = "float32") -> _lib.LgConfig:
     d = cfg.domain_obj
     c = _lib.LgConfig()
+    if obs_dtype not in OBS_FORMATS:
+        raise ValueError(f"unknown obs_dtype {obs_dtype!r}; expected one of {sorted(OBS_FORMATS)}")
+    c.obs_format = OBS_FORMATS[obs_dtype]
     c.domain = d.code
     c.representation = ("narrow", "turtle", "wide").index(cfg.representation)
     c.max_h, c.max_w = cfg.max_height, cfg.max_width
@@ -71,7 +77,10 @@ class BatchEnv:
     """Lockstep batch of identical-config environments with auto-reset."""
 
     def __init__(self, config: EnvConfig, n_envs: int, seed: int = 0, *, device: Any = None,
-                 global_offset: int = 0, validate: bool = True):
+                 global_offset: int = 0, validate: bool = True, obs_dtype: str = "float32"):
+        """``obs_dtype="uint8"`` (opt-in, configs without control planes) writes
+        the same 0/1 observation planes as bytes: 4x less HBM traffic for
+        consumers on the GPU. The default float32 matches the reference."""
         import torch
 
         self._torch = torch
@@ -86,7 +95,8 @@ class BatchEnv:
         self._global_offset = int(global_offset)
         self._seed = int(seed)
         handle = ctypes.c_void_p()
-        cfgc = make_lg_config(config)
+        cfgc = make_lg_config(config, obs_dtype)
+        self.obs_dtype = obs_dtype
         _lib.check(lib.lg_create(ctypes.byref(cfgc), int(n_envs), int(global_offset),
                                  int(seed) & ((1 << 64) - 1), self.device.index, ctypes.byref(handle)))
         self._h = handle
@@ -128,8 +138,8 @@ class BatchEnv:
 
     # -- buffers -------------------------------------------------------------
     def new_obs(self):
-        return self._torch.empty((self._n,) + self.observation_shape, dtype=self._torch.float32,
-                                 device=self.device)
+        dt = self._torch.uint8 if self.obs_dtype == "uint8" else self._torch.float32
+        return self._torch.empty((self._n,) + self.observation_shape, dtype=dt, device=self.device)
 
     def _info_buffers(self):
         t, B, dev = self._torch, self._n, self.device
@@ -380,8 +390,10 @@ class NumpyBatchEnv:
     """
 
     def __init__(self, config: EnvConfig, n_envs: int, seed: int = 0, *, device: Any = None,
-                 global_offset: int = 0, pinned: bool = False, copy: bool = True):
-        self.env = BatchEnv(config, n_envs, seed, device=device, global_offset=global_offset)
+                 global_offset: int = 0, pinned: bool = False, copy: bool = True,
+                 obs_dtype: str = "float32"):
+        self.env = BatchEnv(config, n_envs, seed, device=device, global_offset=global_offset,
+                            obs_dtype=obs_dtype)
         self.pinned = pinned
         self.copy = copy
         self._bufs = None
@@ -398,7 +410,8 @@ class NumpyBatchEnv:
             if self.pinned:
                 return t.empty(shape, dtype=dt, pin_memory=True).numpy()
             return np.empty(shape, dtype=t.empty(0, dtype=dt).numpy().dtype)
-        return {"obs": mk((B,) + self.env.observation_shape, t.float32),
+        odt = t.uint8 if self.env.obs_dtype == "uint8" else t.float32
+        return {"obs": mk((B,) + self.env.observation_shape, odt),
                 "actions": mk((B,), t.int64), "reward": mk((B,), t.float64),
                 "done": mk((B,), t.bool), "terminal": mk((B,), t.bool),
                 "episode_reward": mk((B,), t.float64), "episode_length": mk((B,), t.int64),

@@ -348,3 +348,37 @@ def test_random_config_fuzz_against_oracle(seed):
     s1, s2 = env.state_dict(), ref.state_dict()
     for k in ("tiles", "frozen", "values", "unreach", "prev_loss", "rng", "t", "pos_idx"):
         assert np.array_equal(s1[k], s2[k]), (cfg, k)
+
+
+U8_CASES = [
+    (dict(domain="binary"), 40000, {}),                                   # solo warp, slot layout
+    (dict(domain="dungeon", representation="wide", pinpoints=("player", "key", "door"),
+          randomize_shape=True), 40000, {}),                              # solo warp, stream layout
+    (dict(domain="binary"), 40000, {"LG_STREAM": "1"}),                   # stream layout, PE % 32 != 0
+    (dict(domain="maze", representation="turtle"), 300, {}),              # solo block mode
+    (dict(domain="maze", representation="turtle"), 3000, {}),             # lane-team (mid-size)
+    (dict(domain="binary", max_width=64, max_height=64, obs_size=7), 500, {}),   # lane team 64
+    (dict(domain="dungeon", max_width=40, max_height=20, obs_size=33), 257, {}),  # team 32, odd sizes
+]
+
+
+@pytest.mark.parametrize("case", range(len(U8_CASES)))
+def test_uint8_observations_equal_float32(case, monkeypatch):
+    kw, n, envs = U8_CASES[case]
+    for k, v in envs.items():
+        monkeypatch.setenv(k, v)
+    cfg = EnvConfig(**kw)
+    f32 = BatchEnv(cfg, n, seed=4)
+    u8 = BatchEnv(cfg, n, seed=4, obs_dtype="uint8")
+    a, b = f32.reset(), u8.reset()
+    assert b.dtype == torch.uint8 and torch.equal(a.to(torch.uint8), b)
+    for t in range(5):
+        acts = f32.random_actions(t)
+        a, ra, _, _ = f32.step(acts)
+        b, rb, _, _ = u8.step(acts)
+        assert torch.equal(a.to(torch.uint8), b) and torch.equal(ra, rb), t
+
+
+def test_uint8_rejects_control_planes():
+    with pytest.raises(ValueError):
+        BatchEnv(EnvConfig(domain="maze", controllable=("path_length",)), 8, obs_dtype="uint8")
