@@ -185,6 +185,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-u8", action="store_true", help="skip the opt-in uint8-observation side run")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -293,6 +294,35 @@ def main():
                "d2h_bytes_per_step": B * (obs_b + 8 + 1 + 1 + 8 + 8 + 8 + 8),
                "steps": args.e2e_steps, "api": "NumpyBatchEnv.step -> lg_step_host (pinned)"}
 
+    # Side measurement (does not change the headline): the same workload with
+    # the opt-in uint8 observation format (4x fewer bytes per env-step).
+    u8 = None
+    if not args.no_u8 and not cfg.controllable:
+        import torch as _t
+        _t.cuda.empty_cache()
+        env8 = BatchEnv(cfg, B, seed=0, device=dev, global_offset=offset, validate=False, obs_dtype="uint8")
+        obs8 = env8.new_obs()
+        env8.reset(out=obs8)
+        for i in range(args.warmup):
+            env8.random_actions(1_000_003 * i + 17, out=acts)
+            env8.step_raw(acts, obs8, reward, done, info, None)
+        ev8 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        torch.cuda.synchronize()
+        for i in range(K):
+            env8.random_actions(1_000_003 * (i + args.warmup) + 17, out=acts)
+            ev8[i][0].record(stream)
+            env8.step_raw(acts, obs8, reward, done, info, None)
+            ev8[i][1].record(stream)
+        torch.cuda.synchronize()
+        ms8 = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev8) / K, dev)
+        c_, h_, w_ = env8.observation_shape
+        bytes8 = c_ * h_ * w_ + 17
+        u8 = {"value": global_b / (ms8 / 1e3), "unit": UNIT, "step_kernel_ms": ms8,
+              "bytes_per_env_step": bytes8, "achieved_gbs": B * bytes8 / (ms8 / 1e3) / 1e9,
+              "frac_of_peak": B * bytes8 / (ms8 / 1e3) / 1e9 / peak,
+              "note": "opt-in obs_dtype='uint8' (same 0/1 planes); not the reference float32 contract"}
+        del obs8, env8
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -325,6 +355,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": 2 * K,
+            "obs_uint8": u8,
             "clocks": clocks,
             "episode_stats": [float(x) for x in stats.cpu()],
         }
