@@ -179,9 +179,11 @@ struct SoloK {
         uint8_t *par = reinterpret_cast<uint8_t *>(scratch);
         int runs = 0, merges = 0;
         uint32_t prevR = 0, prevS = 0;
-#pragma unroll
+        // rolled row loop (instruction-cache footprint); the row is picked with
+        // a select chain so the register index stays static
+#pragma unroll 1
         for (int r = 0; r < 16; r++) {
-            uint32_t R = (r & 1) ? (pass.w[r >> 1] >> 16) : (pass.w[r >> 1] & 0xFFFFu);
+            uint32_t R = pass.row(r);
             uint32_t S = R & ~(R << 1);
             int nr = __popc(S);
             for (int i = 0; i < nr; i++) par[r * 8 + i] = (uint8_t)(r * 8 + i);

@@ -763,7 +763,7 @@ __device__ __forceinline__ void solo_env(const Params &p, int mode, long long en
 }
 
 template <int DOM>
-__global__ void __launch_bounds__(128, 1) env_solo_kernel(const Params p, int mode) {
+__global__ void __maxnreg__(144) env_solo_kernel(const Params p, int mode) {  // 7 x 64-thread blocks per SM
     extern __shared__ __align__(16) uint32_t smem_w[];
     const int E = p.solo_E, T = blockDim.x, tid = threadIdx.x;
     const bool warp_mode = E == T;  // uniform over the launch
