@@ -136,7 +136,7 @@ __device__ __forceinline__ Bd<G> rect_board(const Team<G> &t, int h, int w) {
 // ---------------------------------------------------------------------------
 
 template <class G>
-__device__ int kth_cell(const Team<G> &t, const Bd<G> &m, int k) {
+__device__ __forceinline__ int kth_cell(const Team<G> &t, const Bd<G> &m, int k) {
     // flat index (row * 64 + col) of the k-th set cell in row-major order
     int c = m.count();
     int inc = t.scan(c);
@@ -161,7 +161,7 @@ __device__ int kth_cell(const Team<G> &t, const Bd<G> &m, int k) {
 }
 
 template <class G>
-__device__ int lowest_cell(const Team<G> &t, const Bd<G> &m) {
+__device__ __forceinline__ int lowest_cell(const Team<G> &t, const Bd<G> &m) {
     unsigned own = t.ballot(m.nz());
     int src = __ffs((int)own) - 1;
     int res = 0;
@@ -274,7 +274,7 @@ __device__ __forceinline__ void compute_metrics(const K &k, const typename K::B 
 
 // loss_batch (problems.py:251-279): canonical order, explicit IEEE ops (no FMA).
 template <int DOM>
-__device__ double loss_of(const Params &p, const int *val, int unr, const int *lo, const int *hi) {
+__device__ __forceinline__ double loss_of(const Params &p, const int *val, int unr, const int *lo, const int *hi) {
     constexpr int M = Dom<DOM>::M;
     double wreg = p.w[1];
     double total = 0.0;
@@ -295,7 +295,7 @@ __device__ double loss_of(const Params &p, const int *val, int unr, const int *l
 
 // _recompute (env.py:332-347)
 template <class G, int DOM>
-__device__ void recompute(const Params &p, const Team<G> &t, EnvRegs<G, DOM> &e, uint16_t *uf,
+__device__ __forceinline__ void recompute(const Params &p, const Team<G> &t, EnvRegs<G, DOM> &e, uint16_t *uf,
                           bool reset) {
     using Row = typename G::Row;
     TeamK<G> k{t, low_mask<Row>(p.W)};
@@ -320,7 +320,7 @@ __device__ void recompute(const Params &p, const Team<G> &t, EnvRegs<G, DOM> &e,
 // first editable cell in boustrophedon order from row `r0` on (inclusive);
 // returns flat row*64+col or -1.
 template <class G>
-__device__ int serp_first_from(const Team<G> &t, const Bd<G> &ed, int r0) {
+__device__ __forceinline__ int serp_first_from(const Team<G> &t, const Bd<G> &ed, int r0) {
     int best = 0x7fffffff;
 #pragma unroll
     for (int k = 0; k < G::RPL; k++) {
@@ -346,7 +346,7 @@ __device__ int serp_first_from(const Team<G> &t, const Bd<G> &ed, int r0) {
 
 // next editable cell strictly after (r, c) in scan order; -1 if none.
 template <class G>
-__device__ int serp_next(const Team<G> &t, const Bd<G> &ed, int r, int c) {
+__device__ __forceinline__ int serp_next(const Team<G> &t, const Bd<G> &ed, int r, int c) {
     using Row = typename G::Row;
     int src = r / G::RPL;
     int res = -1;
@@ -376,7 +376,7 @@ __device__ int serp_next(const Team<G> &t, const Bd<G> &ed, int r, int c) {
 // ---------------------------------------------------------------------------
 
 template <class G, int DOM>
-__device__ void reset_env(const Params &p, const Team<G> &t, EnvRegs<G, DOM> &e, uint16_t *uf) {
+__device__ __forceinline__ void reset_env(const Params &p, const Team<G> &t, EnvRegs<G, DOM> &e) {
     using Row = typename G::Row;
     constexpr int N = Dom<DOM>::N, NPL = Dom<DOM>::NPL, M = Dom<DOM>::M;
     Pcg &g = e.g;
@@ -406,11 +406,8 @@ __device__ void reset_env(const Params &p, const Team<G> &t, EnvRegs<G, DOM> &e,
 #pragma unroll
                     for (int q = 0; q < N; q++) idx += (p.cdf[q] <= u) ? 1 : 0;  // searchsorted right
                     idx = idx < N - 1 ? idx : N - 1;
-                    if (idx > 0) {
 #pragma unroll
-                        for (int q = 0; q < NPL; q++)
-                            if (q == idx - 1) e.pl[q].r[k] |= Row(1) << c;
-                    }
+                    for (int q = 0; q < NPL; q++) e.pl[q].r[k] |= (q == idx - 1) ? (Row(1) << c) : Row(0);
                 }
             }
         }
@@ -440,16 +437,13 @@ __device__ void reset_env(const Params &p, const Team<G> &t, EnvRegs<G, DOM> &e,
             for (int i = 0; i < k; i++) {
                 int r = picks[i] / w, c = picks[i] % w, tile = p.pins[i];
 #pragma unroll
-                for (int kk = 0; kk < G::RPL; kk++)
-                    if (t.row(kk) == r) {
-                        Row bit = Row(1) << c;
+                for (int kk = 0; kk < G::RPL; kk++) {
+                    const Row m = (t.row(kk) == r) ? (Row(1) << c) : Row(0);
 #pragma unroll
-                        for (int q = 0; q < NPL; q++) {
-                            e.pl[q].r[kk] &= ~bit;
-                            if (q == tile - 1) e.pl[q].r[kk] |= bit;
-                        }
-                        e.frz.r[kk] |= bit;
-                    }
+                    for (int q = 0; q < NPL; q++)
+                        e.pl[q].r[kk] = (e.pl[q].r[kk] & ~m) | (q == tile - 1 ? m : Row(0));
+                    e.frz.r[kk] |= m;
+                }
             }
         }
     }
@@ -469,8 +463,11 @@ __device__ void reset_env(const Params &p, const Team<G> &t, EnvRegs<G, DOM> &e,
         }
         for (int j = 0; j < p.n_ctrl; j++)
             if (p.ctrl[j] == m) lo = hi = (int)pcg_integers(g, 0, (int64_t)cap + 1);
-        e.lo[m] = lo;
-        e.hi[m] = hi;
+#pragma unroll
+        for (int q = 0; q < 8; q++) {  // select chain keeps the register index static
+            e.lo[q] = (q == m) ? lo : e.lo[q];
+            e.hi[q] = (q == m) ? hi : e.hi[q];
+        }
     }
     if (p.det) e.mseed = (long long)pcg_bounded(g, 0x7FFFFFFFFFFFFFFFULL);  // env.py:302-303
     // _install_row (env.py:307-325)
@@ -487,7 +484,7 @@ __device__ void reset_env(const Params &p, const Team<G> &t, EnvRegs<G, DOM> &e,
     e.t = 0;
     e.changes = 0;
     e.max_steps = p.max_steps > 0 ? p.max_steps : 3LL * cap;
-    recompute<G, DOM>(p, t, e, uf, true);
+    // the caller runs _recompute(reset=True) (env.py:305)
 }
 
 // ---------------------------------------------------------------------------
@@ -501,7 +498,7 @@ __device__ __forceinline__ typename G::Row *rows_of(const Params &p, long long e
 }
 
 template <class G, int DOM>
-__device__ void load_env(const Params &p, const Team<G> &t, long long env, EnvRegs<G, DOM> &e) {
+__device__ __forceinline__ void load_env(const Params &p, const Team<G> &t, long long env, EnvRegs<G, DOM> &e) {
     constexpr int NPL = Dom<DOM>::NPL;
     const typename G::Row *rw = rows_of<G, DOM>(p, env);
 #pragma unroll
@@ -546,7 +543,7 @@ __device__ void load_env(const Params &p, const Team<G> &t, long long env, EnvRe
 }
 
 template <class G, int DOM>
-__device__ void store_env(const Params &p, const Team<G> &t, long long env, const EnvRegs<G, DOM> &e,
+__device__ __forceinline__ void store_env(const Params &p, const Team<G> &t, long long env, const EnvRegs<G, DOM> &e,
                           bool rows_dirty, int dirty_row, bool metrics_dirty, bool rng_dirty) {
     constexpr int NPL = Dom<DOM>::NPL;
     if (rows_dirty || dirty_row >= 0) {
@@ -607,28 +604,52 @@ __device__ __forceinline__ void img_or(uint32_t *img, uint32_t off, u128 v) {
     if (hi) atomicOr(&img[w0 + 4], hi);
 }
 
+// OR a window row of <= 32 bits into the image at bit offset `off`.
+__device__ __forceinline__ void img_or64(uint32_t *img, uint32_t off, uint64_t v) {
+    if (v == 0) return;
+    uint64_t x = v << (off & 31);
+    uint32_t w0 = off >> 5;
+    if ((uint32_t)x) atomicOr(&img[w0], (uint32_t)x);
+    if ((uint32_t)(x >> 32)) atomicOr(&img[w0 + 1], (uint32_t)(x >> 32));
+}
+
+// Column masks of an observation window starting at grid column c0: bits of
+// window columns inside the max grid, and all OW bits.
+struct WinMask {
+    u128 inside, full;
+    __device__ __forceinline__ WinMask(int c0, int OW, int W) {
+        int jlo = c0 < 0 ? -c0 : 0;
+        int jhi = W - c0;
+        if (jhi > OW) jhi = OW;
+        inside = 0;
+        if (jhi > jlo) {
+            u128 upto = jhi >= 128 ? ~(u128)0 : (((u128)1 << jhi) - 1);
+            inside = upto & ~(((u128)1 << jlo) - 1);
+        }
+        full = OW >= 128 ? ~(u128)0 : (((u128)1 << OW) - 1);
+    }
+};
+
 // Window row bits of one grid row word: column c0+j -> bit j; columns
 // outside the max grid read `fill`.
-__device__ __forceinline__ u128 window_bits(uint64_t gridrow, int c0, int OW, int W, bool fill) {
+__device__ __forceinline__ u128 window_bits(uint64_t gridrow, int c0, const WinMask &m, bool fill) {
     u128 x = (u128)gridrow;
     u128 win = c0 >= 0 ? (x >> c0) : (x << (-c0));
-    int jlo = c0 < 0 ? -c0 : 0;
-    int jhi = W - c0;
-    if (jhi > OW) jhi = OW;
-    u128 inside = 0;
-    if (jhi > jlo) {
-        u128 upto = jhi >= 128 ? ~(u128)0 : (((u128)1 << jhi) - 1);
-        u128 below = ((u128)1 << jlo) - 1;
-        inside = upto & ~below;
-    }
-    u128 full = OW >= 128 ? ~(u128)0 : (((u128)1 << OW) - 1);
+    win &= m.inside;
+    if (fill) win |= m.full & ~m.inside;
+    return win;
+}
+// the same for windows of <= 32 columns, in 64-bit arithmetic
+__device__ __forceinline__ uint64_t window_bits64(uint64_t gridrow, int c0, uint64_t inside, uint64_t full,
+                                                  bool fill) {
+    uint64_t win = c0 >= 0 ? (gridrow >> c0) : (gridrow << (-c0));
     win &= inside;
     if (fill) win |= full & ~inside;
     return win;
 }
 
 template <class G, int DOM>
-__device__ void render_env(const Params &p, const Team<G> &t, const EnvRegs<G, DOM> &e,
+__device__ __forceinline__ void render_env(const Params &p, const Team<G> &t, const EnvRegs<G, DOM> &e,
                            unsigned char *es) {
     using Row = typename G::Row;
     constexpr int N = Dom<DOM>::N, NPL = Dom<DOM>::NPL;
@@ -659,6 +680,9 @@ __device__ void render_env(const Params &p, const Team<G> &t, const EnvRegs<G, D
     const int OH = p.OH, OW = p.OW;
     const uint32_t plane_bits = (uint32_t)OH * OW;
     Row wmask = low_mask<Row>(p.W);
+    const WinMask wm(c0, OW, p.W);
+    const bool narrow_win = OW <= 32;  // 64-bit window arithmetic suffices (uniform)
+    const uint64_t in64 = (uint64_t)wm.inside, full64 = (uint64_t)wm.full;
     // rows inside the max grid, emitted by the lane that holds them
 #pragma unroll
     for (int k = 0; k < G::RPL; k++) {
@@ -669,25 +693,34 @@ __device__ void render_env(const Params &p, const Team<G> &t, const EnvRegs<G, D
             Row any = 0;
 #pragma unroll
             for (int q = 0; q < NPL; q++) any |= e.pl[q].r[k];
-            uint32_t rowoff = (uint32_t)i * OW;
-            img_or(img, rowoff, window_bits((uint64_t)(act & ~any), c0, OW, p.W, false));
+            const uint32_t rowoff = (uint32_t)i * OW;
+            uint64_t rows[N + 2];
+            rows[0] = (uint64_t)(act & ~any);
 #pragma unroll
-            for (int q = 0; q < NPL; q++)
-                img_or(img, (q + 1) * plane_bits + rowoff,
-                       window_bits((uint64_t)e.pl[q].r[k], c0, OW, p.W, false));
-            img_or(img, N * plane_bits + rowoff,
-                   window_bits((uint64_t)(~act & wmask), c0, OW, p.W, true));
-            img_or(img, (N + 1) * plane_bits + rowoff,
-                   window_bits((uint64_t)e.frz.r[k], c0, OW, p.W, true));
+            for (int q = 0; q < NPL; q++) rows[q + 1] = (uint64_t)e.pl[q].r[k];
+            rows[N] = (uint64_t)(~act & wmask);
+            rows[N + 1] = (uint64_t)e.frz.r[k];
+#pragma unroll
+            for (int q = 0; q < N + 2; q++) {
+                const bool fill = q >= N;  // border and frozen read 1 outside the grid
+                if (narrow_win)
+                    img_or64(img, q * plane_bits + rowoff, window_bits64(rows[q], c0, in64, full64, fill));
+                else
+                    img_or(img, q * plane_bits + rowoff, window_bits(rows[q], c0, wm, fill));
+            }
         }
     }
     // window rows outside the max grid: border and frozen everywhere
-    u128 full = OW >= 128 ? ~(u128)0 : (((u128)1 << OW) - 1);
     for (int i = t.lane; i < OH; i += G::TEAM) {
         int gr = r0 + i;
         if (gr < 0 || gr >= p.H) {
-            img_or(img, N * plane_bits + (uint32_t)i * OW, full);
-            img_or(img, (N + 1) * plane_bits + (uint32_t)i * OW, full);
+            if (narrow_win) {
+                img_or64(img, N * plane_bits + (uint32_t)i * OW, full64);
+                img_or64(img, (N + 1) * plane_bits + (uint32_t)i * OW, full64);
+            } else {
+                img_or(img, N * plane_bits + (uint32_t)i * OW, wm.full);
+                img_or(img, (N + 1) * plane_bits + (uint32_t)i * OW, wm.full);
+            }
         }
     }
 }
@@ -762,7 +795,7 @@ __device__ void write_obs_team(const Params &p, const Team<G> &t, long long env,
 // ---------------------------------------------------------------------------
 
 template <class G, int DOM>
-__global__ void __launch_bounds__(256) env_kernel(const Params p, int mode) {
+__global__ void __launch_bounds__(64) env_kernel(const Params p, int mode) {
     extern __shared__ __align__(16) unsigned char smem[];
     using Row = typename G::Row;
     constexpr int N = Dom<DOM>::N, NPL = Dom<DOM>::NPL;
@@ -777,6 +810,8 @@ __global__ void __launch_bounds__(256) env_kernel(const Params p, int mode) {
         EnvRegs<G, DOM> e;
         load_env<G, DOM>(p, t, env, e);
         bool rows_dirty = false, metrics_dirty = false, rng_dirty = false;
+        bool wrote = false, reset_now = false;
+        double before = 0.0;
         int dirty_row = -1;
         if (mode == MODE_STEP) {
             long long a = p.actions[env];
@@ -823,79 +858,78 @@ __global__ void __launch_bounds__(256) env_kernel(const Params p, int mode) {
             cur = t.from(cur, src);
             editable = t.from(editable, src);
             // narrow: the scan cell is always editable (env.py:366-367)
-            bool wrote = tile >= 0 && tile != cur && (p.rep == REP_NARROW || editable);
-            double reward = 0.0;
-            if (wrote) {
-                if (t.lane == src) {
+            wrote = tile >= 0 && tile != cur && (p.rep == REP_NARROW || editable);
+            if (wrote) {  // env.py:369-372
+                // branch-free value selects (no conditional stores into the
+                // register-resident planes, which would force them to local memory)
 #pragma unroll
-                    for (int k = 0; k < G::RPL; k++)
-                        if (t.row(k) == r) {
-                            Row bit = Row(1) << c;
+                for (int k = 0; k < G::RPL; k++) {
+                    const Row m = (t.row(k) == r) ? (Row(1) << c) : Row(0);
 #pragma unroll
-                            for (int q = 0; q < NPL; q++) {
-                                e.pl[q].r[k] &= ~bit;
-                                if (q == tile - 1) e.pl[q].r[k] |= bit;
-                            }
-                        }
+                    for (int q = 0; q < NPL; q++) e.pl[q].r[k] = (e.pl[q].r[k] & ~m) | (q == tile - 1 ? m : Row(0));
                 }
                 dirty_row = r;
                 e.changes += 1;
-                double before = e.prev_loss;
-                recompute<G, DOM>(p, t, e, uf, false);
-                reward = __dsub_rn(before, e.prev_loss);
-                metrics_dirty = true;
-                rng_dirty = true;
-            }
-            e.ep_reward = __dadd_rn(e.ep_reward, reward);
-            if (p.rep == REP_NARROW) {  // pos_idx = (pos_idx + 1) % order_len
-                int nidx = e.pos_idx + 1;
-                int nxt;
-                Bd<G> ed = andnot(rect_board(t, e.h, e.w), e.frz);
-                if (nidx >= e.order_len) {
-                    nidx = 0;
-                    nxt = serp_first_from(t, ed, 0);
-                } else {
-                    nxt = serp_next(t, ed, e.pr, e.pc);
-                }
-                e.pos_idx = nidx;
-                e.pr = nxt >> 6;
-                e.pc = nxt & 63;
-            }
-            e.t += 1;
-            bool done = e.t >= e.max_steps;
-            if (p.budget > 0) done |= e.changes >= p.budget;
-            if (t.lane == 0) {
-                p.reward[env] = reward;
-                p.done[env] = done;
-                if (p.terminal) p.terminal[env] = done;
-                if (p.ep_rew) p.ep_rew[env] = done ? e.ep_reward : 0.0;
-                if (p.ep_len) p.ep_len[env] = done ? e.t : 0;
-                if (p.ep_start) p.ep_start[env] = done ? e.ep_start_loss : 0.0;
-                if (p.fin_loss) p.fin_loss[env] = done ? e.prev_loss : 0.0;
-                if (done && p.stats) {
-                    atomicAdd(p.stats + 0, 1.0);
-                    atomicAdd(p.stats + 1, e.ep_reward);
-                    atomicAdd(p.stats + 2, (double)e.t);
-                    atomicAdd(p.stats + 3, e.ep_start_loss);
-                    atomicAdd(p.stats + 4, e.prev_loss);
-                }
-            }
-            if (done && !p.no_auto_reset) {
-                reset_env<G, DOM>(p, t, e, uf);
-                rows_dirty = metrics_dirty = rng_dirty = true;
+                before = e.prev_loss;
             }
         } else if (mode == MODE_RESET) {
-            if (!p.reset_mask || p.reset_mask[env]) {
-                reset_env<G, DOM>(p, t, e, uf);
-                rows_dirty = metrics_dirty = rng_dirty = true;
-            }
+            reset_now = !p.reset_mask || p.reset_mask[env];
         } else if (mode == MODE_RECOMPUTE) {
-            if (!p.reset_mask || p.reset_mask[env]) {
-                recompute<G, DOM>(p, t, e, uf, false);
-                metrics_dirty = rng_dirty = true;
-            }
+            wrote = !p.reset_mask || p.reset_mask[env];  // recompute without a write
         } else if (mode == MODE_REPRICE) {
             if (!p.reset_mask || p.reset_mask[env]) e.prev_loss = loss_of<DOM>(p, e.val, e.unr, e.lo, e.hi);
+        }
+        // pass 0: the step's recompute + bookkeeping; pass 1: auto-reset (one
+        // call site for the metric code keeps the instruction footprint small)
+#pragma unroll 1
+        for (int pass = 0; pass < 2; pass++) {
+            if (pass == 1) {
+                if (!reset_now) break;
+                reset_env<G, DOM>(p, t, e);
+                rows_dirty = true;
+            }
+            if (pass == 1 || wrote) {
+                recompute<G, DOM>(p, t, e, uf, pass == 1);  // _recompute (env.py:332-347)
+                metrics_dirty = rng_dirty = true;
+            }
+            if (pass == 0 && mode == MODE_STEP) {
+                double reward = wrote ? __dsub_rn(before, e.prev_loss) : 0.0;
+                e.ep_reward = __dadd_rn(e.ep_reward, reward);
+                if (p.rep == REP_NARROW) {  // pos_idx = (pos_idx + 1) % order_len
+                    int nidx = e.pos_idx + 1;
+                    int nxt;
+                    Bd<G> ed = andnot(rect_board(t, e.h, e.w), e.frz);
+                    if (nidx >= e.order_len) {
+                        nidx = 0;
+                        nxt = serp_first_from(t, ed, 0);
+                    } else {
+                        nxt = serp_next(t, ed, e.pr, e.pc);
+                    }
+                    e.pos_idx = nidx;
+                    e.pr = nxt >> 6;
+                    e.pc = nxt & 63;
+                }
+                e.t += 1;
+                bool done = e.t >= e.max_steps;
+                if (p.budget > 0) done |= e.changes >= p.budget;
+                if (t.lane == 0) {
+                    p.reward[env] = reward;
+                    p.done[env] = done;
+                    if (p.terminal) p.terminal[env] = done;
+                    if (p.ep_rew) p.ep_rew[env] = done ? e.ep_reward : 0.0;
+                    if (p.ep_len) p.ep_len[env] = done ? e.t : 0;
+                    if (p.ep_start) p.ep_start[env] = done ? e.ep_start_loss : 0.0;
+                    if (p.fin_loss) p.fin_loss[env] = done ? e.prev_loss : 0.0;
+                    if (done && p.stats) {
+                        atomicAdd(p.stats + 0, 1.0);
+                        atomicAdd(p.stats + 1, e.ep_reward);
+                        atomicAdd(p.stats + 2, (double)e.t);
+                        atomicAdd(p.stats + 3, e.ep_start_loss);
+                        atomicAdd(p.stats + 4, e.prev_loss);
+                    }
+                }
+                reset_now = done && !p.no_auto_reset;
+            }
         }
         if (mode != MODE_OBSERVE) store_env<G, DOM>(p, t, env, e, rows_dirty, dirty_row, metrics_dirty, rng_dirty);
         if (p.obs) {

@@ -35,7 +35,7 @@ __device__ __forceinline__ uint32_t *solo_rows(const Params &p, long long env) {
 }
 
 template <int DOM>
-__device__ void solo_load(const Params &p, long long env, SoloEnv<DOM> &e) {
+__device__ __forceinline__ void solo_load(const Params &p, long long env, SoloEnv<DOM> &e) {
     constexpr int NPL = Dom<DOM>::NPL;
     const uint4 *rw = reinterpret_cast<const uint4 *>(solo_rows<DOM>(p, env));
 #pragma unroll
@@ -78,7 +78,7 @@ __device__ void solo_load(const Params &p, long long env, SoloEnv<DOM> &e) {
 }
 
 template <int DOM>
-__device__ void solo_store(const Params &p, long long env, const SoloEnv<DOM> &e, bool rows_dirty,
+__device__ __forceinline__ void solo_store(const Params &p, long long env, const SoloEnv<DOM> &e, bool rows_dirty,
                            bool planes_dirty, bool metrics_dirty, bool rng_dirty) {
     constexpr int NPL = Dom<DOM>::NPL;
     if (rows_dirty || planes_dirty) {
@@ -168,7 +168,10 @@ __device__ __forceinline__ void solo_set_tile(SoloEnv<DOM> &e, int r, int c, int
     for (int q = 0; q < NPL; q++)
 #pragma unroll
         for (int k = 0; k < 8; k++)
-            if (k == wi) e.pl[q].w[k] = (e.pl[q].w[k] & ~bit) | (q == tile - 1 ? bit : 0u);
+        {  // value select, not a conditional store (keeps the planes in registers)
+            const uint32_t m = (k == wi) ? bit : 0u;
+            e.pl[q].w[k] = (e.pl[q].w[k] & ~m) | (q == tile - 1 ? m : 0u);
+        }
 }
 
 // reset_rows for one env minus its final _recompute (env.py:284-325)
@@ -236,7 +239,7 @@ __device__ __forceinline__ void solo_reset_setup(const Params &p, SoloEnv<DOM> &
                 const uint32_t bit = 1u << ((r & 1) * 16 + c);
 #pragma unroll
                 for (int kk = 0; kk < 8; kk++)
-                    if (kk == wi) e.frz.w[kk] |= bit;
+                    e.frz.w[kk] |= (kk == wi) ? bit : 0u;
             }
         }
     }
@@ -344,7 +347,7 @@ struct BitW {
 // slot (slot mode), or at bit offset `bit0` of the warp/block stream whose
 // bits are the concatenated outputs of consecutive envs (stream mode).
 template <int DOM>
-__device__ void solo_render(const Params &p, const SoloEnv<DOM> &e, uint32_t *slot, bool stream, uint32_t bit0,
+__device__ __forceinline__ void solo_render(const Params &p, const SoloEnv<DOM> &e, uint32_t *slot, bool stream, uint32_t bit0,
                             bool last) {
     constexpr int N = Dom<DOM>::N, NPL = Dom<DOM>::NPL;
     const int OH = p.OH, OW = p.OW, H = p.H, W = p.W;
@@ -365,8 +368,9 @@ __device__ void solo_render(const Params &p, const SoloEnv<DOM> &e, uint32_t *sl
     int after = OH - before - n_in;
     BitW bw{slot, stream ? (bit0 >> 5) : 0u, 0, stream ? (int)(bit0 & 31) : 0, stream, true, last};
     const uint32_t wm = mask16(W), am = mask16(e.w);
-    // plane loop kept rolled (instruction-cache footprint); the stored plane
-    // for `pl` is picked with selects so register indexing stays static.
+    // plane loop kept rolled (instruction-cache footprint). The stored plane
+    // for `pl` is picked with an AND/OR mask, not a select: a select chain gets
+    // rewritten into a dynamically indexed load, demoting the planes to local memory.
 #pragma unroll 1
     for (int pl = 0; pl < N + 2; pl++) {
         const bool fill = pl >= N;  // border and frozen planes read 1 outside the max grid
@@ -378,7 +382,7 @@ __device__ void solo_render(const Params &p, const SoloEnv<DOM> &e, uint32_t *sl
 #pragma unroll
             for (int q = 0; q < NPL; q++) {
                 any |= e.pl[q].w[k];
-                sel = (q == pl - 1) ? e.pl[q].w[k] : sel;
+                sel |= e.pl[q].w[k] & (0u - (uint32_t)(q == pl - 1));
             }
             const uint32_t act2 = ((2 * k < e.h) ? am : 0u) | ((2 * k + 1 < e.h) ? (am << 16) : 0u);
             const uint32_t wm2 = wm | (wm << 16);

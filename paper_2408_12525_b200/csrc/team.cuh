@@ -151,7 +151,7 @@ __device__ __forceinline__ Bd<G> dilate(const Team<G> &t, const Bd<G> &f, typena
 // BFS from the cells of `f` through `pass`; on return `f` holds the last
 // non-empty layer and the result is its depth (flood_distance layers).
 template <class G>
-__device__ int bfs_last_layer(const Team<G> &t, Bd<G> &f, const Bd<G> &pass, typename G::Row wm) {
+__device__ __forceinline__ int bfs_last_layer(const Team<G> &t, Bd<G> &f, const Bd<G> &pass, typename G::Row wm) {
     Bd<G> vis = f;
     int depth = 0;
     while (true) {
@@ -170,7 +170,7 @@ __device__ int bfs_last_layer(const Team<G> &t, Bd<G> &f, const Bd<G> &pass, typ
 // pathfind.py:188-203), i.e. first layer whose dilation touches a target, +1.
 // -1 = never touched.
 template <class G, bool ENDPOINT>
-__device__ void bfs_touch(const Team<G> &t, Bd<G> f, const Bd<G> &pass, typename G::Row wm,
+__device__ __forceinline__ void bfs_touch(const Team<G> &t, Bd<G> f, const Bd<G> &pass, typename G::Row wm,
                           const Bd<G> &ta, const Bd<G> &tb, bool want_b, int &da, int &db) {
     da = -1;
     db = -1;
@@ -244,7 +244,7 @@ __device__ __forceinline__ int uf_unite(volatile uint16_t *par, int a, int b) {
 }
 
 template <class G>
-__device__ int count_regions(const Team<G> &t, const Bd<G> &pass, uint16_t *par_smem) {
+__device__ __forceinline__ int count_regions(const Team<G> &t, const Bd<G> &pass, uint16_t *par_smem) {
     using Row = typename G::Row;
     volatile uint16_t *par = par_smem;
     int runs = 0;
