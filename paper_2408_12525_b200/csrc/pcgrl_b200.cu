@@ -332,12 +332,12 @@ static int launch_solo_t(lg_env *e, const Params &p, int mode, cudaStream_t s) {
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [] {
-        attr_err = cudaFuncSetAttribute(env_solo_kernel<DOM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        attr_err = cudaFuncSetAttribute(SoloKernel<DOM>::fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         200 * 1024);
     });
     CU(attr_err);
     long long grid = (e->B + e->E - 1) / e->E;
-    env_solo_kernel<DOM><<<(unsigned)grid, e->threads, e->smem, s>>>(p, mode);
+    SoloKernel<DOM>::fn<<<(unsigned)grid, e->threads, e->smem, s>>>(p, mode);
     CU(cudaGetLastError());
     return LG_OK;
 }

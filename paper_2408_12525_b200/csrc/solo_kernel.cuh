@@ -767,7 +767,7 @@ __device__ __forceinline__ void solo_env(const Params &p, int mode, long long en
 }
 
 template <int DOM>
-__global__ void __maxnreg__(144) env_solo_kernel(const Params p, int mode) {  // 7 x 64-thread blocks per SM
+__device__ __forceinline__ void env_solo_body(const Params &p, int mode) {
     extern __shared__ __align__(16) uint32_t smem_w[];
     const int E = p.solo_E, T = blockDim.x, tid = threadIdx.x;
     const bool warp_mode = E == T;  // uniform over the launch
@@ -847,6 +847,28 @@ __global__ void __maxnreg__(144) env_solo_kernel(const Params p, int mode) {  //
         solo_write<4, 2>(p, img, env0, nenv, wl, nthr);
     }
 }
+
+// Register caps (measured): binary keeps 7 x 64-thread blocks per SM at 144
+// registers with no spills; maze/dungeon run faster at 8 blocks (128 regs)
+// despite a few spills (c3: 418 M vs 343 M env-steps/s).
+__global__ void __maxnreg__(144) env_solo_kernel_binary(const Params p, int mode) { env_solo_body<0>(p, mode); }
+__global__ void __maxnreg__(128) env_solo_kernel_maze(const Params p, int mode) { env_solo_body<1>(p, mode); }
+__global__ void __maxnreg__(128) env_solo_kernel_dungeon(const Params p, int mode) { env_solo_body<2>(p, mode); }
+
+template <int DOM>
+struct SoloKernel;
+template <>
+struct SoloKernel<0> {
+    static constexpr auto fn = env_solo_kernel_binary;
+};
+template <>
+struct SoloKernel<1> {
+    static constexpr auto fn = env_solo_kernel_maze;
+};
+template <>
+struct SoloKernel<2> {
+    static constexpr auto fn = env_solo_kernel_dungeon;
+};
 
 // ---- state export / import / metrics for the solo layout -------------------
 
