@@ -190,23 +190,31 @@ struct SoloK {
             runs += nr;
             uint32_t C = R & prevR;
             uint32_t CS = C & ~(C << 1);
+            // contacts arrive left to right, grouped by new run; a new run is
+            // only ever linked by its own contacts, so its current root is
+            // tracked in a register and only the old run needs a find
+            int cur_run = -1, root = 0;
             while (CS) {
                 int c = __ffs((int)CS) - 1;
                 CS &= CS - 1;
                 uint32_t upto = (2u << c) - 1u;
-                int a = r * 8 + __popc(S & upto) - 1;
+                int ir = __popc(S & upto) - 1;
                 int b = (r - 1) * 8 + __popc(prevS & upto) - 1;
-                while (par[a] != a) {
-                    par[a] = par[par[a]];
-                    a = par[a];
+                if (ir != cur_run) {
+                    cur_run = ir;
+                    root = r * 8 + ir;
                 }
                 while (par[b] != b) {
                     par[b] = par[par[b]];
                     b = par[b];
                 }
-                if (a != b) {
-                    if (a < b) par[b] = (uint8_t)a;
-                    else par[a] = (uint8_t)b;
+                if (b != root) {  // link the larger root under the smaller
+                    if (b < root) {
+                        par[root] = (uint8_t)b;
+                        root = b;
+                    } else {
+                        par[b] = (uint8_t)root;
+                    }
                     merges++;
                 }
             }
