@@ -232,6 +232,8 @@ def test_pinpoint_overflow_flags_error():
 
 WARP_MODE_CASES = [
     (dict(domain="binary"), 40000, 4),
+    (dict(domain="binary"), 19001, 4),  # ragged last warp and block
+    (dict(domain="dungeon", representation="wide"), 18977, 3),  # ragged, stream layout
     (dict(domain="maze", representation="turtle"), 20000, 4),
     (dict(domain="dungeon", representation="wide", pinpoints=("player", "key", "door"),
           randomize_shape=True), 20000, 4),
