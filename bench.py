@@ -322,6 +322,26 @@ def main():
               "frac_of_peak": B * bytes8 / (ms8 / 1e3) / 1e9 / peak,
               "note": "opt-in obs_dtype='uint8' (same 0/1 planes); not the reference float32 contract"}
         del obs8, env8
+        if not args.no_e2e:
+            # the same host-buffer e2e loop with uint8 observations (4x fewer PCIe bytes)
+            import numpy as np
+            _t.cuda.empty_cache()
+            n8 = NumpyBatchEnv(cfg, B, seed=0, device=dev, global_offset=offset, pinned=True, copy=False,
+                               obs_dtype="uint8")
+            n8.reset()
+            rng = np.random.default_rng(1)
+            host_acts = [rng.integers(0, cfg.n_actions, size=B) for _ in range(args.e2e_steps + 1)]
+            n8.step(host_acts[0])
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            for a in host_acts[1:]:
+                n8.step(a)
+            dt = max_over_ranks(time.perf_counter() - t0, dev)
+            u8["e2e"] = {"value": global_b * args.e2e_steps / dt, "unit": UNIT,
+                         "h2d_bytes_per_step": B * 8,
+                         "d2h_bytes_per_step": B * (c_ * h_ * w_ + 8 + 1 + 1 + 8 + 8 + 8 + 8)}
+            del n8
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

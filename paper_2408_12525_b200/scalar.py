@@ -40,6 +40,27 @@ class TileGrid:
     active: np.ndarray
     frozen: np.ndarray
 
+    @property
+    def height(self) -> int:
+        return int(self.tiles.shape[0])
+
+    @property
+    def width(self) -> int:
+        return int(self.tiles.shape[1])
+
+    def validate(self) -> None:
+        """Structural invariants (reference grid.py:89-102), ValueError on failure."""
+        b = self.domain.border_id
+        off = ~self.active
+        if np.any(self.tiles[off] != b):
+            raise ValueError("inactive cell holds a non-border tile")
+        if np.any(self.tiles[self.active] == b):
+            raise ValueError("active cell holds the border tile")
+        if np.any(self.tiles > b):
+            raise ValueError("tile id out of range for domain")
+        if not np.all(self.frozen[off]):
+            raise ValueError("inactive cell is not frozen")
+
     def __eq__(self, other) -> bool:
         return (isinstance(other, TileGrid) and self.domain.name == other.domain.name
                 and np.array_equal(self.tiles, other.tiles)

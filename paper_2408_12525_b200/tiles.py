@@ -13,6 +13,11 @@ from dataclasses import dataclass, field
 
 BORDER = "border"
 
+# printable character per tile name (reference tiles.py:20-29): text codec,
+# play frames and traces
+TILE_CHARS = {"air": ".", "wall": "#", "player": "P", "door": "D", "key": "K", "enemy": "E",
+              BORDER: "%"}
+
 
 @dataclass(frozen=True)
 class Domain:
@@ -53,6 +58,15 @@ class Domain:
         if 0 <= tid < len(self.tiles):
             return self.tiles[tid]
         raise KeyError(f"domain {self.name!r} has no tile id {tid}")
+
+    def char_of(self, tid: int) -> str:
+        return TILE_CHARS[self.tile_name(tid)]
+
+    def id_of_char(self, ch: str) -> int:
+        names = [n for n, c in TILE_CHARS.items() if c == ch and (n == BORDER or n in self.tiles)]
+        if not names:
+            raise KeyError(f"domain {self.name!r} has no tile for character {ch!r}")
+        return self.tile_id(names[0])
 
     @property
     def pivotal_ids(self) -> tuple[int, ...]:
