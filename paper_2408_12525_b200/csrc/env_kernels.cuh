@@ -107,6 +107,11 @@ struct Params {
     int group_words;   // solo stream mode: shared words per warp (warp mode) or block
     int stream_words;  // solo stream mode: offset of the union-find scratch in a group
     int off_ctrl;   // byte offset of the control floats within an env's smem
+    // solo slot layout: 1 = the frozen plane is not staged because it equals the
+    // border plane in every env (no active frozen cell); the writer reads the
+    // border plane twice. Decided per launch by the host (lg_env::plain).
+    int elide;
+    unsigned *aux;  // [1] device flag: an imported env has an active frozen cell
 };
 
 template <class G, int DOM>

@@ -285,6 +285,13 @@ struct lg_env {
     size_t row_bytes, rows_per_env;
     Params base;
     size_t smem;
+    // solo slot layout without the frozen plane (Params::elide): allowed by the
+    // config (no pinpoints, no control planes, float32 obs, slot layout) and
+    // used while every env's frozen plane equals its border plane (`plain`;
+    // re-checked on device by every lg_import_state).
+    bool elide_ok = false, plain = true;
+    int slot_elide = 0;
+    size_t smem_elide = 0;
     // e2e staging (lazy)
     long long *d_act = nullptr;
     void *d_obs = nullptr;
@@ -337,7 +344,14 @@ static int launch_solo_t(lg_env *e, const Params &p, int mode, cudaStream_t s) {
     });
     CU(attr_err);
     long long grid = (e->B + e->E - 1) / e->E;
-    SoloKernel<DOM>::fn<<<(unsigned)grid, e->threads, e->smem, s>>>(p, mode);
+    if (e->elide_ok && e->plain && p.obs) {
+        Params q = p;
+        q.elide = 1;
+        q.env_smem = e->slot_elide;
+        SoloKernel<DOM>::fn<<<(unsigned)grid, e->threads, e->smem_elide, s>>>(q, mode);
+    } else {
+        SoloKernel<DOM>::fn<<<(unsigned)grid, e->threads, e->smem, s>>>(p, mode);
+    }
     CU(cudaGetLastError());
     return LG_OK;
 }
@@ -581,6 +595,15 @@ extern "C" int lg_create(const lg_config *cfg, int64_t n_envs, int64_t global_of
             }
         }
         if (e->OW > 64 || e->smem > 200 * 1024) e->geo = pick_geo(17, W);  // too wide: lane teams
+        if (e->geo == 1 && !p.stream_mode && p.n_ctrl == 0 && p.n_pins == 0 && !p.obs_u8 &&
+            !getenv("LG_NO_ELIDE")) {
+            int se = (int)((p.PB - p.OO + 31) / 32 + 1);
+            if (se < 33) se = 33;
+            if (!(se & 1)) se++;
+            e->elide_ok = true;
+            e->slot_elide = se;
+            e->smem_elide = (size_t)e->E * se * 4;
+        }
     }
     if (e->geo != 1) {
         e->team = e->geo == 16 ? 16 : 32;
@@ -623,6 +646,7 @@ extern "C" int lg_create(const lg_config *cfg, int64_t n_envs, int64_t global_of
     alloc((void **)&p.rb, B * sizeof(uint2));
     alloc((void **)&p.mseed, B * sizeof(long long));
     alloc((void **)&p.err, sizeof(unsigned));
+    alloc((void **)&p.aux, sizeof(unsigned));
     if (err != cudaSuccess) {
         set_err("CUDA allocation failed: %s", cudaGetErrorString(err));
         lg_destroy(e);
@@ -644,7 +668,7 @@ extern "C" int lg_destroy(lg_env *e) {
     if (!e) return LG_OK;
     cudaSetDevice(e->device);
     Params &p = e->base;
-    void *ptrs[] = {p.rows, p.hot, p.mv, p.lossv, p.rs, p.ri, p.rb, p.mseed, p.err,
+    void *ptrs[] = {p.rows, p.hot, p.mv, p.lossv, p.rs, p.ri, p.rb, p.mseed, p.err, p.aux,
                     e->d_act, e->d_obs, e->d_rew, e->d_done, e->d_term, e->d_er, e->d_es, e->d_fl, e->d_el};
     for (void *q : ptrs)
         if (q) cudaFree(q);
@@ -798,7 +822,17 @@ extern "C" int lg_import_state(lg_env *e, const lg_state *src, void *stream) {
         return LG_EINVAL;
     }
     CU(cudaSetDevice(e->device));
-    return launch_state(e, *src, false, (cudaStream_t)stream);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!e->elide_ok) return launch_state(e, *src, false, s);
+    // the import kernel flags envs whose frozen plane is not their border plane
+    CU(cudaMemsetAsync(e->base.aux, 0, 4, s));
+    int rc = launch_state(e, *src, false, s);
+    if (rc != LG_OK) return rc;
+    unsigned flag = 1;
+    CU(cudaMemcpyAsync(&flag, e->base.aux, 4, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    e->plain = flag == 0;
+    return LG_OK;
 }
 
 extern "C" int lg_errors(lg_env *e, uint32_t *flags, void *stream) {

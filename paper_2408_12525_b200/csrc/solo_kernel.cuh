@@ -371,8 +371,9 @@ __device__ __forceinline__ void solo_render(const Params &p, const SoloEnv<DOM> 
     // plane loop kept rolled (instruction-cache footprint). The stored plane
     // for `pl` is picked with an AND/OR mask, not a select: a select chain gets
     // rewritten into a dynamically indexed load, demoting the planes to local memory.
+    const int planes = N + 2 - p.elide;
 #pragma unroll 1
-    for (int pl = 0; pl < N + 2; pl++) {
+    for (int pl = 0; pl < planes; pl++) {
         const bool fill = pl >= N;  // border and frozen planes read 1 outside the max grid
         bw.fill(fill, before * OW);
         SB cur;
@@ -421,7 +422,10 @@ __device__ __forceinline__ void solo_render(const Params &p, const SoloEnv<DOM> 
 
 __device__ __forceinline__ float solo_elem(const Params &p, const uint32_t *wimg, uint32_t el, uint32_t le) {
     const uint32_t *slot = wimg + (size_t)el * p.env_smem;
-    if (le < p.PB) return ((slot[le >> 5] >> (le & 31)) & 1u) ? 1.0f : 0.0f;
+    if (le < p.PB) {
+        if (p.elide && le >= p.PB - p.OO) le -= p.OO;  // frozen plane == border plane
+        return ((slot[le >> 5] >> (le & 31)) & 1u) ? 1.0f : 0.0f;
+    }
     return reinterpret_cast<const float *>(slot + p.img_words)[fdiv(p.divOO, le - p.PB)];
 }
 
@@ -510,14 +514,24 @@ __device__ void solo_write_noctrl(const Params &p, const uint32_t *wimg, long lo
         le[u] = e - el[u] * PE;
     }
     const bool small_env = PE <= STEP;  // more than one wrap per round: use the divider
+    // elided frozen plane: elements [PF, PE) read the border plane [PF-OO, PF)
+    const uint32_t OO = p.OO, PF = p.elide ? PE - OO : PE;
     uint32_t q0 = lane;
     for (; q0 + (uint32_t)nthr * (U - 1) < nv; q0 += (uint32_t)nthr * U) {
         uint32_t x[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const uint32_t *sl = wimg + el[u] * stride;
-            const uint32_t wi = le[u] >> 5;
-            uint32_t v = __funnelshift_r(sl[wi], sl[wi + 1], le[u] & 31);
+            const uint32_t b = le[u] >= PF ? le[u] - OO : le[u];
+            const uint32_t wi = b >> 5;
+            uint32_t v = __funnelshift_r(sl[wi], sl[wi + 1], b & 31);
+            const uint32_t kf = PF - le[u];
+            if (kf < 8) {  // group straddles the start of the (elided) frozen plane
+                const uint32_t b2 = PF - OO, w2 = b2 >> 5;
+                const uint32_t v2 = __funnelshift_r(sl[w2], sl[w2 + 1], b2 & 31);
+                const uint32_t m = (1u << kf) - 1u;
+                v = (v & m) | ((v2 << kf) & ~m);
+            }
             const uint32_t k = PE - le[u];
             if (k < 8) {
                 uint32_t m = (1u << k) - 1u;
@@ -851,7 +865,10 @@ __device__ __forceinline__ void env_solo_body(const Params &p, int mode) {
 // Register caps (measured): binary keeps 7 x 64-thread blocks per SM at 144
 // registers with no spills; maze/dungeon run faster at 8 blocks (128 regs)
 // despite a few spills (c3: 418 M vs 343 M env-steps/s).
-__global__ void __maxnreg__(144) env_solo_kernel_binary(const Params p, int mode) { env_solo_body<0>(p, mode); }
+#ifndef LG_BINARY_NREG
+#define LG_BINARY_NREG 144
+#endif
+__global__ void __maxnreg__(LG_BINARY_NREG) env_solo_kernel_binary(const Params p, int mode) { env_solo_body<0>(p, mode); }
 __global__ void __maxnreg__(128) env_solo_kernel_maze(const Params p, int mode) { env_solo_body<1>(p, mode); }
 __global__ void __maxnreg__(128) env_solo_kernel_dungeon(const Params p, int mode) { env_solo_body<2>(p, mode); }
 
@@ -967,6 +984,18 @@ __global__ void solo_import_kernel(const Params p, lg_state src) {
         for (int k = 0; k < 8; k++) rw[q * 8 + k] = wq[q][k];
     Hot hv;
     uint32_t h = (uint32_t)src.shape_hw[2 * env], w = (uint32_t)src.shape_hw[2 * env + 1];
+    {  // frozen plane != border plane (~active rectangle) inside the max grid?
+        const uint32_t wm = mask16(W), am = mask16((int)w);
+        uint32_t diff = 0;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            const uint32_t g0 = 2 * k < H ? wm : 0u, g1 = 2 * k + 1 < H ? wm : 0u;
+            const uint32_t a0 = 2 * k < (int)h ? am : 0u, a1 = 2 * k + 1 < (int)h ? am : 0u;
+            const uint32_t border = (g0 & ~a0) | ((g1 & ~a1) << 16);
+            diff |= (wq[NPL][k] ^ border) & (g0 | (g1 << 16));
+        }
+        if (diff && p.aux) atomicOr(p.aux, 1u);
+    }
     uint32_t pr = (uint32_t)src.pos[2 * env], pc = (uint32_t)src.pos[2 * env + 1];
     hv.geo = h | (w << 8) | (pr << 16) | (pc << 24);
     hv.pos_idx = (int32_t)src.pos_idx[env];
