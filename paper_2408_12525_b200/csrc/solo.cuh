@@ -35,11 +35,13 @@ struct SB {
         for (int k = 0; k < 8; k++) c += __popc(w[k]);
         return c;
     }
-    // 16-bit row r (r static after unrolling, or dynamic via a select chain)
+    // 16-bit row r (r static after unrolling, or dynamic). The word is picked
+    // with AND/OR masks: a select chain is pattern-matched into a dynamically
+    // indexed array, which demotes the plane to local memory.
     __device__ __forceinline__ uint32_t row(int r) const {
         uint32_t x = 0;
 #pragma unroll
-        for (int k = 0; k < 8; k++) x = (k == (r >> 1)) ? w[k] : x;
+        for (int k = 0; k < 8; k++) x |= w[k] & (0u - (uint32_t)(k == (r >> 1)));
         return (r & 1) ? (x >> 16) : (x & 0xFFFFu);
     }
 };
@@ -179,11 +181,15 @@ struct SoloK {
         uint8_t *par = reinterpret_cast<uint8_t *>(scratch);
         int runs = 0, merges = 0;
         uint32_t prevR = 0, prevS = 0;
-        // rolled row loop (instruction-cache footprint); the row is picked with
-        // a select chain so the register index stays static
+        // rolled row loop (instruction-cache footprint); the plane is shifted
+        // down one row per iteration so the current row is always word 0's low half
+        SB q = pass;
 #pragma unroll 1
         for (int r = 0; r < 16; r++) {
-            uint32_t R = pass.row(r);
+            uint32_t R = q.w[0] & 0xFFFFu;
+#pragma unroll
+            for (int k = 0; k < 7; k++) q.w[k] = __funnelshift_r(q.w[k], q.w[k + 1], 16);
+            q.w[7] >>= 16;
             uint32_t S = R & ~(R << 1);
             int nr = __popc(S);
             for (int i = 0; i < nr; i++) par[r * 8 + i] = (uint8_t)(r * 8 + i);

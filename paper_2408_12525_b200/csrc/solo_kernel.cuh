@@ -99,7 +99,20 @@ __device__ __forceinline__ void solo_store(const Params &p, long long env, const
     hv.t = e.t;
     hv.max_steps = e.max_steps;
     p.hot[env] = hv;
-    if (metrics_dirty) {
+    constexpr int M = Dom<DOM>::M;
+    if (metrics_dirty && M <= 2) {  // only live entries: the rest stay dead registers
+        int2 *m2 = reinterpret_cast<int2 *>(p.mv + env * 24);
+        m2[0] = make_int2(e.val[0], e.val[1]);
+        m2[4] = make_int2(e.lo[0], e.lo[1]);
+        m2[8] = make_int2(e.hi[0], e.hi[1]);
+        p.mv[env * 24 + 7] = e.unr;
+    } else if (metrics_dirty && M <= 4) {
+        int4 *mv = reinterpret_cast<int4 *>(p.mv + env * 24);
+        mv[0] = make_int4(e.val[0], e.val[1], e.val[2], e.val[3]);
+        mv[2] = make_int4(e.lo[0], e.lo[1], e.lo[2], e.lo[3]);
+        mv[4] = make_int4(e.hi[0], e.hi[1], e.hi[2], e.hi[3]);
+        p.mv[env * 24 + 7] = e.unr;
+    } else if (metrics_dirty) {
         int4 *mv = reinterpret_cast<int4 *>(p.mv + env * 24);
         mv[0] = make_int4(e.val[0], e.val[1], e.val[2], e.val[3]);
         mv[1] = make_int4(e.val[4], e.val[5], e.val[6], e.unr);
