@@ -111,6 +111,7 @@ struct Params {
     // border plane in every env (no active frozen cell); the writer reads the
     // border plane twice. Decided per launch by the host (lg_env::plain).
     int elide;
+    int frz_derived;  // solo: frozen plane == max grid minus episode rect in every env (not read)
     unsigned *aux;  // [1] device flag: an imported env has an active frozen cell
 };
 

@@ -290,6 +290,7 @@ struct lg_env {
     // used while every env's frozen plane equals its border plane (`plain`;
     // re-checked on device by every lg_import_state).
     bool elide_ok = false, plain = true;
+    bool frz_ok = false;  // solo layout without pinpoints: Params::frz_derived while `plain`
     int slot_elide = 0;
     size_t smem_elide = 0;
     // e2e staging (lazy)
@@ -344,14 +345,15 @@ static int launch_solo_t(lg_env *e, const Params &p, int mode, cudaStream_t s) {
     });
     CU(attr_err);
     long long grid = (e->B + e->E - 1) / e->E;
+    Params q = p;
+    size_t smem = e->smem;
+    q.frz_derived = e->frz_ok && e->plain;
     if (e->elide_ok && e->plain && p.obs) {
-        Params q = p;
         q.elide = 1;
         q.env_smem = e->slot_elide;
-        SoloKernel<DOM>::fn<<<(unsigned)grid, e->threads, e->smem_elide, s>>>(q, mode);
-    } else {
-        SoloKernel<DOM>::fn<<<(unsigned)grid, e->threads, e->smem, s>>>(p, mode);
+        smem = e->smem_elide;
     }
+    SoloKernel<DOM>::fn<<<(unsigned)grid, e->threads, smem, s>>>(q, mode);
     CU(cudaGetLastError());
     return LG_OK;
 }
@@ -595,6 +597,7 @@ extern "C" int lg_create(const lg_config *cfg, int64_t n_envs, int64_t global_of
             }
         }
         if (e->OW > 64 || e->smem > 200 * 1024) e->geo = pick_geo(17, W);  // too wide: lane teams
+        e->frz_ok = e->geo == 1 && p.n_pins == 0 && !getenv("LG_NO_FRZ_DERIVE");
         if (e->geo == 1 && !p.stream_mode && p.n_ctrl == 0 && p.n_pins == 0 && !p.obs_u8 &&
             !getenv("LG_NO_ELIDE")) {
             int se = (int)((p.PB - p.OO + 31) / 32 + 1);
@@ -823,7 +826,7 @@ extern "C" int lg_import_state(lg_env *e, const lg_state *src, void *stream) {
     }
     CU(cudaSetDevice(e->device));
     cudaStream_t s = (cudaStream_t)stream;
-    if (!e->elide_ok) return launch_state(e, *src, false, s);
+    if (!e->frz_ok && !e->elide_ok) return launch_state(e, *src, false, s);
     // the import kernel flags envs whose frozen plane is not their border plane
     CU(cudaMemsetAsync(e->base.aux, 0, 4, s));
     int rc = launch_state(e, *src, false, s);

@@ -14,6 +14,13 @@
 #include "env_kernels.cuh"
 #include "solo.cuh"
 
+#ifndef LG_ST_CLOBBER
+#define LG_ST_CLOBBER "memory"
+#endif
+#ifndef LG_WRITER_U
+#define LG_WRITER_U 2  // 256-bit stores in flight per lane in the float32 slot writer
+#endif
+
 namespace lg {
 
 template <int DOM>
@@ -34,14 +41,21 @@ __device__ __forceinline__ uint32_t *solo_rows(const Params &p, long long env) {
     return reinterpret_cast<uint32_t *>(p.rows) + (size_t)env * (Dom<DOM>::NPL + 1) * 8;
 }
 
+// Per-step state traffic is split: the "hot" part (tile planes, geometry,
+// counters) is read every step; the "cold" part (metric values and targets,
+// losses, RNG stream) only when the step recomputes, finishes an episode or
+// renders control planes. DRAM reads interleaved with the observation write
+// stream cost several times their size in write bandwidth (read/write
+// turnaround; tools/store_pattern.cu), so most steps read 72 bytes per env
+// instead of ~330.
 template <int DOM>
-__device__ __forceinline__ void solo_load(const Params &p, long long env, SoloEnv<DOM> &e) {
+__device__ __forceinline__ void solo_load_hot(const Params &p, long long env, SoloEnv<DOM> &e) {
     constexpr int NPL = Dom<DOM>::NPL;
     const uint4 *rw = reinterpret_cast<const uint4 *>(solo_rows<DOM>(p, env));
 #pragma unroll
-    for (int q = 0; q <= NPL; q++) {
+    for (int q = 0; q < NPL; q++) {
         uint4 a = rw[2 * q], b = rw[2 * q + 1];
-        SB &d = q < NPL ? e.pl[q] : e.frz;
+        SB &d = e.pl[q];
         d.w[0] = a.x; d.w[1] = a.y; d.w[2] = a.z; d.w[3] = a.w;
         d.w[4] = b.x; d.w[5] = b.y; d.w[6] = b.z; d.w[7] = b.w;
     }
@@ -55,14 +69,45 @@ __device__ __forceinline__ void solo_load(const Params &p, long long env, SoloEn
     e.changes = hv.changes;
     e.t = hv.t;
     e.max_steps = hv.max_steps;
+    if (p.frz_derived) {  // no active frozen cell in any env: frozen = max grid minus the episode rect
+        e.frz = andnot(rect_sb(p.H, p.W), rect_sb(e.h, e.w));
+    } else {
+        uint4 a = rw[2 * NPL], b = rw[2 * NPL + 1];
+        SB &d = e.frz;
+        d.w[0] = a.x; d.w[1] = a.y; d.w[2] = a.z; d.w[3] = a.w;
+        d.w[4] = b.x; d.w[5] = b.y; d.w[6] = b.z; d.w[7] = b.w;
+    }
+}
+
+// vals: also the current metric values (control planes, repricing, export);
+// a recompute overwrites them, so a step only needs the targets.
+template <int DOM>
+__device__ __forceinline__ void solo_load_cold(const Params &p, long long env, SoloEnv<DOM> &e, bool vals) {
+    constexpr int M = Dom<DOM>::M;
     const int4 *mv = reinterpret_cast<const int4 *>(p.mv + env * 24);
-    int4 a = mv[0], b = mv[1], c = mv[2], d = mv[3], f = mv[4], h2 = mv[5];
-    e.val[0] = a.x; e.val[1] = a.y; e.val[2] = a.z; e.val[3] = a.w;
-    e.val[4] = b.x; e.val[5] = b.y; e.val[6] = b.z; e.unr = b.w; e.val[7] = 0;
-    e.lo[0] = c.x; e.lo[1] = c.y; e.lo[2] = c.z; e.lo[3] = c.w;
-    e.lo[4] = d.x; e.lo[5] = d.y; e.lo[6] = d.z; e.lo[7] = d.w;
-    e.hi[0] = f.x; e.hi[1] = f.y; e.hi[2] = f.z; e.hi[3] = f.w;
-    e.hi[4] = h2.x; e.hi[5] = h2.y; e.hi[6] = h2.z; e.hi[7] = h2.w;
+#pragma unroll
+    for (int k = 0; k < 8; k++) e.val[k] = e.lo[k] = e.hi[k] = 0;
+    e.unr = 0;
+    if (vals) {
+        int4 a = mv[0];
+        e.val[0] = a.x; e.val[1] = a.y; e.val[2] = a.z; e.val[3] = a.w;
+        if (M > 4) {
+            int4 b = mv[1];
+            e.val[4] = b.x; e.val[5] = b.y; e.val[6] = b.z; e.unr = b.w;
+        } else {
+            e.unr = p.mv[env * 24 + 7];
+        }
+    }
+    {
+        int4 c = mv[2], f = mv[4];
+        e.lo[0] = c.x; e.lo[1] = c.y; e.lo[2] = c.z; e.lo[3] = c.w;
+        e.hi[0] = f.x; e.hi[1] = f.y; e.hi[2] = f.z; e.hi[3] = f.w;
+        if (M > 4) {
+            int4 d = mv[3], h2 = mv[5];
+            e.lo[4] = d.x; e.lo[5] = d.y; e.lo[6] = d.z; e.lo[7] = d.w;
+            e.hi[4] = h2.x; e.hi[5] = h2.y; e.hi[6] = h2.z; e.hi[7] = h2.w;
+        }
+    }
     const double2 *lv = reinterpret_cast<const double2 *>(p.lossv + env * 4);
     double2 l0 = lv[0], l1 = lv[1];
     e.prev_loss = l0.x;
@@ -78,8 +123,14 @@ __device__ __forceinline__ void solo_load(const Params &p, long long env, SoloEn
 }
 
 template <int DOM>
+__device__ __forceinline__ void solo_load(const Params &p, long long env, SoloEnv<DOM> &e) {
+    solo_load_hot<DOM>(p, env, e);
+    solo_load_cold<DOM>(p, env, e, true);
+}
+
+template <int DOM>
 __device__ __forceinline__ void solo_store(const Params &p, long long env, const SoloEnv<DOM> &e, bool rows_dirty,
-                           bool planes_dirty, bool metrics_dirty, bool rng_dirty) {
+                           bool planes_dirty, bool metrics_dirty, bool rng_dirty, bool cold = true) {
     constexpr int NPL = Dom<DOM>::NPL;
     if (rows_dirty || planes_dirty) {
         uint4 *rw = reinterpret_cast<uint4 *>(solo_rows<DOM>(p, env));
@@ -122,7 +173,7 @@ __device__ __forceinline__ void solo_store(const Params &p, long long env, const
         mv[5] = make_int4(e.hi[4], e.hi[5], e.hi[6], e.hi[7]);
     }
     double2 *lv = reinterpret_cast<double2 *>(p.lossv + env * 4);
-    lv[0] = make_double2(e.prev_loss, e.ep_reward);
+    if (cold) lv[0] = make_double2(e.prev_loss, e.ep_reward);
     if (metrics_dirty) lv[1] = make_double2(e.ep_start_loss, 0.0);
     if (rng_dirty) {
         p.rs[env] = make_ulonglong2((unsigned long long)(e.g.s >> 64), (unsigned long long)e.g.s);
@@ -445,7 +496,7 @@ __device__ __forceinline__ float solo_elem(const Params &p, const uint32_t *wimg
 __device__ __forceinline__ void st_cs_v8(float *ptr, const float *v) {
     asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(ptr), "f"(v[0]), "f"(v[1]),
                  "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
-                 : "memory");
+                 : LG_ST_CLOBBER);
 }
 
 // Expand the warp's 32 images to float32. VEC = 8 (32-byte stores) or 4.
@@ -530,6 +581,9 @@ __device__ void solo_write_noctrl(const Params &p, const uint32_t *wimg, long lo
     // elided frozen plane: elements [PF, PE) read the border plane [PF-OO, PF)
     const uint32_t OO = p.OO, PF = p.elide ? PE - OO : PE;
     uint32_t q0 = lane;
+#ifdef LG_EXP_UNROLL
+#pragma unroll LG_EXP_UNROLL
+#endif
     for (; q0 + (uint32_t)nthr * (U - 1) < nv; q0 += (uint32_t)nthr * U) {
         uint32_t x[U];
 #pragma unroll
@@ -539,6 +593,7 @@ __device__ void solo_write_noctrl(const Params &p, const uint32_t *wimg, long lo
             const uint32_t wi = b >> 5;
             uint32_t v = __funnelshift_r(sl[wi], sl[wi + 1], b & 31);
             const uint32_t kf = PF - le[u];
+#ifndef LG_EXP_NOSTRADDLE
             if (kf < 8) {  // group straddles the start of the (elided) frozen plane
                 const uint32_t b2 = PF - OO, w2 = b2 >> 5;
                 const uint32_t v2 = __funnelshift_r(sl[w2], sl[w2 + 1], b2 & 31);
@@ -550,6 +605,7 @@ __device__ void solo_write_noctrl(const Params &p, const uint32_t *wimg, long lo
                 uint32_t m = (1u << k) - 1u;
                 v = (v & m) | ((sl[stride] << k) & ~m);
             }
+#endif
             x[u] = v;
         }
 #pragma unroll
@@ -585,7 +641,7 @@ __device__ void solo_write_noctrl(const Params &p, const uint32_t *wimg, long lo
 __device__ __forceinline__ void st_cs_v8u(uint8_t *ptr, const uint32_t *v) {
     asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(ptr), "r"(v[0]), "r"(v[1]),
                  "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
-                 : "memory");
+                 : LG_ST_CLOBBER);
 }
 
 // uint8 observation writer (opt-in, no control planes), slot layout: 32
@@ -681,7 +737,10 @@ __device__ __forceinline__ void solo_env(const Params &p, int mode, long long en
                                          bool stream, uint32_t bit0, bool last) {
     constexpr int N = Dom<DOM>::N;
     SoloEnv<DOM> e;
-    solo_load<DOM>(p, env, e);
+    solo_load_hot<DOM>(p, env, e);
+    // control planes render the metric values; the other modes use everything
+    bool cold = mode != MODE_STEP || p.n_ctrl > 0;
+    if (cold) solo_load_cold<DOM>(p, env, e, true);
     bool rows_dirty = false, planes_dirty = false, metrics_dirty = false, rng_dirty = false;
     bool wrote = false, reset_now = false;
     double before = 0.0;
@@ -731,8 +790,14 @@ __device__ __forceinline__ void solo_env(const Params &p, int mode, long long en
             solo_set_tile<DOM>(e, r, c, tile);
             planes_dirty = true;
             e.changes += 1;
-            before = e.prev_loss;
         }
+        // this step recomputes or ends the episode (done depends only on counters)
+        bool ends = e.t + 1 >= e.max_steps || (p.budget > 0 && e.changes >= p.budget);
+        if (!cold && (wrote || ends)) {
+            solo_load_cold<DOM>(p, env, e, false);
+            cold = true;
+        }
+        before = e.prev_loss;
     } else if (mode == MODE_RESET) {
         reset_now = !p.reset_mask || p.reset_mask[env];
     } else if (mode == MODE_RECOMPUTE) {
@@ -789,7 +854,7 @@ __device__ __forceinline__ void solo_env(const Params &p, int mode, long long en
             reset_now = done && !p.no_auto_reset;
         }
     }
-    if (mode != MODE_OBSERVE) solo_store<DOM>(p, env, e, rows_dirty, planes_dirty, metrics_dirty, rng_dirty);
+    if (mode != MODE_OBSERVE) solo_store<DOM>(p, env, e, rows_dirty, planes_dirty, metrics_dirty, rng_dirty, cold);
     if (p.obs) solo_render<DOM>(p, e, img, stream, bit0, last);
 }
 
@@ -868,7 +933,7 @@ __device__ __forceinline__ void env_solo_body(const Params &p, int mode) {
     // obs base is 16-byte aligned (checked on the host) and env0 is a multiple
     // of 8, so every block's output starts 32-byte aligned when the base is.
     if ((reinterpret_cast<uintptr_t>(p.obs + first) & 31) == 0) {
-        if (p.PB == p.PE) solo_write_noctrl<2>(p, img, env0, nenv, wl, nthr);
+        if (p.PB == p.PE) solo_write_noctrl<LG_WRITER_U>(p, img, env0, nenv, wl, nthr);
         else solo_write<8, 2>(p, img, env0, nenv, wl, nthr);
     } else {
         solo_write<4, 2>(p, img, env0, nenv, wl, nthr);
