@@ -370,7 +370,9 @@ def main():
                               env.observation_shape[2] / 1e9)},
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
                          "frac": achieved_gbs / peak, "traffic": load_traffic(args.config),
-                         "peak_kind": peak_kind, "kernel": "env_kernel (fused step + obs)",
+                         "peak_kind": peak_kind, "frac_of_8000_nominal": achieved_gbs / 8000.0,
+                         "kernel": (f"env_solo_kernel_{cfg.domain}" if env._desc.team == 1 else
+                                    f"env_kernel<team {env._desc.team}, {cfg.domain}>") + " (fused step + obs)",
                          "bytes_per_env_step": bytes_step, "step_kernel_ms": step_ms},
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -738,8 +738,8 @@ __device__ __forceinline__ void solo_env(const Params &p, int mode, long long en
     constexpr int N = Dom<DOM>::N;
     SoloEnv<DOM> e;
     solo_load_hot<DOM>(p, env, e);
-    // control planes render the metric values; the other modes use everything
-    bool cold = mode != MODE_STEP || p.n_ctrl > 0;
+    // control planes render the metric values; reset/recompute/reprice use everything
+    bool cold = (mode != MODE_STEP && mode != MODE_OBSERVE) || p.n_ctrl > 0;
     if (cold) solo_load_cold<DOM>(p, env, e, true);
     bool rows_dirty = false, planes_dirty = false, metrics_dirty = false, rng_dirty = false;
     bool wrote = false, reset_now = false;

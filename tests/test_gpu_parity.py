@@ -263,6 +263,55 @@ def test_large_batch_warp_mode_against_oracle(case, layout, monkeypatch):
         assert np.array_equal(_np(o1), o2), t
 
 
+@pytest.mark.parametrize("frozen_edit", [False, True])
+def test_imported_frozen_cells_leave_the_fast_layout(frozen_edit, monkeypatch):
+    """A no-pinpoint warp-mode batch skips the frozen plane (shared image and
+    state reads) while every env's frozen plane is its border plane. Importing
+    a state with active frozen cells (designer pins, load_state_dict) must
+    switch back to the full layout: compare with the lane-team kernel, which
+    always reads and renders the stored frozen plane."""
+    cfg = EnvConfig(domain="binary", randomize_shape=True)
+    n = 20000
+    env = BatchEnv(cfg, n, seed=4)
+    env.reset()
+    act = np.random.default_rng(8)
+    for _ in range(5):
+        env.step(act.integers(0, cfg.n_actions, size=n))
+    sd = env.state_dict()
+    if frozen_edit:  # freeze active cells and redo the scan order as with_pin does
+        from paper_2408_12525_b200.scalar import _scan_order, _serp_rank
+        rng = np.random.default_rng(0)
+        H, W = sd["tiles"].shape[1:]
+        rank = _serp_rank(H, W)
+        for b in rng.choice(n, size=500, replace=False):
+            h, w = sd["shape_hw"][b]
+            old = int(sd["order"][b, sd["pos_idx"][b]])
+            sd["frozen"][b, rng.integers(h), rng.integers(w)] = True
+            order = _scan_order(sd["active"][b], sd["frozen"][b])
+            k = int(np.searchsorted(rank[order], rank[old])) % order.size
+            sd["order"][b] = -1
+            sd["order"][b, :order.size] = order
+            sd["order_len"][b] = order.size
+            sd["pos_idx"][b] = k
+            sd["pos"][b] = divmod(int(order[k]), W)
+    fast = BatchEnv(cfg, n, seed=0)
+    fast.load_state_dict(sd)
+    monkeypatch.setenv("LG_FORCE_TEAM", "1")
+    team = BatchEnv(cfg, n, seed=0)
+    team.load_state_dict(sd)
+    assert np.array_equal(_np(fast.observe()), _np(team.observe()))
+    for t in range(12):
+        a = act.integers(0, cfg.n_actions, size=n)
+        o1, r1, d1, _ = fast.step(a)
+        o2, r2, d2, _ = team.step(a)
+        assert np.array_equal(_np(r1), _np(r2)), t
+        assert np.array_equal(_np(d1), _np(d2)), t
+        assert np.array_equal(_np(o1), _np(o2)), t
+    s1, s2 = fast.state_dict(), team.state_dict()
+    for k in ("tiles", "frozen", "values", "prev_loss", "t"):
+        assert np.array_equal(s1[k], s2[k]), k
+
+
 def test_full_size_c5_properties():
     """2^20 envs (config c5): size-independent invariants of the outputs, and a
     shard built with global_offset reproduces its slice of the full batch."""

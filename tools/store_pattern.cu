@@ -153,6 +153,12 @@ int main() {
         PRO_CASE(128, 2000, 122, true, "pro: load + 2000 ALU + image")
         PRO_CASE(128, 8000, 122, true, "pro: load + 8000 ALU + image")
         PRO_CASE(0, 8000, 122, true, "pro: 8000 ALU + image (no load)")
+        for (int kb : {24, 14, 10}) {
+            char name[96];
+            snprintf(name, sizeof name, "pro: 64B load + 2000 ALU, const data, smem %d KB/block", kb);
+            time([&] { region_pro<64, 2000, 0, false><<<blocks, threads, (size_t)kb * 1024>>>(p, state, 32); }, name);
+        }
+        PRO_CASE(64, 2000, 0, false, "pro: 64B load + 2000 ALU, const data, 31.5 KB")
     }
     for (int blocks : {148 * 8, 148 * 64})
         time([&] { gstride<<<blocks, 256>>>(p, (long long)(bytes / 32)); }, blocks == 148 * 8 ? "gstride 1184x256" : "gstride 9472x256");
