@@ -174,13 +174,22 @@ struct SoloK {
             depth++;
         }
     }
-    // count_regions (pathfind.py:116-130) as a sequential run union-find:
-    // nodes are runs of a row (id = row*8 + run index); a run touching a run
-    // of the previous row is united with it; regions = runs - merges.
-    __device__ __forceinline__ int regions(const SB &pass, void *scratch) const {
-        uint8_t *par = reinterpret_cast<uint8_t *>(scratch);
+    // count_regions (pathfind.py:116-130) as a one-pass run labelling held in
+    // registers: runs of set bits are nodes; only the runs of the previous row
+    // (the frontier) can still merge, so each keeps a component label (byte k
+    // of P0/P1 = label of run k) and a merge relabels the frontier with four
+    // byte-wise compare-selects. regions = runs - merges of distinct labels,
+    // the same count a union-find gives, without shared memory.
+    __device__ __forceinline__ static uint32_t lab(uint32_t L0, uint32_t L1, int k) {
+        return ((k < 4 ? L0 : L1) >> ((k & 3) << 3)) & 0xFFu;
+    }
+    __device__ __forceinline__ static uint32_t relabel(uint32_t w, uint32_t from4, uint32_t to4) {
+        const uint32_t m = __vcmpeq4(w, from4);
+        return (w & ~m) | (to4 & m);
+    }
+    __device__ __forceinline__ int regions(const SB &pass, void *) const {
         int runs = 0, merges = 0;
-        uint32_t prevR = 0, prevS = 0;
+        uint32_t prevR = 0, prevS = 0, P0 = 0, P1 = 0;
         // rolled row loop (instruction-cache footprint); the plane is shifted
         // down one row per iteration so the current row is always word 0's low half
         SB q = pass;
@@ -191,39 +200,29 @@ struct SoloK {
             for (int k = 0; k < 7; k++) q.w[k] = __funnelshift_r(q.w[k], q.w[k + 1], 16);
             q.w[7] >>= 16;
             uint32_t S = R & ~(R << 1);
-            int nr = __popc(S);
-            for (int i = 0; i < nr; i++) par[r * 8 + i] = (uint8_t)(r * 8 + i);
-            runs += nr;
+            runs += __popc(S);
+            // fresh label r*8 + k for run k of this row (<= 127, one byte)
+            uint32_t C0 = (uint32_t)(r * 8) * 0x01010101u + 0x03020100u;
+            uint32_t C1 = C0 + 0x04040404u;
             uint32_t C = R & prevR;
-            uint32_t CS = C & ~(C << 1);
-            // contacts arrive left to right, grouped by new run; a new run is
-            // only ever linked by its own contacts, so its current root is
-            // tracked in a register and only the old run needs a find
-            int cur_run = -1, root = 0;
+            uint32_t CS = C & ~(C << 1);  // one bit per (new run, old run) contact
             while (CS) {
                 int c = __ffs((int)CS) - 1;
                 CS &= CS - 1;
                 uint32_t upto = (2u << c) - 1u;
-                int ir = __popc(S & upto) - 1;
-                int b = (r - 1) * 8 + __popc(prevS & upto) - 1;
-                if (ir != cur_run) {
-                    cur_run = ir;
-                    root = r * 8 + ir;
-                }
-                while (par[b] != b) {
-                    par[b] = par[par[b]];
-                    b = par[b];
-                }
-                if (b != root) {  // link the larger root under the smaller
-                    if (b < root) {
-                        par[root] = (uint8_t)b;
-                        root = b;
-                    } else {
-                        par[b] = (uint8_t)root;
-                    }
+                int ir = __popc(S & upto) - 1, ia = __popc(prevS & upto) - 1;
+                uint32_t lc = lab(C0, C1, ir), la = lab(P0, P1, ia);
+                if (lc != la) {
+                    const uint32_t hi4 = max(lc, la) * 0x01010101u, lo4 = min(lc, la) * 0x01010101u;
+                    C0 = relabel(C0, hi4, lo4);
+                    C1 = relabel(C1, hi4, lo4);
+                    P0 = relabel(P0, hi4, lo4);
+                    P1 = relabel(P1, hi4, lo4);
                     merges++;
                 }
             }
+            P0 = C0;
+            P1 = C1;
             prevR = R;
             prevS = S;
         }
