@@ -181,7 +181,7 @@ struct SoloK {
     // byte-wise compare-selects. regions = runs - merges of distinct labels,
     // the same count a union-find gives, without shared memory.
     __device__ __forceinline__ static uint32_t lab(uint32_t L0, uint32_t L1, int k) {
-        return ((k < 4 ? L0 : L1) >> ((k & 3) << 3)) & 0xFFu;
+        return __byte_perm(L0, L1, (uint32_t)k) & 0xFFu;  // byte k of L1:L0
     }
     __device__ __forceinline__ static uint32_t relabel(uint32_t w, uint32_t from4, uint32_t to4) {
         const uint32_t m = __vcmpeq4(w, from4);
@@ -212,13 +212,20 @@ struct SoloK {
                 uint32_t upto = (2u << c) - 1u;
                 int ir = __popc(S & upto) - 1, ia = __popc(prevS & upto) - 1;
                 uint32_t lc = lab(C0, C1, ir), la = lab(P0, P1, ia);
-                if (lc != la) {
+                if (lc == la) continue;
+                merges++;
+                if (lc >= (uint32_t)(r * 8)) {
+                    // first contact of run ir: its fresh label occurs nowhere
+                    // else, so only byte ir changes (to the old run's label)
+                    const uint32_t j = (uint32_t)ir & 3u, sel = 0x3210u + ((4u - j) << (4u * j));
+                    if (ir < 4) C0 = __byte_perm(C0, la, sel);
+                    else C1 = __byte_perm(C1, la, sel);
+                } else {  // two frontier components meet: relabel the larger id
                     const uint32_t hi4 = max(lc, la) * 0x01010101u, lo4 = min(lc, la) * 0x01010101u;
                     C0 = relabel(C0, hi4, lo4);
                     C1 = relabel(C1, hi4, lo4);
                     P0 = relabel(P0, hi4, lo4);
                     P1 = relabel(P1, hi4, lo4);
-                    merges++;
                 }
             }
             P0 = C0;
