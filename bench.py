@@ -212,6 +212,7 @@ def main():
     dev = torch.device("cuda", local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    from paper_2408_12525_b200 import _lib
     from paper_2408_12525_b200.env import INFO_KEYS, BatchEnv, NumpyBatchEnv
 
     from paper_2408_12525_b200.sharding import EpisodeStats, max_over_ranks, shard
@@ -271,14 +272,18 @@ def main():
     achieved_gbs = B * bytes_step / (step_ms / 1e3) / 1e9
 
     # end to end through the public numpy API: H2D actions from pinned host
-    # memory, D2H obs/reward/done/info into pinned host buffers, every step.
-    e2e = None
-    if not args.no_e2e:
-        del obs
+    # memory, D2H of obs/reward/done/info into host arrays, every step. The
+    # observations cross PCIe as packed 0/1 bit planes (1 bit per element) and
+    # the library's host threads expand them into the caller's float32 array
+    # (lg_step_host); LG_HOST_EXPAND=0 gives the plain float32 copy for contrast.
+    import numpy as np
+
+    def e2e_run(obs_dtype: str, packed: bool):
+        os.environ["LG_HOST_EXPAND"] = "1" if packed else "0"
         torch.cuda.empty_cache()
-        nenv = NumpyBatchEnv(cfg, B, seed=0, device=dev, global_offset=offset, pinned=True, copy=False)
+        nenv = NumpyBatchEnv(cfg, B, seed=0, device=dev, global_offset=offset, pinned=True, copy=False,
+                             obs_dtype=obs_dtype)
         nenv.reset()
-        import numpy as np
         rng = np.random.default_rng(1)
         host_acts = [rng.integers(0, cfg.n_actions, size=B) for _ in range(args.e2e_steps + 1)]
         nenv.step(host_acts[0])
@@ -288,11 +293,28 @@ def main():
         for a in host_acts[1:]:
             nenv.step(a)
         dt = max_over_ranks(time.perf_counter() - t0, dev)
-        obs_b = 4 * int(np.prod(env.observation_shape))
-        e2e = {"value": global_b * args.e2e_steps / dt, "unit": UNIT,
-               "h2d_bytes_per_step": B * 8,
-               "d2h_bytes_per_step": B * (obs_b + 8 + 1 + 1 + 8 + 8 + 8 + 8),
-               "steps": args.e2e_steps, "api": "NumpyBatchEnv.step -> lg_step_host (pinned)"}
+        del nenv
+        os.environ.pop("LG_HOST_EXPAND", None)
+        n_el = B * int(np.prod(env.observation_shape))
+        use_packed = packed and not cfg.controllable
+        obs_d2h = (n_el + 31) // 32 * 4 if use_packed else n_el * (1 if obs_dtype == "uint8" else 4)
+        d2h = obs_d2h + B * (8 + 1 + 1 + 8 + 8 + 8 + 8)
+        out = {"value": global_b * args.e2e_steps / dt, "unit": UNIT,
+               "h2d_bytes_per_step": B * 8, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+               "pcie_d2h_gbs": d2h * args.e2e_steps / dt / 1e9,
+               "api": "NumpyBatchEnv.step -> lg_step_host (pinned)"}
+        if use_packed:
+            out["transfer"] = (f"packed 0/1 bit planes D2H, expanded to {obs_dtype} in the caller's array "
+                               f"by {_lib.load().lg_host_threads()} host threads (non-temporal stores)")
+        else:
+            out["transfer"] = f"{obs_dtype} observation copy D2H"
+        return out
+
+    e2e = None
+    if not args.no_e2e:
+        del obs
+        e2e = e2e_run("float32", True)
+        e2e["float32_copy"] = e2e_run("float32", False)
 
     # Side measurement (does not change the headline): the same workload with
     # the opt-in uint8 observation format (4x fewer bytes per env-step).
@@ -323,25 +345,7 @@ def main():
               "note": "opt-in obs_dtype='uint8' (same 0/1 planes); not the reference float32 contract"}
         del obs8, env8
         if not args.no_e2e:
-            # the same host-buffer e2e loop with uint8 observations (4x fewer PCIe bytes)
-            import numpy as np
-            _t.cuda.empty_cache()
-            n8 = NumpyBatchEnv(cfg, B, seed=0, device=dev, global_offset=offset, pinned=True, copy=False,
-                               obs_dtype="uint8")
-            n8.reset()
-            rng = np.random.default_rng(1)
-            host_acts = [rng.integers(0, cfg.n_actions, size=B) for _ in range(args.e2e_steps + 1)]
-            n8.step(host_acts[0])
-            if world > 1:
-                dist.barrier()
-            t0 = time.perf_counter()
-            for a in host_acts[1:]:
-                n8.step(a)
-            dt = max_over_ranks(time.perf_counter() - t0, dev)
-            u8["e2e"] = {"value": global_b * args.e2e_steps / dt, "unit": UNIT,
-                         "h2d_bytes_per_step": B * 8,
-                         "d2h_bytes_per_step": B * (c_ * h_ * w_ + 8 + 1 + 1 + 8 + 8 + 8 + 8)}
-            del n8
+            u8["e2e"] = e2e_run("uint8", True)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -135,9 +135,16 @@ int lg_step_flags(lg_env *env, const int64_t *actions_dev, void *obs_dev, double
 /* BatchEnv.observe (env.py:587-588). */
 int lg_observe(lg_env *env, void *obs_dev, void *stream);
 /* The same step with HOST buffers: H2D of actions and D2H of every output
- * happen inside the call, which returns after the stream synchronises. */
+ * happen inside the call, which returns after the stream synchronises.
+ * Observations without control planes cross PCIe packed (the kernel writes
+ * the 0/1 planes as one bit stream, element t = bit t) in chunks, and the
+ * library's host threads expand each chunk into obs_host (float32 or uint8,
+ * any alignment, pinned or pageable) as soon as its copy lands: 1/32 of the
+ * PCIe bytes of a float32 copy. LG_HOST_EXPAND=0 selects the plain copy. */
 int lg_step_host(lg_env *env, const int64_t *actions_host, void *obs_host, double *reward_host,
                  uint8_t *done_host, const lg_info *info_host, void *stream);
+/* Host threads lg_step_host expands observations with (LG_HOST_THREADS). */
+int lg_host_threads(void);
 
 /* Designer edits on imported states: recompute metrics + loss of the masked
  * envs (mask NULL = all) after their tiles/frozen planes changed (with_pin /

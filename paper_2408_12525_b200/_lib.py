@@ -77,6 +77,7 @@ SIGNATURES = {
     "lg_metrics": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _I64, _P, _P, _P, _P, _P,
                                   _P]),
     "lg_seed_streams": (ctypes.c_int, [ctypes.c_uint64, _I64, _I64, _P]),
+    "lg_host_threads": (ctypes.c_int, []),
 }
 
 _lib = None

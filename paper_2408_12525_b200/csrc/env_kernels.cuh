@@ -103,6 +103,7 @@ struct Params {
     int solo_E;     // solo kernel: envs per block (== blockDim: warp mode)
     int no_auto_reset;  // scalar step (env.py:611-630): finished envs are not reset
     int obs_u8;         // observation format: 0 = float32 (reference), 1 = uint8 0/1 planes
+    int obs_bits;       // packed transfer: `obs` is the batch's 0/1 planes as one u32 bit stream
     int stream_mode;   // solo: envs of a warp/block rendered into one contiguous bit stream
     int group_words;   // solo stream mode: shared words per warp (warp mode) or block
     int stream_words;  // solo stream mode: offset of the union-find scratch in a group
@@ -765,6 +766,35 @@ __device__ void write_obs_team_u8(const Params &p, const Team<G> &t, long long e
         out[e] = (img[e >> 5] >> (e & 31)) & 1u;
 }
 
+// Packed transfer (see solo_write_bits): env's PE bits at stream bits
+// [env*PE, env*PE + PE); words shared with a neighbouring env are OR-ed into
+// the zeroed stream, the ends of the batch are stored.
+template <class G>
+__device__ void write_obs_team_bits(const Params &p, const Team<G> &t, long long env, const unsigned char *es) {
+    const uint32_t *img = reinterpret_cast<const uint32_t *>(es);
+    uint32_t *out = reinterpret_cast<uint32_t *>(p.obs);
+    const uint32_t PE = p.PE;
+    const unsigned long long g0 = (unsigned long long)env * PE;
+    const uint32_t sh = (uint32_t)(g0 & 31), nw = (sh + PE + 31) >> 5;
+    const unsigned long long w0 = g0 >> 5;
+    for (uint32_t i = t.lane; i < nw; i += G::TEAM) {
+        uint32_t v, lp;  // local bits [lp, lp + 32) land at bits [0, 32) (or [sh, 32) for word 0)
+        if (i == 0) {
+            v = img[0];
+            lp = 0;
+        } else {
+            lp = 32 * i - sh;
+            v = __funnelshift_r(img[lp >> 5], img[(lp >> 5) + 1], lp & 31);
+        }
+        const uint32_t avail = PE - lp;  // local bits left from lp
+        if (avail < 32) v &= (1u << avail) - 1u;
+        if (i == 0) v <<= sh;
+        const bool shared = (i == 0 && sh && env > 0) || (i == nw - 1 && ((sh + PE) & 31) && env + 1 < p.B);
+        if (shared) atomicOr(out + w0 + i, v);
+        else out[w0 + i] = v;
+    }
+}
+
 template <class G>
 __device__ void write_obs_team(const Params &p, const Team<G> &t, long long env, const unsigned char *es) {
     const uint32_t *img = reinterpret_cast<const uint32_t *>(es);
@@ -942,7 +972,8 @@ __global__ void __launch_bounds__(64) env_kernel(const Params p, int mode) {
             t.sync();  // union-find scratch is reused for the image
             render_env<G, DOM>(p, t, e, es);
             t.sync();
-            if (p.obs_u8) write_obs_team_u8<G>(p, t, env, es);
+            if (p.obs_bits) write_obs_team_bits<G>(p, t, env, es);
+            else if (p.obs_u8) write_obs_team_u8<G>(p, t, env, es);
             else write_obs_team<G>(p, t, env, es);
         }
     }

@@ -7,9 +7,11 @@
 
 #include <mutex>
 #include <new>
+#include <vector>
 
 #include "../../include/pcgrl_b200.h"
 #include "env_kernels.cuh"
+#include "host_expand.h"
 #include "solo_kernel.cuh"
 
 using namespace lg;
@@ -300,6 +302,12 @@ struct lg_env {
     unsigned char *d_done = nullptr, *d_term = nullptr;
     double *d_er = nullptr, *d_es = nullptr, *d_fl = nullptr;
     long long *d_el = nullptr;
+    // packed observation transfer (lg_step_host): device bit stream, pinned
+    // host copy, one event per copied chunk
+    uint32_t *d_bits = nullptr;
+    uint8_t *h_bits = nullptr;
+    size_t bits_bytes = 0, chunk_bytes = 0;
+    std::vector<cudaEvent_t> chunk_ev;
 };
 
 static void fastdiv_init(FastDiv &f, uint32_t d) {
@@ -672,9 +680,12 @@ extern "C" int lg_destroy(lg_env *e) {
     cudaSetDevice(e->device);
     Params &p = e->base;
     void *ptrs[] = {p.rows, p.hot, p.mv, p.lossv, p.rs, p.ri, p.rb, p.mseed, p.err, p.aux,
-                    e->d_act, e->d_obs, e->d_rew, e->d_done, e->d_term, e->d_er, e->d_es, e->d_fl, e->d_el};
+                    e->d_act, e->d_obs, e->d_rew, e->d_done, e->d_term, e->d_er, e->d_es, e->d_fl, e->d_el,
+                    e->d_bits};
     for (void *q : ptrs)
         if (q) cudaFree(q);
+    if (e->h_bits) cudaFreeHost(e->h_bits);
+    for (cudaEvent_t ev : e->chunk_ev) cudaEventDestroy(ev);
     delete e;
     return LG_OK;
 }
@@ -707,7 +718,7 @@ static int check_obs_ptr(const void *obs) {
 
 static int run_mode(lg_env *e, int mode, const long long *actions, void *obs, double *reward,
                     uint8_t *done, const lg_info *info, double *stats, const uint8_t *mask, void *stream,
-                    unsigned flags = 0) {
+                    unsigned flags = 0, bool obs_bits = false) {
     if (!e) {
         set_err("null env");
         return LG_EINVAL;
@@ -733,6 +744,7 @@ static int run_mode(lg_env *e, int mode, const long long *actions, void *obs, do
     p.stats = stats;
     p.reset_mask = mask;
     p.no_auto_reset = (flags & LG_STEP_NO_AUTO_RESET) ? 1 : 0;
+    p.obs_bits = obs_bits ? 1 : 0;
     return launch_env(e, p, mode, (cudaStream_t)stream);
 }
 
@@ -766,6 +778,36 @@ extern "C" int lg_step_flags(lg_env *e, const int64_t *actions, void *obs, doubl
                     stream, flags);
 }
 
+// Packed transfer is used when every observation element is a 0/1 plane
+// element (no control planes); LG_HOST_EXPAND=0 forces the float32 copy.
+static bool packed_ok(const lg_env *e) {
+    if (e->cfg.n_ctrl > 0) return false;
+    const char *v = getenv("LG_HOST_EXPAND");
+    return !(v && v[0] == '0');
+}
+
+// Some stream words are shared by two blocks (or lane teams): they are
+// merged with atomicOr into a zeroed stream. Warp-mode solo launches own
+// whole words (32 envs x PE bits), so no zeroing is needed there.
+static bool packed_needs_zero(const lg_env *e) {
+    const uint64_t PE = e->base.PE;
+    if (e->geo != 1) return PE % 32 != 0;
+    return ((uint64_t)e->E * PE) % 32 != 0;
+}
+
+struct ChunkPoll {
+    lg_env *e;
+    bool failed;
+};
+static bool chunk_ready(void *ctx, size_t c) {
+    ChunkPoll *cp = static_cast<ChunkPoll *>(ctx);
+    cudaSetDevice(cp->e->device);
+    cudaError_t r = cudaEventQuery(cp->e->chunk_ev[c]);
+    if (r == cudaErrorNotReady) return false;
+    if (r != cudaSuccess) cp->failed = true;  // stop waiting; reported after the sync
+    return true;
+}
+
 extern "C" int lg_step_host(lg_env *e, const int64_t *actions_host, void *obs_host, double *reward_host,
                             uint8_t *done_host, const lg_info *info_host, void *stream) {
     if (!e || !actions_host || !reward_host || !done_host) {
@@ -774,7 +816,9 @@ extern "C" int lg_step_host(lg_env *e, const int64_t *actions_host, void *obs_ho
     }
     CU(cudaSetDevice(e->device));
     size_t B = (size_t)e->B;
-    size_t obs_bytes = B * (size_t)e->C * e->OH * e->OW * (e->base.obs_u8 ? 1 : sizeof(float));
+    const size_t n_elems = B * (size_t)e->C * e->OH * e->OW;
+    size_t obs_bytes = n_elems * (e->base.obs_u8 ? 1 : sizeof(float));
+    const bool packed = obs_host && packed_ok(e);
     if (!e->d_act) {
         CU(cudaMalloc((void **)&e->d_act, B * 8));
         CU(cudaMalloc((void **)&e->d_rew, B * 8));
@@ -785,14 +829,38 @@ extern "C" int lg_step_host(lg_env *e, const int64_t *actions_host, void *obs_ho
         CU(cudaMalloc((void **)&e->d_fl, B * 8));
         CU(cudaMalloc((void **)&e->d_el, B * 8));
     }
-    if (obs_host && !e->d_obs) CU(cudaMalloc((void **)&e->d_obs, obs_bytes));
+    if (packed && !e->d_bits) {
+        e->bits_bytes = ((n_elems + 31) / 32) * 4;
+        const char *cm = getenv("LG_EXPAND_CHUNK_MB");
+        size_t chunk = (size_t)(cm ? atof(cm) * (1 << 20) : 8.0 * (1 << 20));
+        chunk = chunk < 4096 ? 4096 : (chunk & ~(size_t)63);
+        e->chunk_bytes = chunk;
+        size_t nchunks = (e->bits_bytes + chunk - 1) / chunk;
+        CU(cudaMalloc((void **)&e->d_bits, e->bits_bytes));
+        CU(cudaHostAlloc((void **)&e->h_bits, e->bits_bytes, cudaHostAllocDefault));
+        e->chunk_ev.resize(nchunks);
+        for (auto &ev : e->chunk_ev) CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
+    if (obs_host && !packed && !e->d_obs) CU(cudaMalloc((void **)&e->d_obs, obs_bytes));
     cudaStream_t s = (cudaStream_t)stream;
     CU(cudaMemcpyAsync(e->d_act, actions_host, B * 8, cudaMemcpyHostToDevice, s));
+    if (packed && packed_needs_zero(e)) CU(cudaMemsetAsync(e->d_bits, 0, e->bits_bytes, s));
     lg_info di = {e->d_term, e->d_er, (int64_t *)e->d_el, e->d_es, e->d_fl};
-    int rc = lg_step(e, (const int64_t *)e->d_act, obs_host ? e->d_obs : nullptr, e->d_rew, e->d_done,
-                     info_host ? &di : nullptr, nullptr, stream);
+    void *dev_obs = obs_host ? (packed ? (void *)e->d_bits : e->d_obs) : nullptr;
+    int rc = run_mode(e, MODE_STEP, (const long long *)e->d_act, dev_obs, e->d_rew, e->d_done,
+                      info_host ? &di : nullptr, nullptr, nullptr, stream, 0, packed);
     if (rc) return rc;
-    if (obs_host) CU(cudaMemcpyAsync(obs_host, e->d_obs, obs_bytes, cudaMemcpyDeviceToHost, s));
+    if (packed) {  // the bit stream in chunks, one event each, so expansion overlaps the copy
+        for (size_t c = 0; c < e->chunk_ev.size(); c++) {
+            size_t off = c * e->chunk_bytes, len = e->bits_bytes - off;
+            if (len > e->chunk_bytes) len = e->chunk_bytes;
+            CU(cudaMemcpyAsync(e->h_bits + off, reinterpret_cast<uint8_t *>(e->d_bits) + off, len,
+                               cudaMemcpyDeviceToHost, s));
+            CU(cudaEventRecord(e->chunk_ev[c], s));
+        }
+    } else if (obs_host) {
+        CU(cudaMemcpyAsync(obs_host, e->d_obs, obs_bytes, cudaMemcpyDeviceToHost, s));
+    }
     CU(cudaMemcpyAsync(reward_host, e->d_rew, B * 8, cudaMemcpyDeviceToHost, s));
     CU(cudaMemcpyAsync(done_host, e->d_done, B, cudaMemcpyDeviceToHost, s));
     if (info_host) {
@@ -806,9 +874,22 @@ extern "C" int lg_step_host(lg_env *e, const int64_t *actions_host, void *obs_ho
         if (info_host->final_loss)
             CU(cudaMemcpyAsync(info_host->final_loss, e->d_fl, B * 8, cudaMemcpyDeviceToHost, s));
     }
+    if (packed) {
+        ChunkPoll cp{e, false};
+        lg_host::expand_bits(e->h_bits, obs_host, e->base.obs_u8 ? 1 : 0, n_elems, e->chunk_bytes, chunk_ready,
+                             &cp);
+        CU(cudaStreamSynchronize(s));
+        if (cp.failed) {
+            set_err("CUDA error while copying the packed observations");
+            return LG_ECUDA;
+        }
+        return LG_OK;
+    }
     CU(cudaStreamSynchronize(s));
     return LG_OK;
 }
+
+extern "C" int lg_host_threads(void) { return lg_host::expand_threads(); }
 
 extern "C" int lg_export_state(lg_env *e, const lg_state *dst, void *stream) {
     if (!e || !dst) {

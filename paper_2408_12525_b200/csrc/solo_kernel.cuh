@@ -731,6 +731,90 @@ __device__ void solo_write_stream(const Params &p, const uint32_t *st, long long
     for (uint32_t t = nv * VEC + lane; t < total; t += nthr) out[t] = ((st[sidx(t >> 5)] >> (t & 31)) & 1u) ? 1.0f : 0.0f;
 }
 
+// ---------------------------------------------------------------------------
+// Packed observation transfer (lg_step_host): the 0/1 planes of the whole
+// batch as ONE bit stream, element t of the float32 [B,C,OH,OW] observation
+// = bit t (word t/32, bit t%32). The host library expands it to the caller's
+// float32/uint8 array, so PCIe carries 1 bit per element instead of 32.
+// Words that straddle a block's range boundary are shared with the
+// neighbouring block and merged with atomicOr into a zeroed buffer (the host
+// zeroes it when such words exist); words at the ends of the batch are private.
+// ---------------------------------------------------------------------------
+
+// local stream bits [lpos, min(lpos + 32, lend)) of the group's slot images
+// (bit j of the result = local bit lpos + j), with the elided frozen plane
+// read from the border plane as in solo_write_noctrl.
+__device__ __forceinline__ uint32_t solo_bits32(const Params &p, const uint32_t *wimg, uint32_t lpos, uint32_t lend) {
+    const uint32_t PE = p.PE, OO = p.OO, PF = p.elide ? PE - OO : PE, stride = (uint32_t)p.env_smem;
+    uint32_t el = fdiv(p.divPE, lpos), le = lpos - el * PE;
+    uint32_t acc = 0, got = 0;
+    while (got < 32 && lpos < lend) {
+        const uint32_t seg_end = le < PF ? PF : PE;
+        uint32_t take = 32 - got;
+        if (seg_end - le < take) take = seg_end - le;
+        if (lend - lpos < take) take = lend - lpos;
+        const uint32_t phys = le >= PF ? le - OO : le;
+        const uint32_t *sl = wimg + el * stride;
+        uint32_t bits = __funnelshift_r(sl[phys >> 5], sl[(phys >> 5) + 1], phys & 31);
+        if (take < 32) bits &= (1u << take) - 1u;
+        acc |= bits << got;
+        got += take;
+        lpos += take;
+        le += take;
+        if (le == PE) {
+            el++;
+            le = 0;
+        }
+    }
+    return acc;
+}
+
+__device__ __forceinline__ void put_bits_word(const Params &p, uint32_t *out, unsigned long long w, uint32_t v,
+                                              bool shared) {
+    if (shared) atomicOr(out + w, v);
+    else out[w] = v;
+}
+
+// slot layout: envs [env0, env0 + nenv) -> stream bits [env0*PE, (env0+nenv)*PE)
+__device__ void solo_write_bits(const Params &p, const uint32_t *wimg, long long env0, int nenv, int lane, int nthr) {
+    uint32_t *out = reinterpret_cast<uint32_t *>(p.obs);
+    const unsigned long long g0 = (unsigned long long)env0 * p.PE;
+    const uint32_t TB = (uint32_t)nenv * p.PE, sh = (uint32_t)(g0 & 31);
+    const unsigned long long w0 = g0 >> 5;
+    const uint32_t nw = (sh + TB + 31) >> 5;
+    const bool at_end = env0 + nenv >= p.B;
+    for (uint32_t i = (uint32_t)lane; i < nw; i += (uint32_t)nthr) {
+        uint32_t v;
+        if (i == 0 && sh) v = solo_bits32(p, wimg, 0, TB < 32 - sh ? TB : 32 - sh) << sh;
+        else v = solo_bits32(p, wimg, 32 * i - sh, TB);
+        const bool shared = (i == 0 && sh) || (i == nw - 1 && ((sh + TB) & 31) && !at_end);
+        put_bits_word(p, out, w0 + i, v, shared);
+    }
+}
+
+// stream layout: the group's shared-memory stream already is the packed bits
+__device__ void solo_write_stream_bits(const Params &p, const uint32_t *st, long long env0, int nenv, int lane,
+                                       int nthr) {
+    uint32_t *out = reinterpret_cast<uint32_t *>(p.obs);
+    const unsigned long long g0 = (unsigned long long)env0 * p.PE;
+    const uint32_t TB = (uint32_t)nenv * p.PE, sh = (uint32_t)(g0 & 31);
+    const unsigned long long w0 = g0 >> 5;
+    const uint32_t nw = (sh + TB + 31) >> 5, nwl = (TB + 31) >> 5;
+    const bool at_end = env0 + nenv >= p.B;
+    for (uint32_t i = (uint32_t)lane; i < nw; i += (uint32_t)nthr) {
+        uint32_t a = i < nwl ? st[sidx(i)] : 0u;
+        if (i == nwl - 1 && (TB & 31)) a &= (1u << (TB & 31)) - 1u;
+        uint32_t v = a;
+        if (sh) {
+            uint32_t b = i >= 1 ? st[sidx(i - 1)] : 0u;
+            if (i - 1 == nwl - 1 && (TB & 31)) b &= (1u << (TB & 31)) - 1u;
+            v = (a << sh) | (i >= 1 ? (b >> (32 - sh)) : 0u);
+        }
+        const bool shared = (i == 0 && sh) || (i == nw - 1 && ((sh + TB) & 31) && !at_end);
+        put_bits_word(p, out, w0 + i, v, shared);
+    }
+}
+
 // One env, one thread: step / reset / observe, then render its image into `slot`.
 template <int DOM>
 __device__ __forceinline__ void solo_env(const Params &p, int mode, long long env, uint32_t *slot, uint32_t *img,
@@ -901,7 +985,9 @@ __device__ __forceinline__ void env_solo_body(const Params &p, int mode) {
         if (warp_mode) __syncwarp();
         else __syncthreads();
         if (nenv <= 0) return;
-        if (p.obs_u8) {
+        if (p.obs_bits) {
+            solo_write_stream_bits(p, grp, env0, nenv, wl, nthr);
+        } else if (p.obs_u8) {
             // env0 is a multiple of 32, so the warp's byte range is 32-byte aligned
             solo_write_stream_u8(p, grp, env0, nenv, wl, nthr);
         } else if ((reinterpret_cast<uintptr_t>(p.obs + (size_t)env0 * p.PE) & 31) == 0) {
@@ -916,6 +1002,10 @@ __device__ __forceinline__ void env_solo_body(const Params &p, int mode) {
     if (warp_mode) __syncwarp();
     else __syncthreads();
     if (nenv <= 0) return;
+    if (p.obs_bits) {
+        solo_write_bits(p, img, env0, nenv, wl, nthr);
+        return;
+    }
     const size_t first = (size_t)env0 * p.PE;
     if (p.obs_u8) {
         const uintptr_t a = reinterpret_cast<uintptr_t>(reinterpret_cast<uint8_t *>(p.obs) + first);

@@ -433,3 +433,70 @@ def test_uint8_observations_equal_float32(case, monkeypatch):
 def test_uint8_rejects_control_planes():
     with pytest.raises(ValueError):
         BatchEnv(EnvConfig(domain="maze", controllable=("path_length",)), 8, obs_dtype="uint8")
+
+
+# Packed observation transfer (lg_step_host): the kernel writes the 0/1 planes
+# as one bit stream, the host library expands it into the caller's array.
+PACKED_CASES = [
+    (dict(domain="binary"), 40000, {}),                                   # solo warp, slot + elided frozen plane
+    (dict(domain="binary"), 19001, {}),                                   # ragged last warp
+    (dict(domain="dungeon", representation="wide", pinpoints=("player", "key", "door"),
+          randomize_shape=True), 20000, {}),                              # solo warp, stream layout
+    (dict(domain="binary"), 20000, {"LG_STREAM": "1"}),                   # stream layout, PE % 32 != 0
+    (dict(domain="binary"), 64, {}),                                      # c1: block mode, shared words
+    (dict(domain="maze", representation="turtle"), 300, {}),              # block mode, E * PE % 32 != 0
+    (dict(domain="maze", representation="turtle"), 4096, {}),             # c2: lane team 16
+    (dict(domain="binary", max_width=64, max_height=64, obs_size=7), 500, {}),   # lane team 64 (c4 shape)
+    (dict(domain="dungeon", max_width=40, max_height=20, obs_size=33), 257, {}),  # team 32, odd sizes
+    (dict(domain="binary", max_width=8, max_height=8, obs_size=3), 37, {}),       # PE = 36 bits
+    (dict(domain="maze", controllable=("path_length", "regions")), 500, {}),      # control planes: f32 copy
+]
+
+
+@pytest.mark.parametrize("obs_dtype", ["float32", "uint8"])
+@pytest.mark.parametrize("case", range(len(PACKED_CASES)))
+def test_packed_host_transfer_equals_device_obs(case, obs_dtype, monkeypatch):
+    """NumpyBatchEnv.step (packed bits over PCIe, host expansion) returns the
+    same observations as the device path, for every kernel and layout."""
+    kw, n, envs = PACKED_CASES[case]
+    for k, v in envs.items():
+        monkeypatch.setenv(k, v)
+    cfg = EnvConfig(**kw)
+    if obs_dtype == "uint8" and cfg.controllable:
+        pytest.skip("uint8 observations exclude control planes")
+    dev = BatchEnv(cfg, n, seed=9, obs_dtype=obs_dtype)
+    host = NumpyBatchEnv(cfg, n, seed=9, obs_dtype=obs_dtype, pinned=(case % 2 == 0), copy=False)
+    assert np.array_equal(_np(dev.reset()), host.reset())
+    rng = np.random.default_rng(case)
+    for t in range(4):
+        a = rng.integers(0, cfg.n_actions, size=n)
+        o1, r1, d1, i1 = dev.step(torch.from_numpy(a).cuda())
+        o2, r2, d2, i2 = host.step(a)
+        assert o2.dtype == np.dtype(obs_dtype)
+        assert np.array_equal(_np(o1), o2), t
+        assert np.array_equal(_np(r1), r2) and np.array_equal(_np(d1), d2), t
+        assert all(np.array_equal(_np(i1[k]), i2[k]) for k in i2), t
+
+
+def test_packed_and_float32_copy_paths_agree(monkeypatch):
+    """LG_HOST_EXPAND=0 (float32 copy) and the packed path give equal arrays,
+    including unaligned host buffers (numpy arrays offset by 4 bytes)."""
+    cfg = EnvConfig(domain="binary")
+    n = 1000
+    a = NumpyBatchEnv(cfg, n, seed=2, copy=False)
+    b = NumpyBatchEnv(cfg, n, seed=2, copy=False)
+    a.reset()
+    b.reset()
+    rng = np.random.default_rng(0)
+    for t in range(4):
+        acts = rng.integers(0, cfg.n_actions, size=n)
+        monkeypatch.setenv("LG_HOST_EXPAND", "0")
+        o1 = a.step(acts)[0].copy()
+        monkeypatch.setenv("LG_HOST_EXPAND", "1")
+        o2 = b.step(acts)[0]
+        assert np.array_equal(o1, o2), t
+        if t == 1:  # from now on b expands into a 4-byte (not 16-byte) aligned array
+            raw = np.empty(o2.nbytes + 16, dtype=np.uint8)
+            off = (4 - raw.ctypes.data) % 16
+            b._bufs["obs"] = raw[off:off + o2.nbytes].view(np.float32).reshape(o2.shape)
+            assert b._bufs["obs"].ctypes.data % 16 == 4
