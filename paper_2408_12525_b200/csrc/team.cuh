@@ -150,16 +150,26 @@ __device__ __forceinline__ Bd<G> dilate(const Team<G> &t, const Bd<G> &f, typena
 
 // BFS from the cells of `f` through `pass`; on return `f` holds the last
 // non-empty layer and the result is its depth (flood_distance layers).
+// Two layers per team vote: layer 2 is non-empty only if layer 1 is, so one
+// __any_sync decides both (half the votes and loop branches of a per-layer loop).
 template <class G>
 __device__ __forceinline__ int bfs_last_layer(const Team<G> &t, Bd<G> &f, const Bd<G> &pass, typename G::Row wm) {
     Bd<G> vis = f;
     int depth = 0;
     while (true) {
-        Bd<G> nx = andnot(dilate(t, f, wm) & pass, vis);
-        if (!t.any(nx.nz())) return depth;
-        vis = vis | nx;
-        f = nx;
-        depth++;
+        Bd<G> n1 = andnot(dilate(t, f, wm) & pass, vis);
+        Bd<G> v1 = vis | n1;
+        Bd<G> n2 = andnot(dilate(t, n1, wm) & pass, v1);
+        if (!t.any(n2.nz())) {
+            if (t.any(n1.nz())) {
+                f = n1;
+                depth++;
+            }
+            return depth;
+        }
+        vis = v1 | n2;
+        f = n2;
+        depth += 2;
     }
 }
 
@@ -243,9 +253,44 @@ __device__ __forceinline__ int uf_unite(volatile uint16_t *par, int a, int b) {
     return 0;
 }
 
+// Two rows per lane (G64): the lane's rows (2l, 2l+1) form a strip whose run
+// overlap graph is a forest (two runs of one row never overlap, so a cycle
+// would need two runs of the other row sharing a column). Its components are
+// therefore counted without union-find: their spans are disjoint intervals and
+// a run start begins a new component unless the other row is set there (ties
+// go to the top row): K marks the component starts, popc(K) counts them, and
+// the component holding column c is popc(K & (bits <= c)) - 1. Only contacts
+// between strips (row 2l vs row 2l-1) go through the shared-memory
+// union-find, over strip-component nodes (id = lane * 64 + index).
+template <class G>
+__device__ __forceinline__ int count_regions_strips(const Team<G> &t, const Bd<G> &pass, uint16_t *par_smem) {
+    using Row = typename G::Row;
+    volatile uint16_t *par = par_smem;
+    const Row A = pass.r[0], Bv = pass.r[1];
+    const Row sA = A & ~(A << 1), sB = Bv & ~(Bv << 1);
+    const Row K = (sA & (~Bv | sB)) | (sB & ~A);
+    const int nk = popc(K);
+    const int base = t.lane * G::BITS;
+    for (int i = 0; i < nk; i++) par[base + i] = (uint16_t)(base + i);
+    const Row Kup = t.up(K), Bup = t.up(Bv);  // lane l-1: strip starts, row 2l-1
+    t.sync();
+    int links = 0;
+    Row C = A & Bup;
+    Row CS = C & ~(C << 1);
+    while (CS) {  // one union per contact run between row 2l-1 and row 2l
+        int c = ctz(CS);
+        CS &= CS - 1;
+        Row upto = (c == G::BITS - 1) ? ~Row(0) : ((Row(2) << c) - Row(1));
+        int i1 = popc(K & upto) - 1, i2 = popc(Kup & upto) - 1;
+        links += uf_unite(par, base + i1, base - G::BITS + i2);
+    }
+    return t.sum(nk - links);
+}
+
 template <class G>
 __device__ __forceinline__ int count_regions(const Team<G> &t, const Bd<G> &pass, uint16_t *par_smem) {
     using Row = typename G::Row;
+    if constexpr (G::RPL == 2) return count_regions_strips(t, pass, par_smem);
     volatile uint16_t *par = par_smem;
     int runs = 0;
 #pragma unroll
