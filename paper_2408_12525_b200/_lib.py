@@ -9,7 +9,7 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libpcgrl_b200.so")
+LIB_PATH = os.environ.get("LG_LIB_PATH") or os.path.join(_PKG, "libpcgrl_b200.so")  # override: experiments
 
 LG_OK, LG_EINVAL, LG_ECUDA = 0, 1, 2
 FLAG_BAD_ACTION, FLAG_NO_EDITABLE, FLAG_PINPOINTS = 1, 2, 4

@@ -831,7 +831,7 @@ __device__ void write_obs_team(const Params &p, const Team<G> &t, long long env,
 // ---------------------------------------------------------------------------
 
 template <class G, int DOM>
-__global__ void __launch_bounds__(64) env_kernel(const Params p, int mode) {
+__global__ void __launch_bounds__(64, G::MINB) env_kernel(const Params p, int mode) {
     extern __shared__ __align__(16) unsigned char smem[];
     using Row = typename G::Row;
     constexpr int N = Dom<DOM>::N, NPL = Dom<DOM>::NPL;

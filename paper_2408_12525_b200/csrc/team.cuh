@@ -15,8 +15,9 @@
 
 namespace lg {
 
-template <int TEAM_, int RPL_, typename Row_>
+template <int TEAM_, int RPL_, typename Row_, int MINB_ = 1>
 struct Geo {
+    static constexpr int MINB = MINB_;  // __launch_bounds__ min blocks (64-thread blocks) per SM
     static constexpr int TEAM = TEAM_;
     static constexpr int RPL = RPL_;
     static constexpr int ROWS = TEAM_ * RPL_;
@@ -26,7 +27,13 @@ struct Geo {
 };
 using G16 = Geo<16, 1, uint32_t>;  // H <= 16, W <= 32
 using G32 = Geo<32, 1, uint32_t>;  // H <= 32, W <= 32
-using G64 = Geo<32, 2, uint64_t>;  // H <= 64, W <= 64
+// 64x64 maps are latency-bound (BFS shuffles, union-find): occupancy pays
+// more than the spills of a 64-register budget (measured on c4, 32-thread
+// blocks: 80 regs 84M, 64 regs 92M, 48 regs 91M env-steps/s).
+#ifndef LG_G64_MINB
+#define LG_G64_MINB 16
+#endif
+using G64 = Geo<32, 2, uint64_t, LG_G64_MINB>;  // H <= 64, W <= 64
 
 __device__ __forceinline__ int ctz(uint32_t x) { return __ffs((int)x) - 1; }
 __device__ __forceinline__ int ctz(uint64_t x) { return __ffsll((long long)x) - 1; }
