@@ -148,11 +148,14 @@ void expand_bits(const uint8_t *bits, void *dst, int fmt, size_t n_elems, size_t
     chunk_bytes &= ~(size_t)63;
     const size_t nchunks = (nbytes + chunk_bytes - 1) / chunk_bytes;
     const uintptr_t a = reinterpret_cast<uintptr_t>(dst);
-    const bool avx = fmt == 0 && (a & 31) == 0 && __builtin_cpu_supports("avx");
-    const bool sse = (a & 15) == 0;
+    // small outputs: waking the pool costs more than the expansion itself, and
+    // the caller reads them right away, so plain (cached) stores on this thread
+    const bool small = n_elems * (fmt == 0 ? 4 : 1) < ((size_t)4 << 20);
+    const bool avx = !small && fmt == 0 && (a & 31) == 0 && __builtin_cpu_supports("avx");
+    const bool sse = !small && (a & 15) == 0;
     std::atomic<size_t> ready_upto{0};
     std::mutex poll;
-    const int T = pool().size();
+    const int T = small ? 1 : pool().size();
     auto work = [&](int j) {
         for (size_t c = 0; c < nchunks; c++) {
             while (ready_upto.load(std::memory_order_acquire) <= c) {
@@ -193,7 +196,8 @@ void expand_bits(const uint8_t *bits, void *dst, int fmt, size_t n_elems, size_t
         }
         _mm_sfence();
     };
-    pool().run(work);
+    if (small) work(0);
+    else pool().run(work);
 }
 
 }  // namespace lg_host
