@@ -186,6 +186,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-u8", action="store_true", help="skip the opt-in uint8-observation side run")
+    ap.add_argument("--no-policy", action="store_true", help="skip the policy-rollout side run")
+    ap.add_argument("--policy-envs", type=int, default=65536)
+    ap.add_argument("--policy-steps", type=int, default=8)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -347,6 +350,50 @@ def main():
         if not args.no_e2e:
             u8["e2e"] = e2e_run("uint8", True)
 
+    # Side measurement (does not change the headline): the
+    # policy consumer in the loop -- ppo.collect_rollout on device (ConvPolicy
+    # forward, multinomial sampling, env step, rollout buffer) with (a) the
+    # reference's float32 observations + torch conv trunk, (b) the same with
+    # bf16 autocast, (c) packed observation bits + lg_conv1_bits first layer +
+    # bf16 rest. Fewer envs than the headline (the conv trunk dominates).
+    pol = None
+    if not args.no_policy and not cfg.controllable and cfg.representation != "wide":
+        from paper_2408_12525_b200.policy import PackedPolicy, collect_rollout, default_arch, init_policy
+        torch.cuda.empty_cache()
+        Bp = min(B, args.policy_envs)
+        pol = {"envs": Bp, "steps": args.policy_steps, "unit": UNIT,
+               "note": "ppo.collect_rollout on device: policy forward + sampling + env step + rollout buffer"}
+
+        def rollout_rate(fmt, make_policy):
+            e = BatchEnv(cfg, Bp, seed=0, device=dev, global_offset=offset, validate=False, obs_dtype=fmt)
+            o = e.reset()
+            shp = e.observation_shape
+            model = init_policy(default_arch(shp[1], shp[0], cfg.n_actions), seed=0).to(dev)
+            p_ = make_policy(model, shp)
+            gen = torch.Generator(device=dev).manual_seed(0)
+            _, o, _ = collect_rollout(p_, e, 2, gen, o)  # warm-up (cuDNN autotune, allocations)
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record()
+            collect_rollout(p_, e, args.policy_steps, gen, o)
+            a1.record()
+            torch.cuda.synchronize()
+            ms = a0.elapsed_time(a1)
+            del e, model, p_
+            torch.cuda.empty_cache()
+            return Bp * args.policy_steps / (ms / 1e3)
+
+        def autocast_policy(model, shp):
+            def f(x):
+                with torch.autocast("cuda", dtype=torch.bfloat16):
+                    lg, v = model(x)
+                return lg.float(), v.float()
+            return f
+
+        pol["float32_obs_torch_f32"] = rollout_rate("float32", lambda m, shp: m)
+        pol["float32_obs_torch_bf16"] = rollout_rate("float32", autocast_policy)
+        pol["bits_obs_conv1_bits_bf16"] = rollout_rate("bits", lambda m, shp: PackedPolicy(m, shp, bf16=True))
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -382,6 +429,7 @@ def main():
             "e2e": e2e,
             "gpu_launches": 2 * K,
             "obs_uint8": u8,
+            "policy_rollout": pol,
             "clocks": clocks,
             "episode_stats": [float(x) for x in stats.cpu()],
         }

@@ -43,8 +43,11 @@ enum { LG_BINARY = 0, LG_MAZE = 1, LG_DUNGEON = 2 };
 enum { LG_NARROW = 0, LG_TURTLE = 1, LG_WIDE = 2 };
 /* Observation buffers are float32 [B][C][OH][OW] as in the reference
  * (env.py:186-233); LG_OBS_U8 writes the same 0/1 planes as uint8 (4x fewer
- * bytes for GPU-side consumers; configs without control planes only). */
-enum { LG_OBS_F32 = 0, LG_OBS_U8 = 1 };
+ * bytes for GPU-side consumers; configs without control planes only);
+ * LG_OBS_BITS writes them as one packed stream of ceil(B*C*OH*OW/32) uint32
+ * words, element t = bit t%32 of word t/32 (32x fewer bytes; the input of
+ * lg_conv1_bits and of the host expansion in lg_step_host). */
+enum { LG_OBS_F32 = 0, LG_OBS_U8 = 1, LG_OBS_BITS = 2 };
 
 /* EnvConfig (env.py:42-124) flattened; built by the Python mirror. */
 typedef struct {
@@ -169,6 +172,15 @@ int lg_random_actions(lg_env *env, int64_t *actions_dev, uint64_t seed, void *st
 int lg_metrics(int domain, int max_h, int max_w, int64_t n, const uint8_t *tiles_dev,
                const uint8_t *active_dev, uint64_t *rng_dev, int64_t *values_dev,
                uint8_t *unreach_dev, void *stream);
+
+/* Policy consumer: the first layer of the reference's
+ * ConvPolicy trunk (nets.py:150-183: Conv2d(C, K, 3) valid + ReLU) computed
+ * straight from packed observation bits (LG_OBS_BITS layout, n_envs envs of
+ * C x OH x OW elements). weight f32 [K][C][3][3], bias f32 [K] (device);
+ * out [n_envs][K][OH-2][OW-2], float32 (out_bf16 = 0) or bfloat16 (1).
+ * K <= 64 and a multiple of 4, C <= 16. Stream-ordered. */
+int lg_conv1_bits(const uint32_t *bits_dev, int64_t n_envs, int C, int OH, int OW, const float *weight_dev,
+                  const float *bias_dev, int K, void *out_dev, int out_bf16, int relu, void *stream);
 
 /* Host SeedSequence(seed).spawn(offset+n)[offset+i] -> rng [n][6] (env.py:591-594). */
 int lg_seed_streams(uint64_t seed, int64_t offset, int64_t n, uint64_t *rng_host);

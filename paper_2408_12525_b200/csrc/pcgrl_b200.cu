@@ -12,6 +12,7 @@
 #include "../../include/pcgrl_b200.h"
 #include "env_kernels.cuh"
 #include "host_expand.h"
+#include "policy_kernels.cuh"
 #include "solo_kernel.cuh"
 
 using namespace lg;
@@ -462,7 +463,7 @@ static int validate_cfg(const lg_config *c) {
         set_err("obs_size must be within 3..128 on device");
         return LG_EINVAL;
     }
-    if (c->obs_format != 0 && c->obs_format != 1) {
+    if (c->obs_format < 0 || c->obs_format > 2) {
         set_err("unknown observation format %d", c->obs_format);
         return LG_EINVAL;
     }
@@ -535,8 +536,9 @@ extern "C" int lg_create(const lg_config *cfg, int64_t n_envs, int64_t global_of
         p.w[i] = cfg->weights[i];
     }
     p.obs_u8 = cfg->obs_format == 1;
-    if (p.obs_u8 && cfg->n_ctrl > 0) {
-        set_err("uint8 observations need a config without controllable metrics");
+    p.obs_bits = cfg->obs_format == 2;
+    if ((p.obs_u8 || p.obs_bits) && cfg->n_ctrl > 0) {
+        set_err("uint8/bits observations need a config without controllable metrics");
         delete e;
         return LG_EINVAL;
     }
@@ -704,7 +706,8 @@ extern "C" int lg_describe(const lg_env *e, lg_desc *out) {
     out->obs_h = e->OH;
     out->obs_w = e->OW;
     out->team = e->team;
-    out->obs_bytes_per_env = (int64_t)e->C * e->OH * e->OW * (e->base.obs_u8 ? 1 : 4);
+    // bits: the batch is one stream of ceil(B*C*OH*OW/32) u32 words (no per-env size)
+    out->obs_bytes_per_env = e->base.obs_bits ? 0 : (int64_t)e->C * e->OH * e->OW * (e->base.obs_u8 ? 1 : 4);
     out->state_bytes_per_env =
         (int64_t)(e->rows_per_env * e->row_bytes + sizeof(Hot) + 24 * 4 + 32 + 16 + 16 + 8 + 8);
     return LG_OK;
@@ -716,6 +719,23 @@ static int check_obs_ptr(const void *obs) {
         return LG_EINVAL;
     }
     return LG_OK;
+}
+
+// Packed transfer is used when every observation element is a 0/1 plane
+// element (no control planes); LG_HOST_EXPAND=0 forces the float32 copy.
+static bool packed_ok(const lg_env *e) {
+    if (e->cfg.n_ctrl > 0) return false;
+    const char *v = getenv("LG_HOST_EXPAND");
+    return !(v && v[0] == '0');
+}
+
+// Some stream words are shared by two blocks (or lane teams): they are
+// merged with atomicOr into a zeroed stream. Warp-mode solo launches own
+// whole words (32 envs x PE bits), so no zeroing is needed there.
+static bool packed_needs_zero(const lg_env *e) {
+    const uint64_t PE = e->base.PE;
+    if (e->geo != 1) return PE % 32 != 0;
+    return ((uint64_t)e->E * PE) % 32 != 0;
 }
 
 static int run_mode(lg_env *e, int mode, const long long *actions, void *obs, double *reward,
@@ -746,7 +766,11 @@ static int run_mode(lg_env *e, int mode, const long long *actions, void *obs, do
     p.stats = stats;
     p.reset_mask = mask;
     p.no_auto_reset = (flags & LG_STEP_NO_AUTO_RESET) ? 1 : 0;
-    p.obs_bits = obs_bits ? 1 : 0;
+    if (obs_bits) p.obs_bits = 1;
+    if (p.obs_bits && obs && packed_needs_zero(e)) {
+        const size_t words = ((size_t)e->B * p.PE + 31) / 32;
+        CU(cudaMemsetAsync(obs, 0, words * 4, (cudaStream_t)stream));
+    }
     return launch_env(e, p, mode, (cudaStream_t)stream);
 }
 
@@ -780,23 +804,6 @@ extern "C" int lg_step_flags(lg_env *e, const int64_t *actions, void *obs, doubl
                     stream, flags);
 }
 
-// Packed transfer is used when every observation element is a 0/1 plane
-// element (no control planes); LG_HOST_EXPAND=0 forces the float32 copy.
-static bool packed_ok(const lg_env *e) {
-    if (e->cfg.n_ctrl > 0) return false;
-    const char *v = getenv("LG_HOST_EXPAND");
-    return !(v && v[0] == '0');
-}
-
-// Some stream words are shared by two blocks (or lane teams): they are
-// merged with atomicOr into a zeroed stream. Warp-mode solo launches own
-// whole words (32 envs x PE bits), so no zeroing is needed there.
-static bool packed_needs_zero(const lg_env *e) {
-    const uint64_t PE = e->base.PE;
-    if (e->geo != 1) return PE % 32 != 0;
-    return ((uint64_t)e->E * PE) % 32 != 0;
-}
-
 struct ChunkPoll {
     lg_env *e;
     bool failed;
@@ -820,7 +827,8 @@ extern "C" int lg_step_host(lg_env *e, const int64_t *actions_host, void *obs_ho
     size_t B = (size_t)e->B;
     const size_t n_elems = B * (size_t)e->C * e->OH * e->OW;
     size_t obs_bytes = n_elems * (e->base.obs_u8 ? 1 : sizeof(float));
-    const bool packed = obs_host && packed_ok(e);
+    const bool dev_bits = e->base.obs_bits;  // the env's own format is the packed stream
+    const bool packed = obs_host && (dev_bits || packed_ok(e));
     if (!e->d_act) {
         CU(cudaMalloc((void **)&e->d_act, B * 8));
         CU(cudaMalloc((void **)&e->d_rew, B * 8));
@@ -839,20 +847,21 @@ extern "C" int lg_step_host(lg_env *e, const int64_t *actions_host, void *obs_ho
         e->chunk_bytes = chunk;
         size_t nchunks = (e->bits_bytes + chunk - 1) / chunk;
         CU(cudaMalloc((void **)&e->d_bits, e->bits_bytes));
-        CU(cudaHostAlloc((void **)&e->h_bits, e->bits_bytes, cudaHostAllocDefault));
-        e->chunk_ev.resize(nchunks);
+        if (!dev_bits) CU(cudaHostAlloc((void **)&e->h_bits, e->bits_bytes, cudaHostAllocDefault));
+        e->chunk_ev.resize(dev_bits ? 0 : nchunks);
         for (auto &ev : e->chunk_ev) CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     }
     if (obs_host && !packed && !e->d_obs) CU(cudaMalloc((void **)&e->d_obs, obs_bytes));
     cudaStream_t s = (cudaStream_t)stream;
     CU(cudaMemcpyAsync(e->d_act, actions_host, B * 8, cudaMemcpyHostToDevice, s));
-    if (packed && packed_needs_zero(e)) CU(cudaMemsetAsync(e->d_bits, 0, e->bits_bytes, s));
     lg_info di = {e->d_term, e->d_er, (int64_t *)e->d_el, e->d_es, e->d_fl};
     void *dev_obs = obs_host ? (packed ? (void *)e->d_bits : e->d_obs) : nullptr;
     int rc = run_mode(e, MODE_STEP, (const long long *)e->d_act, dev_obs, e->d_rew, e->d_done,
                       info_host ? &di : nullptr, nullptr, nullptr, stream, 0, packed);
     if (rc) return rc;
-    if (packed) {  // the bit stream in chunks, one event each, so expansion overlaps the copy
+    if (dev_bits) {
+        if (obs_host) CU(cudaMemcpyAsync(obs_host, e->d_bits, e->bits_bytes, cudaMemcpyDeviceToHost, s));
+    } else if (packed) {  // the bit stream in chunks, one event each, so expansion overlaps the copy
         for (size_t c = 0; c < e->chunk_ev.size(); c++) {
             size_t off = c * e->chunk_bytes, len = e->bits_bytes - off;
             if (len > e->chunk_bytes) len = e->chunk_bytes;
@@ -876,7 +885,7 @@ extern "C" int lg_step_host(lg_env *e, const int64_t *actions_host, void *obs_ho
         if (info_host->final_loss)
             CU(cudaMemcpyAsync(info_host->final_loss, e->d_fl, B * 8, cudaMemcpyDeviceToHost, s));
     }
-    if (packed) {
+    if (packed && !dev_bits) {
         ChunkPoll cp{e, false};
         lg_host::expand_bits(e->h_bits, obs_host, e->base.obs_u8 ? 1 : 0, n_elems, e->chunk_bytes, chunk_ready,
                              &cp);
@@ -892,6 +901,51 @@ extern "C" int lg_step_host(lg_env *e, const int64_t *actions_host, void *obs_ho
 }
 
 extern "C" int lg_host_threads(void) { return lg_host::expand_threads(); }
+
+template <int KC, bool BF16>
+static int launch_conv1(const uint32_t *bits, long long B, int C, int OH, int OW, const float *w,
+                        const float *bias, int K, void *out, int relu, size_t smem, cudaStream_t s) {
+    auto fn = conv1_bits_kernel<KC, BF16>;
+    CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int dev = 0, sms = 0, per = 0;
+    CU(cudaGetDevice(&dev));
+    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, 256, smem));
+    long long grid = (long long)sms * (per > 0 ? per : 1);
+    if (grid > B) grid = B;
+    fn<<<(unsigned)grid, 256, smem, s>>>(bits, B, C, OH, OW, w, bias, K, out, relu);
+    CU(cudaGetLastError());
+    return LG_OK;
+}
+
+extern "C" int lg_conv1_bits(const uint32_t *bits, int64_t n_envs, int C, int OH, int OW, const float *weight,
+                             const float *bias, int K, void *out, int out_bf16, int relu, void *stream) {
+    if (!bits || !weight || !bias || !out || n_envs < 1) {
+        set_err("conv1_bits needs bits, weight, bias and output buffers and n_envs >= 1");
+        return LG_EINVAL;
+    }
+    if (C < 1 || C > 16 || OH < 3 || OW < 3 || K < 1 || K > 64) {
+        set_err("conv1_bits supports 1 <= C <= 16, 3 <= OH, OW and 1 <= K <= 64");
+        return LG_EINVAL;
+    }
+    const int KC = (K + 3) / 4, KCt = KC <= 4 ? 4 : KC <= 8 ? 8 : 16;
+    const size_t table = (size_t)((C + 3) / 4) * 9 * 16 * (4 * KCt) * sizeof(float);
+    const size_t words = ((size_t)C * OH * OW + 31) / 32 + 1;
+    const size_t smem = table + words * 4;
+    if (smem > 200 * 1024) {
+        set_err("conv1_bits: tables + one observation exceed shared memory (%zu bytes)", smem);
+        return LG_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    long long B = (long long)n_envs;
+#define LG_CONV1(KCV)                                                                                   \
+    return out_bf16 ? launch_conv1<KCV, true>(bits, B, C, OH, OW, weight, bias, K, out, relu, smem, s) \
+                    : launch_conv1<KCV, false>(bits, B, C, OH, OW, weight, bias, K, out, relu, smem, s)
+    if (KCt == 4) LG_CONV1(4);
+    if (KCt == 8) LG_CONV1(8);
+    LG_CONV1(16);
+#undef LG_CONV1
+}
 
 extern "C" int lg_export_state(lg_env *e, const lg_state *dst, void *stream) {
     if (!e || !dst) {

@@ -27,7 +27,7 @@ from .tiles import get_domain
 INFO_KEYS = ("terminal", "episode_reward", "episode_length", "episode_start_loss", "final_loss")
 
 
-OBS_FORMATS = {"float32": 0, "uint8": 1}
+OBS_FORMATS = {"float32": 0, "uint8": 1, "bits": 2}
 
 
 def make_lg_config(cfg: EnvConfig, obs_dtype: str = "float32") -> _lib.LgConfig:
@@ -80,7 +80,9 @@ class BatchEnv:
                  global_offset: int = 0, validate: bool = True, obs_dtype: str = "float32"):
         """``obs_dtype="uint8"`` (opt-in, configs without control planes) writes
         the same 0/1 observation planes as bytes: 4x less HBM traffic for
-        consumers on the GPU. The default float32 matches the reference."""
+        consumers on the GPU; ``"bits"`` writes them as one packed int32 stream
+        (32x less; see ``unpack_obs`` and ``policy.conv1_bits``). The default
+        float32 matches the reference."""
         import torch
 
         self._torch = torch
@@ -138,8 +140,12 @@ class BatchEnv:
 
     # -- buffers -------------------------------------------------------------
     def new_obs(self):
-        dt = self._torch.uint8 if self.obs_dtype == "uint8" else self._torch.float32
-        return self._torch.empty((self._n,) + self.observation_shape, dtype=dt, device=self.device)
+        t = self._torch
+        if self.obs_dtype == "bits":  # one packed stream: element i = bit i % 32 of word i // 32
+            n = self._n * int(np.prod(self.observation_shape))
+            return t.empty((n + 31) // 32, dtype=t.int32, device=self.device)
+        dt = t.uint8 if self.obs_dtype == "uint8" else t.float32
+        return t.empty((self._n,) + self.observation_shape, dtype=dt, device=self.device)
 
     def _info_buffers(self):
         t, B, dev = self._torch, self._n, self.device
@@ -410,8 +416,11 @@ class NumpyBatchEnv:
             if self.pinned:
                 return t.empty(shape, dtype=dt, pin_memory=True).numpy()
             return np.empty(shape, dtype=t.empty(0, dtype=dt).numpy().dtype)
-        odt = t.uint8 if self.env.obs_dtype == "uint8" else t.float32
-        return {"obs": mk((B,) + self.env.observation_shape, odt),
+        if self.env.obs_dtype == "bits":
+            obs = mk(((B * int(np.prod(self.env.observation_shape)) + 31) // 32,), t.int32)
+        else:
+            obs = mk((B,) + self.env.observation_shape, t.uint8 if self.env.obs_dtype == "uint8" else t.float32)
+        return {"obs": obs,
                 "actions": mk((B,), t.int64), "reward": mk((B,), t.float64),
                 "done": mk((B,), t.bool), "terminal": mk((B,), t.bool),
                 "episode_reward": mk((B,), t.float64), "episode_length": mk((B,), t.int64),
@@ -456,4 +465,15 @@ class NumpyBatchEnv:
         self.env.load_state_dict(state)
 
 
-__all__ = ["BatchEnv", "NumpyBatchEnv", "EnvConfig", "get_domain", "spawn_streams", "make_lg_config"]
+def unpack_obs(bits, n_envs: int, shape, dtype=None):
+    """Packed observation stream (obs_dtype="bits") -> [n_envs, C, OH, OW] 0/1 tensor."""
+    import torch
+    n = n_envs * int(np.prod(shape))
+    b = bits.view(torch.uint8)[: (n + 7) // 8]
+    sh = torch.arange(8, device=bits.device, dtype=torch.uint8)
+    x = ((b[:, None] >> sh) & 1).reshape(-1)[:n]
+    return x.reshape((n_envs,) + tuple(shape)).to(dtype or torch.float32)
+
+
+__all__ = ["BatchEnv", "NumpyBatchEnv", "EnvConfig", "get_domain", "spawn_streams", "make_lg_config",
+           "unpack_obs"]

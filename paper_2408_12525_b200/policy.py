@@ -1,0 +1,222 @@
+"""Policy consumer of the observation on the GPU.
+
+The reference feeds ``BatchEnv`` observations to a conv actor-critic
+(``levelgen/nets.py:150-183``) inside ``ppo.collect_rollout``
+(``levelgen/ppo.py:101-143``). This module keeps that consumer on the device:
+
+* ``ArchConfig`` / ``ConvPolicy`` mirror ``nets.ArchConfig`` / ``nets.ConvPolicy``
+  with the same module layout and parameter names (``trunk.<i>``,
+  ``policy_head``, ``value_head``), so ``state_dict``s move between the two;
+* ``conv1_bits`` runs the trunk's first layer (``Conv2d(C, K, 3)`` + ReLU)
+  straight from the packed observation stream of a ``BatchEnv(obs_dtype="bits")``
+  with the ``lg_conv1_bits`` CUDA kernel: 1 bit per input element is read
+  instead of a float32, and the float32 observation is never written;
+* ``PackedPolicy`` = that first layer + the rest of the trunk and the heads
+  in torch (cuDNN/cuBLAS), numerically the same function as
+  ``ConvPolicy(unpack(bits))`` up to float32 summation order;
+* ``collect_rollout`` mirrors ``ppo.collect_rollout`` on device tensors.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+
+@dataclass(frozen=True)
+class ArchConfig:
+    """nets.ArchConfig (nets.py:33-70): widths of the conv trunk and FC stack."""
+    obs_size: int
+    in_channels: int
+    n_actions: int
+    conv_channels: tuple = (16, 32)
+    fc_dims: tuple = (64,)
+
+    def __post_init__(self) -> None:
+        if self.obs_size < 1 or self.in_channels < 1:
+            raise ValueError("bad observation dimensions")
+        if self.n_actions < 2:
+            raise ValueError("need at least a no-op and one tile action")
+        if not self.fc_dims:
+            raise ValueError("at least one fully connected layer is required")
+        if any(c < 1 for c in self.conv_channels) or any(d < 1 for d in self.fc_dims):
+            raise ValueError("layer widths must be positive")
+        if self.conv_side() < 1:
+            raise ValueError(f"{len(self.conv_channels)} 3x3 valid convs need obs_size >= "
+                             f"{2 * len(self.conv_channels) + 1}, got {self.obs_size}")
+
+    def conv_side(self) -> int:
+        return self.obs_size - 2 * len(self.conv_channels)
+
+    def flat_dim(self) -> int:
+        c = self.conv_channels[-1] if self.conv_channels else self.in_channels
+        return c * self.conv_side() ** 2
+
+
+def default_arch(obs_size: int, in_channels: int, n_actions: int) -> ArchConfig:
+    """nets.default_arch (nets.py:73-82)."""
+    return ArchConfig(obs_size, in_channels, n_actions, (16, 32) if obs_size >= 5 else (16,), (64,))
+
+
+def count_params(arch: ArchConfig) -> int:
+    """nets.count_params (nets.py:85-98)."""
+    n, cin = 0, arch.in_channels
+    for cout in arch.conv_channels:
+        n += 9 * cin * cout + cout
+        cin = cout
+    d = arch.flat_dim()
+    for h in arch.fc_dims:
+        n += d * h + h
+        d = h
+    return n + d * arch.n_actions + arch.n_actions + d + 1
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def make_policy(arch: ArchConfig):
+    """nets.ConvPolicy (nets.py:150-183): conv trunk (3x3 valid + ReLU each),
+    flatten, FC stack with ReLU, linear policy and value heads. Orthogonal
+    init (gain sqrt 2; heads 0.01 and 1.0), zero biases, as nets.layer_init."""
+    torch = _torch()
+    nn = torch.nn
+
+    def init(layer, gain=float(np.sqrt(2))):
+        nn.init.orthogonal_(layer.weight, gain)
+        nn.init.constant_(layer.bias, 0.0)
+        return layer
+
+    class ConvPolicy(nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.arch = arch
+            mods, cin = [], arch.in_channels
+            for cout in arch.conv_channels:
+                mods += [init(nn.Conv2d(cin, cout, kernel_size=3)), nn.ReLU()]
+                cin = cout
+            mods.append(nn.Flatten())
+            d = arch.flat_dim()
+            for h in arch.fc_dims:
+                mods += [init(nn.Linear(d, h)), nn.ReLU()]
+                d = h
+            self.trunk = nn.Sequential(*mods)
+            self.policy_head = init(nn.Linear(d, arch.n_actions), 0.01)
+            self.value_head = init(nn.Linear(d, 1), 1.0)
+
+        def forward(self, obs):
+            want = (arch.in_channels, arch.obs_size, arch.obs_size)
+            if obs.ndim != 4 or tuple(obs.shape[1:]) != want:
+                raise ValueError(f"expected [batch, {want[0]}, {want[1]}, {want[2]}] observations, "
+                                 f"got {tuple(obs.shape)}")
+            h = self.trunk(obs)
+            return self.policy_head(h), self.value_head(h).squeeze(-1)
+
+    return ConvPolicy()
+
+
+def init_policy(arch: ArchConfig, seed: int):
+    """nets.init_policy (nets.py:186-189): same seed, same weights."""
+    _torch().manual_seed(seed)
+    return make_policy(arch)
+
+
+def conv1_bits(bits, n_envs: int, obs_shape, weight, bias, *, out_dtype=None, relu: bool = True, out=None):
+    """relu(conv2d(obs, weight, bias)) (3x3, valid) from the packed stream of a
+    ``BatchEnv(obs_dtype="bits")``; obs_shape = (C, OH, OW). Output
+    [n_envs, K, OH-2, OW-2] in float32 (default) or bfloat16."""
+    torch = _torch()
+    C, OH, OW = (int(x) for x in obs_shape)
+    K = int(weight.shape[0])
+    if tuple(weight.shape) != (K, C, 3, 3):
+        raise ValueError(f"weight must be [K, {C}, 3, 3], got {tuple(weight.shape)}")
+    out_dtype = out_dtype or torch.float32
+    if out_dtype not in (torch.float32, torch.bfloat16):
+        raise ValueError("out_dtype must be float32 or bfloat16")
+    w = weight.detach().to(torch.float32).contiguous()
+    b = bias.detach().to(torch.float32).contiguous()
+    if out is None:
+        out = torch.empty((n_envs, K, OH - 2, OW - 2), dtype=out_dtype, device=bits.device)
+    stream = ctypes.c_void_p(torch.cuda.current_stream(bits.device).cuda_stream)
+    p = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    _lib.check(_lib.load().lg_conv1_bits(p(bits), int(n_envs), C, OH, OW, p(w), p(b), K, p(out),
+                                         int(out_dtype == torch.bfloat16), int(relu), stream))
+    return out
+
+
+class PackedPolicy:
+    """A ConvPolicy evaluated from packed observation bits: the first conv +
+    ReLU by ``lg_conv1_bits``, the rest of the trunk and both heads by the
+    model's own torch modules (optionally under bf16 autocast)."""
+
+    def __init__(self, model, obs_shape, *, bf16: bool = False):
+        if not model.arch.conv_channels:
+            raise ValueError("the packed path needs at least one conv layer")
+        self.model = model
+        self.obs_shape = tuple(obs_shape)
+        self.bf16 = bf16
+        self.conv1 = model.trunk[0]
+        self.rest = model.trunk[2:]  # after Conv2d + ReLU
+
+    def __call__(self, bits, n_envs: int):
+        torch = _torch()
+        h = conv1_bits(bits, n_envs, self.obs_shape, self.conv1.weight, self.conv1.bias,
+                       out_dtype=torch.bfloat16 if self.bf16 else torch.float32)
+        with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.bf16):
+            h = self.rest(h)
+            return self.model.policy_head(h).float(), self.model.value_head(h).squeeze(-1).float()
+
+
+@dataclass
+class RolloutBatch:
+    """ppo.RolloutBatch (ppo.py:91-98), device tensors; obs in the env's format."""
+    obs: object       # [T, *obs] (float32 [T,B,C,O,O], or packed int32 [T, words])
+    actions: object   # [T, B] int64
+    logprobs: object  # [T, B] float32
+    rewards: object   # [T, B] float64
+    values: object    # [T, B] float32
+    dones: object     # [T, B] bool
+
+
+def collect_rollout(policy, env, length: int, sampler, obs):
+    """ppo.collect_rollout (ppo.py:101-143) on the GPU: ``length`` lockstep
+    steps sampling actions from ``policy`` (a ConvPolicy taking float32
+    observations, or a PackedPolicy for an ``obs_dtype="bits"`` env). Returns
+    the batch, the observation after the last step and the rewards of the
+    episodes that finished (one host sync at the end, not one per step)."""
+    torch = _torch()
+    B = env.n_envs
+    packed = isinstance(policy, PackedPolicy)
+    dev = env.device
+    out_obs = torch.empty((length,) + tuple(obs.shape), dtype=obs.dtype, device=dev)
+    out_actions = torch.empty((length, B), dtype=torch.int64, device=dev)
+    out_logprobs = torch.empty((length, B), dtype=torch.float32, device=dev)
+    out_rewards = torch.empty((length, B), dtype=torch.float64, device=dev)
+    out_values = torch.empty((length, B), dtype=torch.float32, device=dev)
+    out_dones = torch.empty((length, B), dtype=torch.bool, device=dev)
+    finished_sum = []
+    with torch.no_grad():
+        for t in range(length):
+            logits, value = policy(obs, B) if packed else policy(obs)
+            probs = torch.softmax(logits.float(), dim=-1)
+            actions = torch.multinomial(probs, 1, generator=sampler).squeeze(1)
+            logp = torch.log_softmax(logits.float(), dim=-1).gather(1, actions[:, None]).squeeze(1)
+            out_obs[t].copy_(obs)
+            out_actions[t] = actions
+            out_logprobs[t] = logp
+            out_values[t] = value.float()
+            obs, reward, done, info = env.step(actions)
+            out_rewards[t] = reward
+            out_dones[t] = done
+            finished_sum.append(info["episode_reward"])
+    ep = torch.stack(finished_sum)
+    finished = ep[out_dones].tolist()  # time-major, env order within a step (ppo.py:141-142)
+    return RolloutBatch(out_obs, out_actions, out_logprobs, out_rewards, out_values, out_dones), obs, finished
+
+
+__all__ = ["ArchConfig", "default_arch", "count_params", "make_policy", "init_policy", "conv1_bits",
+           "PackedPolicy", "RolloutBatch", "collect_rollout"]

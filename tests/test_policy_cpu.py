@@ -1,0 +1,48 @@
+"""Policy mirror (paper_2408_12525_b200.policy) vs the reference's nets.py,
+pinned by tests/golden/policy.npz (made from the live reference by
+tests/golden/make_policy_golden.py): same parameter names, shapes, counts and
+seeded initial weights, and the same forward pass (CPU, float32)."""
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from paper_2408_12525_b200.policy import ArchConfig, count_params, default_arch, init_policy  # noqa: E402
+
+GOLD = np.load(os.path.join(os.path.dirname(__file__), "golden", "policy.npz"))
+ARCHS = [
+    (7, 4, 3, (16, 32), (64,), 0),
+    (9, 6, 8, (16, 32), (64,), 5),
+    (4, 4, 3, (16,), (64,), 1),
+    (11, 8, 768, (8, 12), (16, 8), 2),
+]
+
+
+@pytest.mark.parametrize("i", range(len(ARCHS)))
+def test_init_and_forward_match_reference(i):
+    o, c, a, cc, fc, seed = ARCHS[i]
+    arch = ArchConfig(o, c, a, cc, fc)
+    assert count_params(arch) == int(GOLD[f"a{i}_count"])
+    model = init_policy(arch, seed)
+    sd = model.state_dict()
+    want = {k.split("/", 1)[1]: GOLD[k] for k in GOLD.files if k.startswith(f"a{i}_param/")}
+    assert sorted(sd) == sorted(want)
+    for k, v in want.items():
+        assert np.array_equal(sd[k].numpy(), v), k
+    with torch.no_grad():
+        logits, value = model(torch.from_numpy(GOLD[f"a{i}_obs"]))
+    np.testing.assert_allclose(logits.numpy(), GOLD[f"a{i}_logits"], rtol=1e-6, atol=1e-6)
+    np.testing.assert_allclose(value.numpy(), GOLD[f"a{i}_value"], rtol=1e-6, atol=1e-6)
+
+
+def test_arch_validation_and_defaults():
+    assert default_arch(3, 4, 3).conv_channels == (16,)
+    assert default_arch(31, 4, 3).conv_channels == (16, 32)
+    with pytest.raises(ValueError):
+        ArchConfig(3, 4, 3, (16, 32), (64,))
+    with pytest.raises(ValueError):
+        ArchConfig(7, 4, 1)
+    with pytest.raises(ValueError):
+        init_policy(ArchConfig(7, 4, 3), 0)(torch.zeros(2, 4, 5, 5))
