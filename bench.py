@@ -390,6 +390,43 @@ def main():
                 return lg.float(), v.float()
             return f
 
+        # the first conv alone: lg_conv1_bits from packed bits vs cuDNN on float32 obs
+        from paper_2408_12525_b200.policy import conv1_bits
+        e = BatchEnv(cfg, Bp, seed=0, device=dev, global_offset=offset, validate=False, obs_dtype="bits")
+        bits_o = e.reset()
+        shp = e.observation_shape
+        m0 = init_policy(default_arch(shp[1], shp[0], cfg.n_actions), seed=0).to(dev)
+        conv = m0.trunk[0]
+        from paper_2408_12525_b200.env import unpack_obs
+        obs_f = unpack_obs(bits_o, Bp, shp)
+
+        def time_ms(fn, reps=10):
+            fn()
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record()
+            for _ in range(reps):
+                fn()
+            a1.record()
+            torch.cuda.synchronize()
+            return a0.elapsed_time(a1) / reps
+
+        K_, P_ = conv.weight.shape[0], (shp[1] - 2) * (shp[2] - 2)
+        n_in = Bp * shp[0] * shp[1] * shp[2]
+        with torch.no_grad():
+            t_f32 = time_ms(lambda: conv1_bits(bits_o, Bp, shp, conv.weight, conv.bias))
+            t_bf = time_ms(lambda: conv1_bits(bits_o, Bp, shp, conv.weight, conv.bias, out_dtype=torch.bfloat16))
+            t_cud = time_ms(lambda: torch.relu(conv(obs_f)))
+        by_f32 = Bp * K_ * P_ * 4 + n_in / 8
+        by_bf = Bp * K_ * P_ * 2 + n_in / 8
+        pol["conv1"] = {
+            "lg_conv1_bits_f32_ms": t_f32, "lg_conv1_bits_f32_gbs": by_f32 / t_f32 / 1e6,
+            "lg_conv1_bits_bf16_ms": t_bf, "lg_conv1_bits_bf16_gbs": by_bf / t_bf / 1e6,
+            "cudnn_f32_obs_ms": t_cud, "frac_of_peak_bf16": by_bf / t_bf / 1e6 / peak,
+            "note": "bytes = output + packed input (1 bit/element); cuDNN reads float32 obs"}
+        del e, m0, conv, obs_f, bits_o
+        torch.cuda.empty_cache()
+
         pol["float32_obs_torch_f32"] = rollout_rate("float32", lambda m, shp: m)
         pol["float32_obs_torch_bf16"] = rollout_rate("float32", autocast_policy)
         pol["bits_obs_conv1_bits_bf16"] = rollout_rate("bits", lambda m, shp: PackedPolicy(m, shp, bf16=True))

@@ -902,18 +902,26 @@ extern "C" int lg_step_host(lg_env *e, const int64_t *actions_host, void *obs_ho
 
 extern "C" int lg_host_threads(void) { return lg_host::expand_threads(); }
 
+#ifndef LG_CONV1_EB
+#define LG_CONV1_EB 4  // envs per block iteration in conv1_bits_kernel
+#endif
 template <int KC, bool BF16>
 static int launch_conv1(const uint32_t *bits, long long B, int C, int OH, int OW, const float *w,
                         const float *bias, int K, void *out, int relu, size_t smem, cudaStream_t s) {
-    auto fn = conv1_bits_kernel<KC, BF16>;
+    Conv1Div dv;
+    fastdiv_init(dv.oo, (uint32_t)(OH * OW));
+    fastdiv_init(dv.pw, (uint32_t)(OW - 2));
+    fastdiv_init(dv.np, (uint32_t)((OH - 2) * (OW - 2)));
+    fastdiv_init(dv.g, (uint32_t)((C + 3) / 4));
+    auto fn = conv1_bits_kernel<KC, BF16, LG_CONV1_EB>;
     CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int dev = 0, sms = 0, per = 0;
     CU(cudaGetDevice(&dev));
     CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, 256, smem));
     long long grid = (long long)sms * (per > 0 ? per : 1);
-    if (grid > B) grid = B;
-    fn<<<(unsigned)grid, 256, smem, s>>>(bits, B, C, OH, OW, w, bias, K, out, relu);
+    if (grid * LG_CONV1_EB > B) grid = (B + LG_CONV1_EB - 1) / LG_CONV1_EB;
+    fn<<<(unsigned)grid, 256, smem, s>>>(bits, B, C, OH, OW, w, bias, K, out, relu, dv);
     CU(cudaGetLastError());
     return LG_OK;
 }
@@ -929,9 +937,11 @@ extern "C" int lg_conv1_bits(const uint32_t *bits, int64_t n_envs, int C, int OH
         return LG_EINVAL;
     }
     const int KC = (K + 3) / 4, KCt = KC <= 4 ? 4 : KC <= 8 ? 8 : 16;
-    const size_t table = (size_t)((C + 3) / 4) * 9 * 16 * (4 * KCt) * sizeof(float);
-    const size_t words = ((size_t)C * OH * OW + 31) / 32 + 1;
-    const size_t smem = table + words * 4;
+    const size_t G = (size_t)((C + 3) / 4);
+    const size_t table = G * 10 * 16 * (4 * KCt + 4) * sizeof(float);  // 9 tap tables + their sum
+    const size_t masks = (LG_CONV1_EB * G * OH * OW + 15) & ~(size_t)15;
+    const size_t words = ((size_t)LG_CONV1_EB * C * OH * OW + 31) / 32 + 1;
+    const size_t smem = table + masks + words * 4;
     if (smem > 200 * 1024) {
         set_err("conv1_bits: tables + one observation exceed shared memory (%zu bytes)", smem);
         return LG_EINVAL;

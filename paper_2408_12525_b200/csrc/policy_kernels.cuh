@@ -14,18 +14,31 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include "env_kernels.cuh"
+
 namespace lg {
 
-template <int KC, bool BF16>
+struct Conv1Div {  // runtime divisors of the index math (mul-hi + shift)
+    FastDiv oo, pw, np, g;
+};
+
+// Shared memory: T [G][9][16][RS] tap tables (bias folded into tap 0 of
+// group 0), S [G][16][RS] = sum over the 9 taps (a 3x3 neighbourhood whose
+// cells all carry the same channel mask -- the border around the map in an
+// egocentric window -- is one lookup instead of nine), the env's channel
+// mask per cell and group (bytes), and the env's bits.
+template <int KC, bool BF16, int EB>
 __global__ void __launch_bounds__(256) conv1_bits_kernel(const uint32_t *__restrict__ bits, long long B, int C,
                                                          int OH, int OW, const float *__restrict__ w,
                                                          const float *__restrict__ bias, int K, void *out,
-                                                         int relu) {
+                                                         int relu, const Conv1Div dv) {
     extern __shared__ __align__(16) float csm[];
     constexpr int KP = 4 * KC;  // padded output channels per table row
+    constexpr int RS = KP + 4;  // row stride (floats): rows land 20 banks apart, not 16
     const int G = (C + 3) >> 2;
-    float *T = csm;  // [G][9][16][KP]
+    float *T = csm;  // [G][9][16][RS]
     const int rows = G * 9 * 16;
+    float *S = T + (size_t)rows * RS;  // [G][16][RS]
     for (int i = threadIdx.x; i < rows; i += blockDim.x) {
         const int m = i & 15, tap = (i >> 4) % 9, g = i / (9 * 16);
         for (int k = 0; k < KP; k++) {
@@ -37,17 +50,27 @@ __global__ void __launch_bounds__(256) conv1_bits_kernel(const uint32_t *__restr
                     if (c < C && ((m >> j) & 1)) s += w[((size_t)k * C + c) * 9 + tap];
                 }
             }
-            T[(size_t)i * KP + k] = s;
+            T[(size_t)i * RS + k] = s;
         }
     }
+    __syncthreads();
+    for (int i = threadIdx.x; i < G * 16 * KP; i += blockDim.x) {
+        const int k = i % KP, m = (i / KP) & 15, g = i / (16 * KP);
+        float s = 0.0f;
+        for (int tap = 0; tap < 9; tap++) s += T[((size_t)(g * 9 + tap) * 16 + m) * RS + k];
+        S[((size_t)g * 16 + m) * RS + k] = s;
+    }
     const int OO = OH * OW, PE = C * OO;
-    const int NW = (PE + 31) / 32 + 1;
-    uint32_t *eb = reinterpret_cast<uint32_t *>(T + (size_t)rows * KP);
+    // EB consecutive envs per block iteration (fewer barriers, fuller rounds)
+    const int NW = (EB * PE + 31) / 32 + 1;
+    uint8_t *mk = reinterpret_cast<uint8_t *>(S + (size_t)G * 16 * RS);  // [EB][G][OO]
+    uint32_t *eb = reinterpret_cast<uint32_t *>(mk + (((size_t)EB * G * OO + 15) & ~(size_t)15));
     const int PH = OH - 2, PW = OW - 2, NP = PH * PW;
     const unsigned long long total_words = ((unsigned long long)B * PE + 31) / 32;
-    for (long long env = blockIdx.x; env < B; env += gridDim.x) {
-        __syncthreads();  // tables built / previous env's bits consumed
-        const unsigned long long g0 = (unsigned long long)env * PE, w0 = g0 >> 5;
+    for (long long env0 = (long long)blockIdx.x * EB; env0 < B; env0 += (long long)gridDim.x * EB) {
+        const int ne = B - env0 < EB ? (int)(B - env0) : EB;
+        __syncthreads();  // tables built / previous envs consumed
+        const unsigned long long g0 = (unsigned long long)env0 * PE, w0 = g0 >> 5;
         const uint32_t sh = (uint32_t)(g0 & 31);
         for (int i = threadIdx.x; i < NW; i += blockDim.x) {
             const uint32_t lo = w0 + i < total_words ? bits[w0 + i] : 0u;
@@ -55,25 +78,38 @@ __global__ void __launch_bounds__(256) conv1_bits_kernel(const uint32_t *__restr
             eb[i] = __funnelshift_r(lo, hi, sh);
         }
         __syncthreads();
-        for (int px = threadIdx.x; px < NP; px += blockDim.x) {
-            const int y = px / PW, x = px - y * PW;
+        for (int i = threadIdx.x; i < ne * G * OO; i += blockDim.x) {  // channel mask per env, group, cell
+            const int eg = (int)fdiv(dv.oo, (uint32_t)i), cell = i - eg * OO, e = (int)fdiv(dv.g, (uint32_t)eg),
+                      g = eg - e * G;
+            int m = 0;
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const int c = g * 4 + j;
+                if (c < C) {
+                    const int b = e * PE + c * OO + cell;
+                    m |= (int)((eb[b >> 5] >> (b & 31)) & 1u) << j;
+                }
+            }
+            mk[i] = (uint8_t)m;
+        }
+        __syncthreads();
+        for (int it = threadIdx.x; it < ne * NP; it += blockDim.x) {
+            const int e = (int)fdiv(dv.np, (uint32_t)it), px = it - e * NP;
+            const long long env = env0 + e;
+            const int y = (int)fdiv(dv.pw, (uint32_t)px), x = px - y * PW;
             float4 acc[KC];
 #pragma unroll
             for (int q = 0; q < KC; q++) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int g = 0; g < G; g++) {
+                const uint8_t *mg = mk + (e * G + g) * OO + y * OW + x;
+                int ms[9];
 #pragma unroll
-            for (int tap = 0; tap < 9; tap++) {
-                const int cell = (y + tap / 3) * OW + x + tap % 3;
-                for (int g = 0; g < G; g++) {
-                    int m = 0;
+                for (int tap = 0; tap < 9; tap++) ms[tap] = mg[(tap / 3) * OW + tap % 3];
+                bool uni = true;
 #pragma unroll
-                    for (int j = 0; j < 4; j++) {
-                        const int c = g * 4 + j;
-                        if (c < C) {
-                            const int b = c * OO + cell;
-                            m |= (int)((eb[b >> 5] >> (b & 31)) & 1u) << j;
-                        }
-                    }
-                    const float4 *row = reinterpret_cast<const float4 *>(T + ((size_t)(g * 9 + tap) * 16 + m) * KP);
+                for (int tap = 1; tap < 9; tap++) uni &= ms[tap] == ms[0];
+                if (uni) {
+                    const float4 *row = reinterpret_cast<const float4 *>(S + ((size_t)g * 16 + ms[0]) * RS);
 #pragma unroll
                     for (int q = 0; q < KC; q++) {
                         const float4 v = row[q];
@@ -82,8 +118,26 @@ __global__ void __launch_bounds__(256) conv1_bits_kernel(const uint32_t *__restr
                         acc[q].z += v.z;
                         acc[q].w += v.w;
                     }
+                } else {
+#pragma unroll
+                    for (int tap = 0; tap < 9; tap++) {
+                        const float4 *row =
+                            reinterpret_cast<const float4 *>(T + ((size_t)(g * 9 + tap) * 16 + ms[tap]) * RS);
+#pragma unroll
+                        for (int q = 0; q < KC; q++) {
+                            const float4 v = row[q];
+                            acc[q].x += v.x;
+                            acc[q].y += v.y;
+                            acc[q].z += v.z;
+                            acc[q].w += v.w;
+                        }
+                    }
                 }
             }
+            // [env][k][px]: one base per pixel, channel planes NP apart
+            const size_t base = (size_t)env * K * NP + px;
+            __nv_bfloat16 *ob = reinterpret_cast<__nv_bfloat16 *>(out) + base;
+            float *of = reinterpret_cast<float *>(out) + base;
 #pragma unroll
             for (int q = 0; q < KC; q++) {
                 const float a4[4] = {acc[q].x, acc[q].y, acc[q].z, acc[q].w};
@@ -93,9 +147,8 @@ __global__ void __launch_bounds__(256) conv1_bits_kernel(const uint32_t *__restr
                     if (k < K) {
                         float v = a4[j];
                         if (relu) v = v > 0.f ? v : 0.f;
-                        const size_t o = ((size_t)env * K + k) * NP + px;
-                        if (BF16) reinterpret_cast<__nv_bfloat16 *>(out)[o] = __float2bfloat16_rn(v);
-                        else reinterpret_cast<float *>(out)[o] = v;
+                        if (BF16) ob[k * NP] = __float2bfloat16_rn(v);
+                        else of[k * NP] = v;
                     }
                 }
             }
