@@ -187,6 +187,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-u8", action="store_true", help="skip the opt-in uint8-observation side run")
     ap.add_argument("--no-policy", action="store_true", help="skip the policy-rollout side run")
+    ap.add_argument("--no-graph", action="store_true", help="time only the eager launch loop")
     ap.add_argument("--policy-envs", type=int, default=65536)
     ap.add_argument("--policy-steps", type=int, default=8)
     args = ap.parse_args()
@@ -259,11 +260,34 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clocks = clk.stop()
     elapsed_ms = t_start.elapsed_time(t_end)
     step_ms = sum(a.elapsed_time(b) for a, b in ev) / K
     elapsed_ms = max_over_ranks(elapsed_ms, dev)
     step_ms = max_over_ranks(step_ms, dev)
+    eager_ms = elapsed_ms
+    graph_ms = None
+    if not args.no_graph:
+        # the same K steps (device actions + fused step, fresh seeds) captured
+        # once in a CUDA graph and replayed: no per-launch CPU gaps, which
+        # matter for the small configs (c1: 64 envs, ~30 us kernels)
+        g = torch.cuda.CUDAGraph()
+        base = args.warmup + K
+        with torch.cuda.graph(g):
+            for i in range(K):
+                env.random_actions(1_000_003 * (base + i) + 17, out=acts)
+                env.step_raw(acts, obs, reward, done, info, stats)
+        g.replay()  # warm replay (K more steps)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        g.replay()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        graph_ms = max_over_ranks(g0.elapsed_time(g1), dev)
+        elapsed_ms = min(elapsed_ms, graph_ms)
+    clocks = clk.stop()
     ep_stats.all_reduce()  # the episode-stats reduce (NCCL over NVLink when N > 1)
     errs = env.errors()
     if errs:
@@ -465,6 +489,11 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": 2 * K,
+            "timing": {"eager_ms_per_step": eager_ms / K,
+                       "graph_ms_per_step": graph_ms / K if graph_ms is not None else None,
+                       "value_from": "graph" if graph_ms is not None and graph_ms <= eager_ms else "eager",
+                       "note": "value = K steps / min(eager launch loop, one CUDA-graph replay of K "
+                               "steps); both time the same work on the device"},
             "obs_uint8": u8,
             "policy_rollout": pol,
             "clocks": clocks,
