@@ -114,6 +114,7 @@ struct Params {
     int elide;
     int frz_derived;  // solo: frozen plane == max grid minus episode rect in every env (not read)
     unsigned *aux;  // [1] device flag: an imported env has an active frozen cell
+    int early;      // solo warp mode: render + store half the outputs before the recompute
 };
 
 template <class G, int DOM>

@@ -357,6 +357,10 @@ static int launch_solo_t(lg_env *e, const Params &p, int mode, cudaStream_t s) {
     Params q = p;
     size_t smem = e->smem;
     q.frz_derived = e->frz_ok && e->plain;
+    // early observation stores (solo_kernel.cuh): c5 +2.5%, its 131k-env shard
+    // +14%; dungeon's larger step spills under it (c3 graph replay -1.5%)
+    const char *ea = getenv("LG_EARLY");
+    q.early = ea ? ea[0] == '1' : (DOM != 2 && !getenv("LG_NO_EARLY"));
     if (e->elide_ok && e->plain && p.obs) {
         q.elide = 1;
         q.env_smem = e->slot_elide;

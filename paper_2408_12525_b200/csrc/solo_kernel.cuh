@@ -562,29 +562,33 @@ __device__ void solo_write(const Params &p, const uint32_t *wimg, long long env0
 // 32-byte aligned output: U independent 256-bit stores per lane per round.
 // A group of 8 elements that straddles an env boundary takes its high bits
 // from the first word of the next env's image.
+// [qa, qb): the range of 8-element groups to write (qa a multiple of nthr * U);
+// the ragged end (groups past the last full round, elements past the last
+// group) is written by the call whose range ends at the last group.
 template <int U>
 __device__ void solo_write_noctrl(const Params &p, const uint32_t *wimg, long long env0, int nenv, int lane,
-                                  int nthr) {
+                                  int nthr, uint32_t qa = 0, uint32_t qb = 0xFFFFFFFFu) {
     float *out = p.obs + (size_t)env0 * p.PE;
     const uint32_t PE = p.PE, stride = (uint32_t)p.env_smem;
     const uint32_t total = (uint32_t)nenv * PE;
     const uint32_t nv = total / 8;
+    if (qb > nv) qb = nv;
     const uint32_t STEP = (uint32_t)nthr * U * 8;  // elements per round per lane
     uint32_t el[U], le[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
-        uint32_t e = (uint32_t)(lane + nthr * u) * 8;
+        uint32_t e = (qa + (uint32_t)(lane + nthr * u)) * 8;
         el[u] = fdiv(p.divPE, e);
         le[u] = e - el[u] * PE;
     }
     const bool small_env = PE <= STEP;  // more than one wrap per round: use the divider
     // elided frozen plane: elements [PF, PE) read the border plane [PF-OO, PF)
     const uint32_t OO = p.OO, PF = p.elide ? PE - OO : PE;
-    uint32_t q0 = lane;
+    uint32_t q0 = qa + lane;
 #ifdef LG_EXP_UNROLL
 #pragma unroll LG_EXP_UNROLL
 #endif
-    for (; q0 + (uint32_t)nthr * (U - 1) < nv; q0 += (uint32_t)nthr * U) {
+    for (; q0 + (uint32_t)nthr * (U - 1) < qb; q0 += (uint32_t)nthr * U) {
         uint32_t x[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
@@ -630,6 +634,7 @@ __device__ void solo_write_noctrl(const Params &p, const uint32_t *wimg, long lo
             }
         }
     }
+    if (qb < nv) return;
     for (uint32_t t = q0 * 8; t < total; t += (uint32_t)nthr * 8) {  // ragged end, element by element
         for (uint32_t j = 0; j < 8 && t + j < total; j++) {
             uint32_t e2 = fdiv(p.divPE, t + j);
@@ -700,13 +705,14 @@ __device__ void solo_write_stream_u8(const Params &p, const uint32_t *st, long l
 // a lane-constant shift, VEC selects and one store. No env bookkeeping.
 template <int VEC, int U>
 __device__ void solo_write_stream(const Params &p, const uint32_t *st, long long env0, int nenv, int lane,
-                                  int nthr) {
+                                  int nthr, uint32_t qa = 0, uint32_t qb = 0xFFFFFFFFu) {
     float *out = p.obs + (size_t)env0 * p.PE;
     const uint32_t total = (uint32_t)nenv * p.PE;
     const uint32_t nv = total / VEC;
-    const uint32_t sh = ((uint32_t)lane * VEC) & 31;  // nthr * VEC is a multiple of 32
-    uint32_t q0 = lane;
-    for (; q0 + (uint32_t)nthr * (U - 1) < nv; q0 += (uint32_t)nthr * U) {
+    if (qb > nv) qb = nv;
+    const uint32_t sh = ((uint32_t)lane * VEC) & 31;  // nthr * VEC is a multiple of 32 (and qa * VEC)
+    uint32_t q0 = qa + lane;
+    for (; q0 + (uint32_t)nthr * (U - 1) < qb; q0 += (uint32_t)nthr * U) {
         uint32_t x[U];
 #pragma unroll
         for (int u = 0; u < U; u++) x[u] = st[sidx(((q0 + (uint32_t)nthr * u) * VEC) >> 5)] >> sh;
@@ -720,6 +726,7 @@ __device__ void solo_write_stream(const Params &p, const uint32_t *st, long long
             else __stcs(reinterpret_cast<float4 *>(out) + q, make_float4(f[0], f[1], f[2], f[3]));
         }
     }
+    if (qb < nv) return;
     for (uint32_t q = q0; q < nv; q += nthr) {
         uint32_t x = st[sidx((q * VEC) >> 5)] >> sh;
         float f[8];
@@ -815,19 +822,31 @@ __device__ void solo_write_stream_bits(const Params &p, const uint32_t *st, long
     }
 }
 
-// One env, one thread: step / reset / observe, then render its image into `slot`.
+// One env, one thread: step / reset / observe (solo_begin + solo_finish), then
+// render its image into `slot`. A step's observation depends only on the tiles
+// after the action and the next scan position -- not on the metrics -- unless
+// the episode ends (auto-reset) or control planes are rendered, so the warp
+// can render and start storing before it recomputes (env_solo_body).
 template <int DOM>
-__device__ __forceinline__ void solo_env(const Params &p, int mode, long long env, uint32_t *slot, uint32_t *img,
-                                         bool stream, uint32_t bit0, bool last) {
-    constexpr int N = Dom<DOM>::N;
+struct SoloStep {
     SoloEnv<DOM> e;
+    bool cold, rows_dirty, planes_dirty, metrics_dirty, rng_dirty, wrote, reset_now, ends;
+    double before;
+};
+
+// load; apply the action (env.py:355-372); advance the scan position and t
+// (env.py:374-381: independent of the recompute)
+template <int DOM>
+__device__ __forceinline__ void solo_begin(const Params &p, int mode, long long env, SoloStep<DOM> &st) {
+    constexpr int N = Dom<DOM>::N;
+    SoloEnv<DOM> &e = st.e;
     solo_load_hot<DOM>(p, env, e);
     // control planes render the metric values; reset/recompute/reprice use everything
-    bool cold = (mode != MODE_STEP && mode != MODE_OBSERVE) || p.n_ctrl > 0;
-    if (cold) solo_load_cold<DOM>(p, env, e, true);
-    bool rows_dirty = false, planes_dirty = false, metrics_dirty = false, rng_dirty = false;
-    bool wrote = false, reset_now = false;
-    double before = 0.0;
+    st.cold = (mode != MODE_STEP && mode != MODE_OBSERVE) || p.n_ctrl > 0;
+    if (st.cold) solo_load_cold<DOM>(p, env, e, true);
+    st.rows_dirty = st.planes_dirty = st.metrics_dirty = st.rng_dirty = false;
+    st.wrote = st.reset_now = st.ends = false;
+    st.before = 0.0;
     if (mode == MODE_STEP) {
         long long a = p.actions[env];
         bool ok = a >= 0 && a < p.n_actions;
@@ -868,59 +887,67 @@ __device__ __forceinline__ void solo_env(const Params &p, int mode, long long en
                 }
             }
             bool editable = act && !fz;
-            wrote = tile != cur && (p.rep == REP_NARROW || editable);
+            st.wrote = tile != cur && (p.rep == REP_NARROW || editable);
         }
-        if (wrote) {  // env.py:369-372
+        if (st.wrote) {  // env.py:369-372
             solo_set_tile<DOM>(e, r, c, tile);
-            planes_dirty = true;
+            st.planes_dirty = true;
             e.changes += 1;
         }
-        // this step recomputes or ends the episode (done depends only on counters)
-        bool ends = e.t + 1 >= e.max_steps || (p.budget > 0 && e.changes >= p.budget);
-        if (!cold && (wrote || ends)) {
-            solo_load_cold<DOM>(p, env, e, false);
-            cold = true;
+        if (p.rep == REP_NARROW) {  // pos_idx = (pos_idx + 1) % order_len
+            SB ed = andnot(rect_sb(e.h, e.w), e.frz);
+            int nidx = e.pos_idx + 1, nxt;
+            if (nidx >= e.order_len) {
+                nidx = 0;
+                nxt = solo_serp_first(ed, 0);
+            } else {
+                nxt = solo_serp_next(ed, e.pr, e.pc);
+            }
+            e.pos_idx = nidx;
+            e.pr = nxt >> 4;
+            e.pc = nxt & 15;
         }
-        before = e.prev_loss;
+        e.t += 1;
+        // the episode ends this step (done depends only on counters)
+        st.ends = e.t >= e.max_steps || (p.budget > 0 && e.changes >= p.budget);
     } else if (mode == MODE_RESET) {
-        reset_now = !p.reset_mask || p.reset_mask[env];
+        st.reset_now = !p.reset_mask || p.reset_mask[env];
     } else if (mode == MODE_RECOMPUTE) {
-        wrote = !p.reset_mask || p.reset_mask[env];  // recompute without a write
+        st.wrote = !p.reset_mask || p.reset_mask[env];  // recompute without a write
     } else if (mode == MODE_REPRICE) {
         if (!p.reset_mask || p.reset_mask[env]) e.prev_loss = loss_of<DOM>(p, e.val, e.unr, e.lo, e.hi);
+    }
+}
+
+// recompute (env.py:332-347), reward/done/info (env.py:373-390), auto-reset
+// (env.py:391-392), state write-back
+template <int DOM>
+__device__ __forceinline__ void solo_finish(const Params &p, int mode, long long env, SoloStep<DOM> &st, void *slot) {
+    SoloEnv<DOM> &e = st.e;
+    if (mode == MODE_STEP) {
+        if (!st.cold && (st.wrote || st.ends)) {
+            solo_load_cold<DOM>(p, env, e, false);
+            st.cold = true;
+        }
+        st.before = e.prev_loss;
     }
     // pass 0: the step's recompute + bookkeeping; pass 1: auto-reset. One
     // call site for the metric code keeps the kernel's instruction footprint small.
 #pragma unroll 1
     for (int pass = 0; pass < 2; pass++) {
         if (pass == 1) {
-            if (!reset_now) break;
+            if (!st.reset_now) break;
             solo_reset_setup<DOM>(p, e);
-            rows_dirty = true;
+            st.rows_dirty = true;
         }
-        if (pass == 1 || wrote) {
+        if (pass == 1 || st.wrote) {
             solo_recompute<DOM>(p, e, slot, pass == 1);  // _recompute (env.py:332-347)
-            metrics_dirty = rng_dirty = true;
+            st.metrics_dirty = st.rng_dirty = true;
         }
         if (pass == 0 && mode == MODE_STEP) {
-            double reward = wrote ? __dsub_rn(before, e.prev_loss) : 0.0;
+            double reward = st.wrote ? __dsub_rn(st.before, e.prev_loss) : 0.0;
             e.ep_reward = __dadd_rn(e.ep_reward, reward);
-            if (p.rep == REP_NARROW) {  // pos_idx = (pos_idx + 1) % order_len
-                SB ed = andnot(rect_sb(e.h, e.w), e.frz);
-                int nidx = e.pos_idx + 1, nxt;
-                if (nidx >= e.order_len) {
-                    nidx = 0;
-                    nxt = solo_serp_first(ed, 0);
-                } else {
-                    nxt = solo_serp_next(ed, e.pr, e.pc);
-                }
-                e.pos_idx = nidx;
-                e.pr = nxt >> 4;
-                e.pc = nxt & 15;
-            }
-            e.t += 1;
-            bool done = e.t >= e.max_steps;
-            if (p.budget > 0) done |= e.changes >= p.budget;
+            const bool done = st.ends;
             p.reward[env] = reward;
             p.done[env] = done;
             if (p.terminal) p.terminal[env] = done;
@@ -935,11 +962,20 @@ __device__ __forceinline__ void solo_env(const Params &p, int mode, long long en
                 atomicAdd(p.stats + 3, e.ep_start_loss);
                 atomicAdd(p.stats + 4, e.prev_loss);
             }
-            reset_now = done && !p.no_auto_reset;
+            st.reset_now = done && !p.no_auto_reset;
         }
     }
-    if (mode != MODE_OBSERVE) solo_store<DOM>(p, env, e, rows_dirty, planes_dirty, metrics_dirty, rng_dirty, cold);
-    if (p.obs) solo_render<DOM>(p, e, img, stream, bit0, last);
+    if (mode != MODE_OBSERVE)
+        solo_store<DOM>(p, env, e, st.rows_dirty, st.planes_dirty, st.metrics_dirty, st.rng_dirty, st.cold);
+}
+
+template <int DOM>
+__device__ __forceinline__ void solo_env(const Params &p, int mode, long long env, uint32_t *slot, uint32_t *img,
+                                         bool stream, uint32_t bit0, bool last) {
+    SoloStep<DOM> st;
+    solo_begin<DOM>(p, mode, env, st);
+    solo_finish<DOM>(p, mode, env, st, slot);
+    if (p.obs) solo_render<DOM>(p, st.e, img, stream, bit0, last);
 }
 
 template <int DOM>
@@ -978,8 +1014,34 @@ __device__ __forceinline__ void env_solo_body(const Params &p, int mode) {
     } else {
         scratch = img = grp + (size_t)local * p.env_smem;
     }
-    if (valid)
+    // Early observation (warp mode, float32 planes only): render right after
+    // the action, store the first half of the warp's output, recompute, then
+    // store the rest -- so a launch does not start with every warp computing
+    // and no warp storing (one-wave batches: c3; the shards of a multi-GPU c5).
+    // Not when an env of the warp ends this step (auto-reset changes its map).
+    if (warp_mode && p.early && mode == MODE_STEP && p.obs && p.n_ctrl == 0 && !p.obs_u8 && !p.obs_bits &&
+        (p.stream_mode || p.PB == p.PE) &&
+        (reinterpret_cast<uintptr_t>(p.obs + (size_t)env0 * p.PE) & 31) == 0) {
+        SoloStep<DOM> st;
+        if (valid) solo_begin<DOM>(p, mode, env, st);
+        if (!__any_sync(0xffffffffu, valid && st.ends)) {
+            if (valid) solo_render<DOM>(p, st.e, img, p.stream_mode != 0, (uint32_t)local * p.PE, local == nenv - 1);
+            __syncwarp();
+            const uint32_t nv = (uint32_t)nenv * p.PE / 8, qm = (nv / 2) & ~127u;  // multiple of nthr * U
+            if (p.stream_mode) solo_write_stream<8, 2>(p, grp, env0, nenv, wl, nthr, 0, qm);
+            else solo_write_noctrl<LG_WRITER_U>(p, grp, env0, nenv, wl, nthr, 0, qm);
+            if (valid) solo_finish<DOM>(p, mode, env, st, scratch);
+            if (p.stream_mode) solo_write_stream<8, 2>(p, grp, env0, nenv, wl, nthr, qm);
+            else solo_write_noctrl<LG_WRITER_U>(p, grp, env0, nenv, wl, nthr, qm);
+            return;
+        }
+        if (valid) {
+            solo_finish<DOM>(p, mode, env, st, scratch);
+            solo_render<DOM>(p, st.e, img, p.stream_mode != 0, (uint32_t)local * p.PE, local == nenv - 1);
+        }
+    } else if (valid) {
         solo_env<DOM>(p, mode, env, scratch, img, p.stream_mode != 0, (uint32_t)local * p.PE, local == nenv - 1);
+    }
     if (p.stream_mode) {
         if (!p.obs) return;
         if (warp_mode) __syncwarp();

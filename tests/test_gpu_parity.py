@@ -232,6 +232,11 @@ def test_pinpoint_overflow_flags_error():
 
 WARP_MODE_CASES = [
     (dict(domain="binary"), 40000, 4),
+    # episodes ending at different steps: warps mixing early-observation and
+    # end-of-episode (auto-reset) envs, slot and stream layouts
+    (dict(domain="binary", change_budget=2), 20000, 10),
+    (dict(domain="dungeon", representation="wide", change_budget=3), 20000, 10),
+    (dict(domain="maze", representation="turtle", max_steps=4), 19500, 9),
     (dict(domain="binary"), 19001, 4),  # ragged last warp and block
     (dict(domain="dungeon", representation="wide"), 18977, 3),  # ragged, stream layout
     (dict(domain="maze", representation="turtle"), 20000, 4),
