@@ -1092,11 +1092,13 @@ __device__ __forceinline__ void env_solo_body(const Params &p, int mode) {
     }
 }
 
-// Register caps (measured): binary keeps 7 x 64-thread blocks per SM at 144
-// registers with no spills; maze/dungeon run faster at 8 blocks (128 regs)
-// despite a few spills (c3: 418 M vs 343 M env-steps/s).
+// Register caps (measured): binary runs 8 x 64-thread blocks per SM at 128
+// registers (8 bytes of spills; with the early-observation split it would
+// otherwise take 133 and 7 blocks: 131k-env shard 366 M vs 355 M, c5 equal);
+// maze/dungeon run faster at 8 blocks (128 regs) despite spills (c3: 418 M
+// vs 343 M env-steps/s at 144).
 #ifndef LG_BINARY_NREG
-#define LG_BINARY_NREG 144
+#define LG_BINARY_NREG 128
 #endif
 __global__ void __maxnreg__(LG_BINARY_NREG) env_solo_kernel_binary(const Params p, int mode) { env_solo_body<0>(p, mode); }
 __global__ void __maxnreg__(128) env_solo_kernel_maze(const Params p, int mode) { env_solo_body<1>(p, mode); }
