@@ -916,6 +916,39 @@ __global__ void __launch_bounds__(64, G::MINB) env_kernel(const Params p, int mo
         } else if (mode == MODE_REPRICE) {
             if (!p.reset_mask || p.reset_mask[env]) e.prev_loss = loss_of<DOM>(p, e.val, e.unr, e.lo, e.hi);
         }
+        bool ends = false, early = false;
+        if (mode == MODE_STEP) {
+            // scan advance and t (env.py:374-381) do not depend on the recompute
+            if (p.rep == REP_NARROW) {  // pos_idx = (pos_idx + 1) % order_len
+                int nidx = e.pos_idx + 1;
+                int nxt;
+                Bd<G> ed = andnot(rect_board(t, e.h, e.w), e.frz);
+                if (nidx >= e.order_len) {
+                    nidx = 0;
+                    nxt = serp_first_from(t, ed, 0);
+                } else {
+                    nxt = serp_next(t, ed, e.pr, e.pc);
+                }
+                e.pos_idx = nidx;
+                e.pr = nxt >> 6;
+                e.pc = nxt & 63;
+            }
+            e.t += 1;
+            ends = e.t >= e.max_steps || (p.budget > 0 && e.changes >= p.budget);
+            // early observation: unless the episode ends (auto-reset) or control
+            // planes show metric values, the observation is final now -- write
+            // it before the recompute so its stores drain while the team computes
+            early = p.early && p.obs && p.n_ctrl == 0 && !ends;
+            if (early) {
+                t.sync();
+                render_env<G, DOM>(p, t, e, es);
+                t.sync();
+                if (p.obs_bits) write_obs_team_bits<G>(p, t, env, es);
+                else if (p.obs_u8) write_obs_team_u8<G>(p, t, env, es);
+                else write_obs_team<G>(p, t, env, es);
+                t.sync();  // the image doubles as union-find scratch
+            }
+        }
         // pass 0: the step's recompute + bookkeeping; pass 1: auto-reset (one
         // call site for the metric code keeps the instruction footprint small)
 #pragma unroll 1
@@ -932,23 +965,7 @@ __global__ void __launch_bounds__(64, G::MINB) env_kernel(const Params p, int mo
             if (pass == 0 && mode == MODE_STEP) {
                 double reward = wrote ? __dsub_rn(before, e.prev_loss) : 0.0;
                 e.ep_reward = __dadd_rn(e.ep_reward, reward);
-                if (p.rep == REP_NARROW) {  // pos_idx = (pos_idx + 1) % order_len
-                    int nidx = e.pos_idx + 1;
-                    int nxt;
-                    Bd<G> ed = andnot(rect_board(t, e.h, e.w), e.frz);
-                    if (nidx >= e.order_len) {
-                        nidx = 0;
-                        nxt = serp_first_from(t, ed, 0);
-                    } else {
-                        nxt = serp_next(t, ed, e.pr, e.pc);
-                    }
-                    e.pos_idx = nidx;
-                    e.pr = nxt >> 6;
-                    e.pc = nxt & 63;
-                }
-                e.t += 1;
-                bool done = e.t >= e.max_steps;
-                if (p.budget > 0) done |= e.changes >= p.budget;
+                const bool done = ends;
                 if (t.lane == 0) {
                     p.reward[env] = reward;
                     p.done[env] = done;
@@ -969,7 +986,7 @@ __global__ void __launch_bounds__(64, G::MINB) env_kernel(const Params p, int mo
             }
         }
         if (mode != MODE_OBSERVE) store_env<G, DOM>(p, t, env, e, rows_dirty, dirty_row, metrics_dirty, rng_dirty);
-        if (p.obs) {
+        if (p.obs && !early) {
             t.sync();  // union-find scratch is reused for the image
             render_env<G, DOM>(p, t, e, es);
             t.sync();

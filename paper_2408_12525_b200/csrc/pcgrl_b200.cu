@@ -339,7 +339,10 @@ static int launch_env_t(lg_env *e, const Params &p, int mode, cudaStream_t s) {
     CU(attr_err);
     int E = e->threads / G::TEAM;
     long long grid = (e->B + E - 1) / E;
-    env_kernel<G, DOM><<<(unsigned)grid, e->threads, e->smem, s>>>(p, mode);
+    Params q = p;
+    const char *ea = getenv("LG_EARLY");
+    q.early = ea ? ea[0] == '1' : 1;
+    env_kernel<G, DOM><<<(unsigned)grid, e->threads, e->smem, s>>>(q, mode);
     CU(cudaGetLastError());
     return LG_OK;
 }
