@@ -403,6 +403,8 @@ class NumpyBatchEnv:
         self.pinned = pinned
         self.copy = copy
         self._bufs = None
+        self._args = None
+        self._obs_seen = None
 
     config = property(lambda self: self.env.config)
     n_envs = property(lambda self: self.env.n_envs)
@@ -442,15 +444,23 @@ class NumpyBatchEnv:
             raise ValueError("action id out of range")
         if self._bufs is None or (self.copy and not self.pinned):
             self._bufs = self._host()
+            p = lambda x: x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+            b = self._bufs
+            # argument pointers built once per buffer set (small batches are latency-bound)
+            self._args = (p(b["actions"]), p(b["obs"]), p(b["reward"]), p(b["done"]),
+                          ctypes.byref(_lib.LgInfo(*[p(b[k]) for k in INFO_KEYS])))
         b = self._bufs
+        if b["obs"] is not self._obs_seen:  # a caller may swap in its own obs array
+            self._obs_seen = b["obs"]
+            self._args = self._args[:1] + (b["obs"].ctypes.data_as(ctypes.c_void_p),) + self._args[2:]
         np.copyto(b["actions"], a)
-        p = lambda x: x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
-        ci = _lib.LgInfo(*[p(b[k]) for k in INFO_KEYS])
         t = self.env._torch
-        with t.cuda.device(self.env.device):
-            _lib.check(_lib.load().lg_step_host(self.env.handle, p(b["actions"]), p(b["obs"]),
-                                                p(b["reward"]), p(b["done"]), ctypes.byref(ci),
-                                                _stream(t, self.env.device)))
+        dev = self.env.device
+        if t.cuda.current_device() == dev.index:
+            _lib.check(_lib.load().lg_step_host(self.env.handle, *self._args, _stream(t, dev)))
+        else:
+            with t.cuda.device(dev):
+                _lib.check(_lib.load().lg_step_host(self.env.handle, *self._args, _stream(t, dev)))
         info = {k: b[k] for k in INFO_KEYS}
         out = (b["obs"], b["reward"], b["done"], info)
         if self.copy and self.pinned:
