@@ -733,7 +733,11 @@ static int check_obs_ptr(const void *obs) {
 static bool packed_ok(const lg_env *e) {
     if (e->cfg.n_ctrl > 0) return false;
     const char *v = getenv("LG_HOST_EXPAND");
-    return !(v && v[0] == '0');
+    if (v) return v[0] != '0';
+    // below ~2 MB of float32 observations the copy is latency, not bandwidth:
+    // the plain copy wins (c1, 64 envs: 0.61 vs 0.58 M env-steps/s)
+    const size_t n = (size_t)e->B * e->C * e->OH * e->OW;
+    return n * 4 >= ((size_t)2 << 20);
 }
 
 // Some stream words are shared by two blocks (or lane teams): they are

@@ -464,6 +464,7 @@ def test_packed_host_transfer_equals_device_obs(case, obs_dtype, monkeypatch):
     """NumpyBatchEnv.step (packed bits over PCIe, host expansion) returns the
     same observations as the device path, for every kernel and layout."""
     kw, n, envs = PACKED_CASES[case]
+    monkeypatch.setenv("LG_HOST_EXPAND", "1")  # small batches would take the plain copy by default
     for k, v in envs.items():
         monkeypatch.setenv(k, v)
     cfg = EnvConfig(**kw)
