@@ -151,26 +151,19 @@ __device__ __forceinline__ void solo_store(const Params &p, long long env, const
     hv.max_steps = e.max_steps;
     p.hot[env] = hv;
     constexpr int M = Dom<DOM>::M;
-    if (metrics_dirty && M <= 2) {  // only live entries: the rest stay dead registers
-        int2 *m2 = reinterpret_cast<int2 *>(p.mv + env * 24);
-        m2[0] = make_int2(e.val[0], e.val[1]);
-        m2[4] = make_int2(e.lo[0], e.lo[1]);
-        m2[8] = make_int2(e.hi[0], e.hi[1]);
-        p.mv[env * 24 + 7] = e.unr;
-    } else if (metrics_dirty && M <= 4) {
+    // metric values + unreachable mask: one whole 32-byte sector (ints 0..7),
+    // so the write needs no DRAM read-fill; the targets (lo/hi) change only
+    // when an episode starts (rows_dirty) and are written only then.
+    if (metrics_dirty) {
         int4 *mv = reinterpret_cast<int4 *>(p.mv + env * 24);
-        mv[0] = make_int4(e.val[0], e.val[1], e.val[2], e.val[3]);
-        mv[2] = make_int4(e.lo[0], e.lo[1], e.lo[2], e.lo[3]);
-        mv[4] = make_int4(e.hi[0], e.hi[1], e.hi[2], e.hi[3]);
-        p.mv[env * 24 + 7] = e.unr;
-    } else if (metrics_dirty) {
-        int4 *mv = reinterpret_cast<int4 *>(p.mv + env * 24);
-        mv[0] = make_int4(e.val[0], e.val[1], e.val[2], e.val[3]);
-        mv[1] = make_int4(e.val[4], e.val[5], e.val[6], e.unr);
-        mv[2] = make_int4(e.lo[0], e.lo[1], e.lo[2], e.lo[3]);
-        mv[3] = make_int4(e.lo[4], e.lo[5], e.lo[6], e.lo[7]);
-        mv[4] = make_int4(e.hi[0], e.hi[1], e.hi[2], e.hi[3]);
-        mv[5] = make_int4(e.hi[4], e.hi[5], e.hi[6], e.hi[7]);
+        mv[0] = make_int4(e.val[0], e.val[1], M > 2 ? e.val[2] : 0, M > 3 ? e.val[3] : 0);
+        mv[1] = make_int4(M > 4 ? e.val[4] : 0, M > 5 ? e.val[5] : 0, M > 6 ? e.val[6] : 0, e.unr);
+        if (rows_dirty) {
+            mv[2] = make_int4(e.lo[0], e.lo[1], e.lo[2], e.lo[3]);
+            mv[3] = make_int4(e.lo[4], e.lo[5], e.lo[6], e.lo[7]);
+            mv[4] = make_int4(e.hi[0], e.hi[1], e.hi[2], e.hi[3]);
+            mv[5] = make_int4(e.hi[4], e.hi[5], e.hi[6], e.hi[7]);
+        }
     }
     double2 *lv = reinterpret_cast<double2 *>(p.lossv + env * 4);
     if (cold) lv[0] = make_double2(e.prev_loss, e.ep_reward);
