@@ -80,9 +80,10 @@ struct Params {
     Hot *hot;            // [B]
     int *mv;             // [B][24]: values 0..6, unreach mask at 7, lo 8..14, hi 16..22
     double *lossv;       // [B][4]: prev_loss, ep_reward, ep_start_loss, -
-    ulonglong2 *rs;      // [B] PCG state (hi, lo)
+    ulonglong2 *rs;      // [B][2] PCG state (hi, lo), then (has_uint32 | uinteger << 32, 0):
+                         // one 32-byte sector per env, rewritten whole (no partial-sector fill)
     ulonglong2 *ri;      // [B] PCG inc (hi, lo)
-    uint2 *rb;           // [B] (has_uint32, uinteger)
+    uint2 *rb;           // unused (kept for the layout of Params)
     long long *mseed;    // [B]
     unsigned *err;       // error flags
     // io
@@ -116,6 +117,18 @@ struct Params {
     unsigned *aux;  // [1] device flag: an imported env has an active frozen cell
     int early;      // solo warp mode: render + store half the outputs before the recompute
 };
+
+__device__ __forceinline__ void rng_load(const Params &p, long long env, Pcg &g) {
+    const ulonglong2 s = p.rs[2 * env], b = p.rs[2 * env + 1], inc = p.ri[env];
+    g.s = ((u128)s.x << 64) | s.y;
+    g.inc = ((u128)inc.x << 64) | inc.y;
+    g.has = (uint32_t)b.x;
+    g.u = (uint32_t)(b.x >> 32);
+}
+__device__ __forceinline__ void rng_store(const Params &p, long long env, const Pcg &g) {
+    p.rs[2 * env] = make_ulonglong2((unsigned long long)(g.s >> 64), (unsigned long long)g.s);
+    p.rs[2 * env + 1] = make_ulonglong2((unsigned long long)g.has | ((unsigned long long)g.u << 32), 0ull);
+}
 
 template <class G, int DOM>
 struct EnvRegs {
@@ -541,12 +554,7 @@ __device__ __forceinline__ void load_env(const Params &p, const Team<G> &t, long
     e.prev_loss = l0.x;
     e.ep_reward = l0.y;
     e.ep_start_loss = l1.x;
-    ulonglong2 s = p.rs[env], inc = p.ri[env];
-    uint2 bf = p.rb[env];
-    e.g.s = ((u128)s.x << 64) | s.y;
-    e.g.inc = ((u128)inc.x << 64) | inc.y;
-    e.g.has = bf.x;
-    e.g.u = bf.y;
+    rng_load(p, env, e.g);
     e.mseed = p.det ? p.mseed[env] : 0;
 }
 
@@ -588,8 +596,7 @@ __device__ __forceinline__ void store_env(const Params &p, const Team<G> &t, lon
     lv[0] = make_double2(e.prev_loss, e.ep_reward);
     if (metrics_dirty) lv[1] = make_double2(e.ep_start_loss, 0.0);
     if (rng_dirty) {
-        p.rs[env] = make_ulonglong2((unsigned long long)(e.g.s >> 64), (unsigned long long)e.g.s);
-        p.rb[env] = make_uint2(e.g.has, e.g.u);
+        rng_store(p, env, e.g);
         if (p.det) p.mseed[env] = e.mseed;
     }
 }

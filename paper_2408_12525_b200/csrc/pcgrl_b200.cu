@@ -46,9 +46,9 @@ __global__ void seed_kernel(long long B, unsigned long long seed, long long offs
     if (b >= B) return;
     Pcg g;
     seedseq_pcg(seed, true, (uint64_t)(offset + b), g);
-    rs[b] = make_ulonglong2((unsigned long long)(g.s >> 64), (unsigned long long)g.s);
+    rs[2 * b] = make_ulonglong2((unsigned long long)(g.s >> 64), (unsigned long long)g.s);
+    rs[2 * b + 1] = make_ulonglong2(0ull, 0ull);  // has_uint32 = 0, uinteger = 0
     ri[b] = make_ulonglong2((unsigned long long)(g.inc >> 64), (unsigned long long)g.inc);
-    rb[b] = make_uint2(0, 0);
 }
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -207,9 +207,9 @@ __global__ void __launch_bounds__(256) import_kernel(const Params p, lg_state sr
     lv[3] = 0.0;
     p.mseed[env] = src.metric_seeds[env];
     const uint64_t *rg = src.rng + 6 * env;
-    p.rs[env] = make_ulonglong2(rg[0], rg[1]);
+    p.rs[2 * env] = make_ulonglong2(rg[0], rg[1]);
+    p.rs[2 * env + 1] = make_ulonglong2((rg[4] & 0xFFFFFFFFull) | (rg[5] << 32), 0ull);
     p.ri[env] = make_ulonglong2(rg[2], rg[3]);
-    p.rb[env] = make_uint2((unsigned)rg[4], (unsigned)rg[5]);
 }
 
 // compute_metrics_batch on raw stacks (problems.py:105-129), team per grid.
@@ -663,9 +663,8 @@ extern "C" int lg_create(const lg_config *cfg, int64_t n_envs, int64_t global_of
     alloc((void **)&p.hot, B * sizeof(Hot));
     alloc((void **)&p.mv, B * 24 * sizeof(int));
     alloc((void **)&p.lossv, B * 4 * sizeof(double));
-    alloc((void **)&p.rs, B * sizeof(ulonglong2));
+    alloc((void **)&p.rs, B * 2 * sizeof(ulonglong2));
     alloc((void **)&p.ri, B * sizeof(ulonglong2));
-    alloc((void **)&p.rb, B * sizeof(uint2));
     alloc((void **)&p.mseed, B * sizeof(long long));
     alloc((void **)&p.err, sizeof(unsigned));
     alloc((void **)&p.aux, sizeof(unsigned));

@@ -113,12 +113,7 @@ __device__ __forceinline__ void solo_load_cold(const Params &p, long long env, S
     e.prev_loss = l0.x;
     e.ep_reward = l0.y;
     e.ep_start_loss = l1.x;
-    ulonglong2 s = p.rs[env], inc = p.ri[env];
-    uint2 bf = p.rb[env];
-    e.g.s = ((u128)s.x << 64) | s.y;
-    e.g.inc = ((u128)inc.x << 64) | inc.y;
-    e.g.has = bf.x;
-    e.g.u = bf.y;
+    rng_load(p, env, e.g);
     e.mseed = p.det ? p.mseed[env] : 0;
 }
 
@@ -166,11 +161,12 @@ __device__ __forceinline__ void solo_store(const Params &p, long long env, const
         }
     }
     double2 *lv = reinterpret_cast<double2 *>(p.lossv + env * 4);
-    if (cold) lv[0] = make_double2(e.prev_loss, e.ep_reward);
-    if (metrics_dirty) lv[1] = make_double2(e.ep_start_loss, 0.0);
+    if (cold) {  // the whole 32-byte record (metrics_dirty implies cold)
+        lv[0] = make_double2(e.prev_loss, e.ep_reward);
+        lv[1] = make_double2(e.ep_start_loss, 0.0);
+    }
     if (rng_dirty) {
-        p.rs[env] = make_ulonglong2((unsigned long long)(e.g.s >> 64), (unsigned long long)e.g.s);
-        p.rb[env] = make_uint2(e.g.has, e.g.u);
+        rng_store(p, env, e.g);
         if (p.det) p.mseed[env] = e.mseed;
     }
 }
@@ -1246,9 +1242,9 @@ __global__ void solo_import_kernel(const Params p, lg_state src) {
     lv[3] = 0.0;
     p.mseed[env] = src.metric_seeds[env];
     const uint64_t *rg = src.rng + 6 * env;
-    p.rs[env] = make_ulonglong2(rg[0], rg[1]);
+    p.rs[2 * env] = make_ulonglong2(rg[0], rg[1]);
+    p.rs[2 * env + 1] = make_ulonglong2((rg[4] & 0xFFFFFFFFull) | (rg[5] << 32), 0ull);
     p.ri[env] = make_ulonglong2(rg[2], rg[3]);
-    p.rb[env] = make_uint2((unsigned)rg[4], (unsigned)rg[5]);
 }
 
 // compute_metrics_batch on raw stacks for maps <= 16x16, one grid per thread.
