@@ -36,9 +36,12 @@ struct SoloEnv {
     long long mseed;
 };
 
-template <int DOM>
-__device__ __forceinline__ uint32_t *solo_rows(const Params &p, long long env) {
-    return reinterpret_cast<uint32_t *>(p.rows) + (size_t)env * (Dom<DOM>::NPL + 1) * 8;
+// Bit-planes plane-major: plane q (q < NPL tile planes, q == NPL frozen) of
+// env b is 32 bytes at rows + (q * B + b) * 32, so a warp's 32 envs read one
+// contiguous KB per plane and a step that never touches the frozen plane does
+// not drag its bytes along (DRAM bursts are wider than a sector).
+__device__ __forceinline__ uint32_t *solo_plane(const Params &p, long long env, int q) {
+    return reinterpret_cast<uint32_t *>(p.rows) + ((size_t)q * p.B + env) * 8;
 }
 
 // Per-step state traffic is split: the "hot" part (tile planes, geometry,
@@ -51,10 +54,10 @@ __device__ __forceinline__ uint32_t *solo_rows(const Params &p, long long env) {
 template <int DOM>
 __device__ __forceinline__ void solo_load_hot(const Params &p, long long env, SoloEnv<DOM> &e) {
     constexpr int NPL = Dom<DOM>::NPL;
-    const uint4 *rw = reinterpret_cast<const uint4 *>(solo_rows<DOM>(p, env));
 #pragma unroll
     for (int q = 0; q < NPL; q++) {
-        uint4 a = rw[2 * q], b = rw[2 * q + 1];
+        const uint4 *rw = reinterpret_cast<const uint4 *>(solo_plane(p, env, q));
+        uint4 a = rw[0], b = rw[1];
         SB &d = e.pl[q];
         d.w[0] = a.x; d.w[1] = a.y; d.w[2] = a.z; d.w[3] = a.w;
         d.w[4] = b.x; d.w[5] = b.y; d.w[6] = b.z; d.w[7] = b.w;
@@ -72,7 +75,8 @@ __device__ __forceinline__ void solo_load_hot(const Params &p, long long env, So
     if (p.frz_derived) {  // no active frozen cell in any env: frozen = max grid minus the episode rect
         e.frz = andnot(rect_sb(p.H, p.W), rect_sb(e.h, e.w));
     } else {
-        uint4 a = rw[2 * NPL], b = rw[2 * NPL + 1];
+        const uint4 *rw = reinterpret_cast<const uint4 *>(solo_plane(p, env, NPL));
+        uint4 a = rw[0], b = rw[1];
         SB &d = e.frz;
         d.w[0] = a.x; d.w[1] = a.y; d.w[2] = a.z; d.w[3] = a.w;
         d.w[4] = b.x; d.w[5] = b.y; d.w[6] = b.z; d.w[7] = b.w;
@@ -128,13 +132,13 @@ __device__ __forceinline__ void solo_store(const Params &p, long long env, const
                            bool planes_dirty, bool metrics_dirty, bool rng_dirty, bool cold = true) {
     constexpr int NPL = Dom<DOM>::NPL;
     if (rows_dirty || planes_dirty) {
-        uint4 *rw = reinterpret_cast<uint4 *>(solo_rows<DOM>(p, env));
 #pragma unroll
         for (int q = 0; q <= NPL; q++) {
             if (q == NPL && !rows_dirty) break;
             const SB &d = q < NPL ? e.pl[q] : e.frz;
-            rw[2 * q] = make_uint4(d.w[0], d.w[1], d.w[2], d.w[3]);
-            rw[2 * q + 1] = make_uint4(d.w[4], d.w[5], d.w[6], d.w[7]);
+            uint4 *rw = reinterpret_cast<uint4 *>(solo_plane(p, env, q));
+            rw[0] = make_uint4(d.w[0], d.w[1], d.w[2], d.w[3]);
+            rw[1] = make_uint4(d.w[4], d.w[5], d.w[6], d.w[7]);
         }
     }
     Hot hv;
@@ -1198,11 +1202,12 @@ __global__ void solo_import_kernel(const Params p, lg_state src) {
                 if (src.frozen[o]) wq[NPL][k] |= bit;
             }
         }
-    uint32_t *rw = solo_rows<DOM>(p, env);
 #pragma unroll
-    for (int q = 0; q <= NPL; q++)
+    for (int q = 0; q <= NPL; q++) {
+        uint32_t *rw = solo_plane(p, env, q);
 #pragma unroll
-        for (int k = 0; k < 8; k++) rw[q * 8 + k] = wq[q][k];
+        for (int k = 0; k < 8; k++) rw[k] = wq[q][k];
+    }
     Hot hv;
     uint32_t h = (uint32_t)src.shape_hw[2 * env], w = (uint32_t)src.shape_hw[2 * env + 1];
     {  // frozen plane != border plane (~active rectangle) inside the max grid?
