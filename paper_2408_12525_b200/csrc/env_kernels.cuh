@@ -564,10 +564,12 @@ __device__ __forceinline__ void store_env(const Params &p, const Team<G> &t, lon
     constexpr int NPL = Dom<DOM>::NPL;
     if (rows_dirty || dirty_row >= 0) {
         typename G::Row *rw = rows_of<G, DOM>(p, env);
+        constexpr int SEC = 32 / (int)sizeof(typename G::Row);  // rows per 32-byte sector
 #pragma unroll
         for (int k = 0; k < G::RPL; k++) {
             int r = t.row(k);
-            if (rows_dirty || r == dirty_row) {
+            // the whole sector around the edited row (no partial-sector read-fill)
+            if (rows_dirty || (dirty_row >= 0 && r / SEC == dirty_row / SEC)) {
 #pragma unroll
                 for (int q = 0; q < NPL; q++) rw[q * G::ROWS + r] = e.pl[q].r[k];
                 if (rows_dirty) rw[NPL * G::ROWS + r] = e.frz.r[k];
@@ -594,7 +596,7 @@ __device__ __forceinline__ void store_env(const Params &p, const Team<G> &t, lon
     }
     double2 *lv = reinterpret_cast<double2 *>(p.lossv + env * 4);
     lv[0] = make_double2(e.prev_loss, e.ep_reward);
-    if (metrics_dirty) lv[1] = make_double2(e.ep_start_loss, 0.0);
+    lv[1] = make_double2(e.ep_start_loss, 0.0);
     if (rng_dirty) {
         rng_store(p, env, e.g);
         if (p.det) p.mseed[env] = e.mseed;
