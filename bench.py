@@ -182,7 +182,7 @@ def main():
     ap.add_argument("--envs", type=int, default=0, help="override the global env count")
     ap.add_argument("--cpu-envs", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-u8", action="store_true", help="skip the opt-in uint8-observation side run")
@@ -321,7 +321,7 @@ def main():
         nenv.step(a0)  # sizes the timed loop
         per = time.perf_counter() - t0
         # at least e2e_steps steps and ~0.3 s of them (small batches are microseconds per step)
-        n_steps = max(args.e2e_steps, min(500, int(0.3 / max(per, 1e-6))))
+        n_steps = max(args.e2e_steps, min(500, int(0.5 / max(per, 1e-6))))
         if world > 1:
             n_steps = int(max_over_ranks(float(n_steps), dev))
         host_acts = [rng.integers(0, cfg.n_actions, size=B) for _ in range(n_steps)]
