@@ -116,6 +116,7 @@ struct Params {
     int frz_derived;  // solo: frozen plane == max grid minus episode rect in every env (not read)
     unsigned *aux;  // [1] device flag: an imported env has an active frozen cell
     int early;      // solo warp mode: render + store half the outputs before the recompute
+    int coop;       // solo block mode: the warp renders its envs' images together
 };
 
 __device__ __forceinline__ void rng_load(const Params &p, long long env, Pcg &g) {

@@ -364,6 +364,8 @@ static int launch_solo_t(lg_env *e, const Params &p, int mode, cudaStream_t s) {
     // +14%; dungeon's larger step spills under it (c3 graph replay -1.5%)
     const char *ea = getenv("LG_EARLY");
     q.early = ea ? ea[0] == '1' : (DOM != 2 && !getenv("LG_NO_EARLY"));
+    const char *co = getenv("LG_COOP");
+    q.coop = co ? co[0] == '1' : 1;
     if (e->elide_ok && e->plain && p.obs) {
         q.elide = 1;
         q.env_smem = e->slot_elide;
