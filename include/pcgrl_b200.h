@@ -148,6 +148,11 @@ int lg_step_host(lg_env *env, const int64_t *actions_host, void *obs_host, doubl
                  uint8_t *done_host, const lg_info *info_host, void *stream);
 /* Host threads lg_step_host expands observations with (LG_HOST_THREADS). */
 int lg_host_threads(void);
+/* Host-side expansion of a packed observation stream (LG_OBS_BITS layout,
+ * element t = bit t%32 of word t/32) into n_elems float32 (fmt 0) or uint8
+ * (fmt 1) 0/1 values at dst (any alignment). What lg_step_host does after the
+ * copy; no GPU involved. */
+int lg_unpack_host(const uint32_t *bits, int64_t n_elems, void *dst, int fmt);
 
 /* Designer edits on imported states: recompute metrics + loss of the masked
  * envs (mask NULL = all) after their tiles/frozen planes changed (with_pin /

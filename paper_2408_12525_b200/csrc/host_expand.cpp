@@ -161,7 +161,7 @@ void expand_bits(const uint8_t *bits, void *dst, int fmt, size_t n_elems, size_t
             while (ready_upto.load(std::memory_order_acquire) <= c) {
                 if (poll.try_lock()) {
                     size_t k = ready_upto.load(std::memory_order_relaxed);
-                    while (k < nchunks && ready(ctx, k)) k++;
+                    while (k < nchunks && (!ready || ready(ctx, k))) k++;
                     ready_upto.store(k, std::memory_order_release);
                     poll.unlock();
                     if (k > c) break;

@@ -13,8 +13,9 @@ namespace lg_host {
 // Expand stream bits [0, n_elems) of `bits` into dst (float32 when fmt == 0,
 // uint8 when fmt == 1). The stream is processed in chunks of chunk_bytes
 // bytes of `bits` (a multiple of 64); chunk c is read only after ready(ctx, c)
-// returned true (polled by the workers). Runs on the library's host thread
-// pool plus the calling thread; returns after dst is complete.
+// returned true (polled by the workers; ready == nullptr: every chunk is
+// there). Runs on the library's host thread pool plus the calling thread
+// (small outputs: the calling thread only); returns after dst is complete.
 void expand_bits(const uint8_t *bits, void *dst, int fmt, size_t n_elems, size_t chunk_bytes,
                  bool (*ready)(void *ctx, size_t chunk), void *ctx);
 

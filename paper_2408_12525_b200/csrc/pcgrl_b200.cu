@@ -914,6 +914,18 @@ extern "C" int lg_step_host(lg_env *e, const int64_t *actions_host, void *obs_ho
 
 extern "C" int lg_host_threads(void) { return lg_host::expand_threads(); }
 
+extern "C" int lg_unpack_host(const uint32_t *bits, int64_t n_elems, void *dst, int fmt) {
+    if (!bits || !dst || n_elems < 0 || (fmt != 0 && fmt != 1)) {
+        set_err("unpack_host needs bits, a destination, n_elems >= 0 and fmt 0 (float32) or 1 (uint8)");
+        return LG_EINVAL;
+    }
+    if (n_elems == 0) return LG_OK;
+    const size_t bytes = ((size_t)n_elems + 7) / 8;
+    lg_host::expand_bits(reinterpret_cast<const uint8_t *>(bits), dst, fmt, (size_t)n_elems,
+                         (bytes + 63) & ~(size_t)63, nullptr, nullptr);
+    return LG_OK;
+}
+
 #ifndef LG_CONV1_EB
 #define LG_CONV1_EB 4  // envs per block iteration in conv1_bits_kernel
 #endif
