@@ -354,6 +354,9 @@ static int launch_solo_t(lg_env *e, const Params &p, int mode, cudaStream_t s) {
     std::call_once(once, [] {
         attr_err = cudaFuncSetAttribute(SoloKernel<DOM>::fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         200 * 1024);
+        if (attr_err == cudaSuccess)
+            attr_err = cudaFuncSetAttribute(SoloKernel<DOM>::fn_small,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     });
     CU(attr_err);
     long long grid = (e->B + e->E - 1) / e->E;
@@ -363,7 +366,7 @@ static int launch_solo_t(lg_env *e, const Params &p, int mode, cudaStream_t s) {
     // early observation stores (solo_kernel.cuh): c5 +2.5%, its 131k-env shard
     // +14%; dungeon's larger step spills under it (c3 graph replay -1.5%)
     const char *ea = getenv("LG_EARLY");
-    q.early = ea ? ea[0] == '1' : (DOM != 2 && !getenv("LG_NO_EARLY"));
+    q.early = ea ? ea[0] == '1' : !getenv("LG_NO_EARLY");  // dungeon: compiled out (LG_DUNGEON_EARLY)
     const char *co = getenv("LG_COOP");
     q.coop = co ? co[0] == '1' : 1;
     if (e->elide_ok && e->plain && p.obs) {
@@ -371,7 +374,8 @@ static int launch_solo_t(lg_env *e, const Params &p, int mode, cudaStream_t s) {
         q.env_smem = e->slot_elide;
         smem = e->smem_elide;
     }
-    SoloKernel<DOM>::fn<<<(unsigned)grid, e->threads, smem, s>>>(q, mode);
+    if (e->E == e->threads) SoloKernel<DOM>::fn<<<(unsigned)grid, e->threads, smem, s>>>(q, mode);
+    else SoloKernel<DOM>::fn_small<<<(unsigned)grid, e->threads, smem, s>>>(q, mode);
     CU(cudaGetLastError());
     return LG_OK;
 }

@@ -1037,11 +1037,18 @@ __device__ __forceinline__ void solo_env(const Params &p, int mode, long long en
     if (p.obs) solo_render<DOM>(p, st.e, img, stream, bit0, last);
 }
 
-template <int DOM>
+#ifndef LG_DUNGEON_EARLY
+#define LG_DUNGEON_EARLY 0  // dungeon's warp kernel without the early-observation path (c3: spills)
+#endif
+// WARP = 1: the warp-mode kernel (E == blockDim: each warp owns 32 envs);
+// WARP = 0: the block-mode kernel (small batches). Two kernels, so neither
+// carries the other's code paths (register pressure, instruction footprint).
+template <int DOM, int WARP>
 __device__ __forceinline__ void env_solo_body(const Params &p, int mode) {
     extern __shared__ __align__(16) uint32_t smem_w[];
     const int E = p.solo_E, T = blockDim.x, tid = threadIdx.x;
-    const bool warp_mode = E == T;  // uniform over the launch
+    constexpr bool warp_mode = WARP == 1;  // the host launches this kernel only when E == T
+    (void)E;
     // warp mode (large batches): warp w owns 32 consecutive envs and writes
     // their outputs; block mode (small batches): E < T envs per block and all
     // T threads write them.
@@ -1078,7 +1085,8 @@ __device__ __forceinline__ void env_solo_body(const Params &p, int mode) {
     // store the rest -- so a launch does not start with every warp computing
     // and no warp storing (one-wave batches: c3; the shards of a multi-GPU c5).
     // Not when an env of the warp ends this step (auto-reset changes its map).
-    if (warp_mode && p.early && mode == MODE_STEP && p.obs && p.n_ctrl == 0 && !p.obs_u8 && !p.obs_bits &&
+    if (warp_mode && (DOM != 2 || LG_DUNGEON_EARLY) && p.early && mode == MODE_STEP && p.obs && p.n_ctrl == 0 &&
+        !p.obs_u8 && !p.obs_bits &&
         (p.stream_mode || p.PB == p.PE) &&
         (reinterpret_cast<uintptr_t>(p.obs + (size_t)env0 * p.PE) & 31) == 0) {
         SoloStep<DOM> st;
@@ -1169,23 +1177,29 @@ __device__ __forceinline__ void env_solo_body(const Params &p, int mode) {
 #ifndef LG_BINARY_NREG
 #define LG_BINARY_NREG 128
 #endif
-__global__ void __maxnreg__(LG_BINARY_NREG) env_solo_kernel_binary(const Params p, int mode) { env_solo_body<0>(p, mode); }
-__global__ void __maxnreg__(128) env_solo_kernel_maze(const Params p, int mode) { env_solo_body<1>(p, mode); }
-__global__ void __maxnreg__(128) env_solo_kernel_dungeon(const Params p, int mode) { env_solo_body<2>(p, mode); }
+__global__ void __maxnreg__(LG_BINARY_NREG) env_solo_kernel_binary(const Params p, int mode) { env_solo_body<0, 1>(p, mode); }
+__global__ void __maxnreg__(128) env_solo_kernel_maze(const Params p, int mode) { env_solo_body<1, 1>(p, mode); }
+__global__ void __maxnreg__(128) env_solo_kernel_dungeon(const Params p, int mode) { env_solo_body<2, 1>(p, mode); }
+__global__ void __maxnreg__(128) env_solo_kernel_binary_small(const Params p, int mode) { env_solo_body<0, 0>(p, mode); }
+__global__ void __maxnreg__(128) env_solo_kernel_maze_small(const Params p, int mode) { env_solo_body<1, 0>(p, mode); }
+__global__ void __maxnreg__(128) env_solo_kernel_dungeon_small(const Params p, int mode) { env_solo_body<2, 0>(p, mode); }
 
 template <int DOM>
 struct SoloKernel;
 template <>
 struct SoloKernel<0> {
     static constexpr auto fn = env_solo_kernel_binary;
+    static constexpr auto fn_small = env_solo_kernel_binary_small;
 };
 template <>
 struct SoloKernel<1> {
     static constexpr auto fn = env_solo_kernel_maze;
+    static constexpr auto fn_small = env_solo_kernel_maze_small;
 };
 template <>
 struct SoloKernel<2> {
     static constexpr auto fn = env_solo_kernel_dungeon;
+    static constexpr auto fn_small = env_solo_kernel_dungeon_small;
 };
 
 // ---- state export / import / metrics for the solo layout -------------------
