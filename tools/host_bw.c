@@ -25,7 +25,7 @@ int main(int argc, char **argv) {
     for (size_t i = 0; i < nf; i += 1024) dst[i] = 0.f;  // first touch
     int maxt = omp_get_max_threads();
     for (int th = 1; th <= maxt; th *= 2) {
-        for (int mode = 0; mode < 3; mode++) {
+        for (int mode = 0; mode < 4; mode++) {
             double best = 1e9;
             for (int rep = 0; rep < 3; rep++) {
                 double t0 = now();
@@ -33,7 +33,13 @@ int main(int argc, char **argv) {
                 for (size_t w = 0; w < nf / 32; w++) {
                     uint32_t x = bits[w];
                     float *o = dst + w * 32;
-                    if (mode == 0) {  // plain NT store of zeros (write ceiling)
+                    if (mode == 3) {  // AVX-512: one 64-byte NT store per 16 elements
+                        for (int k = 0; k < 2; k++) {
+                            __mmask16 m = (__mmask16)((x >> (16 * k)) & 0xFFFF);
+                            __m512 f = _mm512_maskz_mov_ps(m, _mm512_set1_ps(1.0f));
+                            _mm512_stream_ps(o + 16 * k, f);
+                        }
+                    } else if (mode == 0) {  // plain NT store of zeros (write ceiling)
                         __m256 z = _mm256_setzero_ps();
                         for (int k = 0; k < 4; k++) _mm256_stream_ps(o + 8 * k, z);
                     } else {
@@ -51,7 +57,8 @@ int main(int argc, char **argv) {
                 double dt = now() - t0;
                 if (dt < best) best = dt;
             }
-            printf("threads %2d %-14s %7.1f GB/s\n", th, mode == 0 ? "nt-zero" : mode == 1 ? "expand-nt" : "expand-store",
+            printf("threads %2d %-14s %7.1f GB/s\n", th,
+                   mode == 0 ? "nt-zero" : mode == 1 ? "expand-nt" : mode == 2 ? "expand-store" : "expand-nt512",
                    nf * 4 / best / 1e9);
         }
     }
