@@ -467,6 +467,8 @@ def main():
         pol["float32_obs_torch_f32"] = rollout_rate("float32", lambda m, shp: m)
         pol["float32_obs_torch_bf16"] = rollout_rate("float32", autocast_policy)
         pol["bits_obs_conv1_bits_bf16"] = rollout_rate("bits", lambda m, shp: PackedPolicy(m, shp, bf16=True))
+        pol["bits_obs_conv1_bits_bf16_nhwc"] = rollout_rate(
+            "bits", lambda m, shp: PackedPolicy(m, shp, bf16=True, channels_last=True))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -182,10 +182,11 @@ int lg_metrics(int domain, int max_h, int max_w, int64_t n, const uint8_t *tiles
  * ConvPolicy trunk (nets.py:150-183: Conv2d(C, K, 3) valid + ReLU) computed
  * straight from packed observation bits (LG_OBS_BITS layout, n_envs envs of
  * C x OH x OW elements). weight f32 [K][C][3][3], bias f32 [K] (device);
- * out [n_envs][K][OH-2][OW-2], float32 (out_bf16 = 0) or bfloat16 (1).
- * K <= 64 and a multiple of 4, C <= 16. Stream-ordered. */
+ * out [n_envs][K][OH-2][OW-2] (nhwc = 0) or [n_envs][OH-2][OW-2][K] (nhwc = 1,
+ * the channels-last layout), float32 (out_bf16 = 0) or bfloat16 (1).
+ * 1 <= K <= 64, C <= 16. Stream-ordered. */
 int lg_conv1_bits(const uint32_t *bits_dev, int64_t n_envs, int C, int OH, int OW, const float *weight_dev,
-                  const float *bias_dev, int K, void *out_dev, int out_bf16, int relu, void *stream);
+                  const float *bias_dev, int K, void *out_dev, int out_bf16, int relu, int nhwc, void *stream);
 
 /* Host SeedSequence(seed).spawn(offset+n)[offset+i] -> rng [n][6] (env.py:591-594). */
 int lg_seed_streams(uint64_t seed, int64_t offset, int64_t n, uint64_t *rng_host);

@@ -80,7 +80,7 @@ SIGNATURES = {
     "lg_host_threads": (ctypes.c_int, []),
     "lg_unpack_host": (ctypes.c_int, [_P, _I64, _P, ctypes.c_int]),
     "lg_conv1_bits": (ctypes.c_int, [_P, _I64, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, _P, ctypes.c_int,
-                                     _P, ctypes.c_int, ctypes.c_int, _P]),
+                                     _P, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P]),
 }
 
 _lib = None

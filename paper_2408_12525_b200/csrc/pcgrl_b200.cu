@@ -935,7 +935,7 @@ extern "C" int lg_unpack_host(const uint32_t *bits, int64_t n_elems, void *dst, 
 #endif
 template <int KC, bool BF16>
 static int launch_conv1(const uint32_t *bits, long long B, int C, int OH, int OW, const float *w,
-                        const float *bias, int K, void *out, int relu, size_t smem, cudaStream_t s) {
+                        const float *bias, int K, void *out, int relu, int nhwc, size_t smem, cudaStream_t s) {
     Conv1Div dv;
     fastdiv_init(dv.oo, (uint32_t)(OH * OW));
     fastdiv_init(dv.pw, (uint32_t)(OW - 2));
@@ -949,13 +949,13 @@ static int launch_conv1(const uint32_t *bits, long long B, int C, int OH, int OW
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, 256, smem));
     long long grid = (long long)sms * (per > 0 ? per : 1);
     if (grid * LG_CONV1_EB > B) grid = (B + LG_CONV1_EB - 1) / LG_CONV1_EB;
-    fn<<<(unsigned)grid, 256, smem, s>>>(bits, B, C, OH, OW, w, bias, K, out, relu, dv);
+    fn<<<(unsigned)grid, 256, smem, s>>>(bits, B, C, OH, OW, w, bias, K, out, relu, nhwc, dv);
     CU(cudaGetLastError());
     return LG_OK;
 }
 
 extern "C" int lg_conv1_bits(const uint32_t *bits, int64_t n_envs, int C, int OH, int OW, const float *weight,
-                             const float *bias, int K, void *out, int out_bf16, int relu, void *stream) {
+                             const float *bias, int K, void *out, int out_bf16, int relu, int nhwc, void *stream) {
     if (!bits || !weight || !bias || !out || n_envs < 1) {
         set_err("conv1_bits needs bits, weight, bias and output buffers and n_envs >= 1");
         return LG_EINVAL;
@@ -977,8 +977,8 @@ extern "C" int lg_conv1_bits(const uint32_t *bits, int64_t n_envs, int C, int OH
     cudaStream_t s = (cudaStream_t)stream;
     long long B = (long long)n_envs;
 #define LG_CONV1(KCV)                                                                                   \
-    return out_bf16 ? launch_conv1<KCV, true>(bits, B, C, OH, OW, weight, bias, K, out, relu, smem, s) \
-                    : launch_conv1<KCV, false>(bits, B, C, OH, OW, weight, bias, K, out, relu, smem, s)
+    return out_bf16 ? launch_conv1<KCV, true>(bits, B, C, OH, OW, weight, bias, K, out, relu, nhwc, smem, s) \
+                    : launch_conv1<KCV, false>(bits, B, C, OH, OW, weight, bias, K, out, relu, nhwc, smem, s)
     if (KCt == 4) LG_CONV1(4);
     if (KCt == 8) LG_CONV1(8);
     LG_CONV1(16);

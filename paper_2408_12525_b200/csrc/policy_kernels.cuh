@@ -31,7 +31,7 @@ template <int KC, bool BF16, int EB>
 __global__ void __launch_bounds__(256) conv1_bits_kernel(const uint32_t *__restrict__ bits, long long B, int C,
                                                          int OH, int OW, const float *__restrict__ w,
                                                          const float *__restrict__ bias, int K, void *out,
-                                                         int relu, const Conv1Div dv) {
+                                                         int relu, int nhwc, const Conv1Div dv) {
     extern __shared__ __align__(16) float csm[];
     constexpr int KP = 4 * KC;  // padded output channels per table row
     constexpr int RS = KP + 4;  // row stride (floats): rows land 20 banks apart, not 16
@@ -133,6 +133,65 @@ __global__ void __launch_bounds__(256) conv1_bits_kernel(const uint32_t *__restr
                         }
                     }
                 }
+            }
+            if (nhwc) {  // [env][px][k]: the pixel's K channels are contiguous (vector stores)
+                const size_t base = ((size_t)env * NP + px) * K;
+                if (BF16 && (K & 7) == 0) {
+                    uint4 *o = reinterpret_cast<uint4 *>(reinterpret_cast<__nv_bfloat16 *>(out) + base);
+#pragma unroll
+                    for (int q = 0; q + 1 < KC + 1; q += 2) {
+                        if (4 * q >= K) break;
+                        float v[8] = {acc[q].x, acc[q].y, acc[q].z, acc[q].w, 0.f, 0.f, 0.f, 0.f};
+                        if (q + 1 < KC) {
+                            v[4] = acc[q + 1].x;
+                            v[5] = acc[q + 1].y;
+                            v[6] = acc[q + 1].z;
+                            v[7] = acc[q + 1].w;
+                        }
+                        uint32_t wd[4];
+#pragma unroll
+                        for (int j = 0; j < 4; j++) {
+                            float a = v[2 * j], b = v[2 * j + 1];
+                            if (relu) {
+                                a = a > 0.f ? a : 0.f;
+                                b = b > 0.f ? b : 0.f;
+                            }
+                            __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+                            wd[j] = *reinterpret_cast<uint32_t *>(&h2);
+                        }
+                        o[q / 2] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+                    }
+                } else if (!BF16 && (K & 3) == 0) {
+                    float4 *o = reinterpret_cast<float4 *>(reinterpret_cast<float *>(out) + base);
+#pragma unroll
+                    for (int q = 0; q < KC; q++) {
+                        if (4 * q >= K) break;
+                        float4 v = acc[q];
+                        if (relu) {
+                            v.x = v.x > 0.f ? v.x : 0.f;
+                            v.y = v.y > 0.f ? v.y : 0.f;
+                            v.z = v.z > 0.f ? v.z : 0.f;
+                            v.w = v.w > 0.f ? v.w : 0.f;
+                        }
+                        o[q] = v;
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < KC; q++) {
+                        const float a4[4] = {acc[q].x, acc[q].y, acc[q].z, acc[q].w};
+#pragma unroll
+                        for (int j = 0; j < 4; j++) {
+                            const int k = 4 * q + j;
+                            if (k < K) {
+                                float v = a4[j];
+                                if (relu) v = v > 0.f ? v : 0.f;
+                                if (BF16) reinterpret_cast<__nv_bfloat16 *>(out)[base + k] = __float2bfloat16_rn(v);
+                                else reinterpret_cast<float *>(out)[base + k] = v;
+                            }
+                        }
+                    }
+                }
+                continue;
             }
             // [env][k][px]: one base per pixel, channel planes NP apart
             const size_t base = (size_t)env * K * NP + px;

@@ -125,10 +125,13 @@ def init_policy(arch: ArchConfig, seed: int):
     return make_policy(arch)
 
 
-def conv1_bits(bits, n_envs: int, obs_shape, weight, bias, *, out_dtype=None, relu: bool = True, out=None):
+def conv1_bits(bits, n_envs: int, obs_shape, weight, bias, *, out_dtype=None, relu: bool = True, out=None,
+               channels_last: bool = False):
     """relu(conv2d(obs, weight, bias)) (3x3, valid) from the packed stream of a
     ``BatchEnv(obs_dtype="bits")``; obs_shape = (C, OH, OW). Output
-    [n_envs, K, OH-2, OW-2] in float32 (default) or bfloat16."""
+    [n_envs, K, OH-2, OW-2] in float32 (default) or bfloat16; with
+    ``channels_last`` the same logical tensor in torch's channels-last layout
+    (the kernel then writes each pixel's K channels with vector stores)."""
     torch = _torch()
     C, OH, OW = (int(x) for x in obs_shape)
     K = int(weight.shape[0])
@@ -140,11 +143,15 @@ def conv1_bits(bits, n_envs: int, obs_shape, weight, bias, *, out_dtype=None, re
     w = weight.detach().to(torch.float32).contiguous()
     b = bias.detach().to(torch.float32).contiguous()
     if out is None:
-        out = torch.empty((n_envs, K, OH - 2, OW - 2), dtype=out_dtype, device=bits.device)
+        if channels_last:
+            out = torch.empty((n_envs, OH - 2, OW - 2, K), dtype=out_dtype, device=bits.device).permute(0, 3, 1, 2)
+        else:
+            out = torch.empty((n_envs, K, OH - 2, OW - 2), dtype=out_dtype, device=bits.device)
+    nhwc = int(out.dim() == 4 and out.stride(1) == 1 and K > 1)
     stream = ctypes.c_void_p(torch.cuda.current_stream(bits.device).cuda_stream)
     p = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
     _lib.check(_lib.load().lg_conv1_bits(p(bits), int(n_envs), C, OH, OW, p(w), p(b), K, p(out),
-                                         int(out_dtype == torch.bfloat16), int(relu), stream))
+                                         int(out_dtype == torch.bfloat16), int(relu), nhwc, stream))
     return out
 
 
@@ -153,19 +160,26 @@ class PackedPolicy:
     ReLU by ``lg_conv1_bits``, the rest of the trunk and both heads by the
     model's own torch modules (optionally under bf16 autocast)."""
 
-    def __init__(self, model, obs_shape, *, bf16: bool = False):
+    def __init__(self, model, obs_shape, *, bf16: bool = False, channels_last: bool = False):
         if not model.arch.conv_channels:
             raise ValueError("the packed path needs at least one conv layer")
         self.model = model
         self.obs_shape = tuple(obs_shape)
         self.bf16 = bf16
+        self.channels_last = channels_last
+        if channels_last:  # the rest of the conv trunk in NHWC: converts the model's conv weights in place
+            torch = _torch()
+            for m in model.trunk:
+                if isinstance(m, torch.nn.Conv2d):
+                    m.to(memory_format=torch.channels_last)
         self.conv1 = model.trunk[0]
         self.rest = model.trunk[2:]  # after Conv2d + ReLU
 
     def __call__(self, bits, n_envs: int):
         torch = _torch()
         h = conv1_bits(bits, n_envs, self.obs_shape, self.conv1.weight, self.conv1.bias,
-                       out_dtype=torch.bfloat16 if self.bf16 else torch.float32)
+                       out_dtype=torch.bfloat16 if self.bf16 else torch.float32,
+                       channels_last=self.channels_last)
         with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.bf16):
             h = self.rest(h)
             return self.model.policy_head(h).float(), self.model.value_head(h).squeeze(-1).float()

@@ -67,6 +67,11 @@ def test_conv1_bits_matches_conv2d(case, K):
     torch.testing.assert_close(got16.float(), want, rtol=1e-2, atol=1e-2)
     lin = conv1_bits(bits, n, shape, w, b, relu=False)
     torch.testing.assert_close(lin, lin64.float(), rtol=1e-5, atol=1e-5)
+    # channels-last output: the same tensor values, NHWC strides
+    cl = conv1_bits(bits, n, shape, w, b, channels_last=True)
+    assert cl.stride(1) == 1 and torch.equal(cl, got)
+    cl16 = conv1_bits(bits, n, shape, w, b, out_dtype=torch.bfloat16, channels_last=True)
+    assert torch.equal(cl16, got16)
 
 
 @pytest.fixture(autouse=True)
@@ -87,8 +92,11 @@ def test_packed_policy_matches_conv_policy():
     with torch.no_grad():
         l1, v1 = model(unpack_obs(bits, n, shape))
         l2, v2 = PackedPolicy(model, shape)(bits, n)
+        l3, v3 = PackedPolicy(model, shape, channels_last=True)(bits, n)
     torch.testing.assert_close(l2, l1, rtol=1e-4, atol=1e-5)
     torch.testing.assert_close(v2, v1, rtol=1e-4, atol=1e-5)
+    torch.testing.assert_close(l3, l1, rtol=1e-4, atol=1e-5)
+    torch.testing.assert_close(v3, v1, rtol=1e-4, atol=1e-5)
 
 
 @pytest.mark.parametrize("packed", [False, True])
