@@ -1037,6 +1037,9 @@ __device__ __forceinline__ void solo_env(const Params &p, int mode, long long en
     if (p.obs) solo_render<DOM>(p, st.e, img, stream, bit0, last);
 }
 
+#ifndef LG_EARLY_SPLIT
+#define LG_EARLY_SPLIT 4  // eighths of the warp's output stored before the recompute
+#endif
 #ifndef LG_DUNGEON_EARLY
 #define LG_DUNGEON_EARLY 0  // dungeon's warp kernel without the early-observation path (c3: spills)
 #endif
@@ -1094,7 +1097,8 @@ __device__ __forceinline__ void env_solo_body(const Params &p, int mode) {
         if (!__any_sync(0xffffffffu, valid && st.ends)) {
             if (valid) solo_render<DOM>(p, st.e, img, p.stream_mode != 0, (uint32_t)local * p.PE, local == nenv - 1);
             __syncwarp();
-            const uint32_t nv = (uint32_t)nenv * p.PE / 8, qm = (nv / 2) & ~127u;  // multiple of nthr * U
+            const uint32_t nv = (uint32_t)nenv * p.PE / 8;
+            const uint32_t qm = (uint32_t)((uint64_t)nv * LG_EARLY_SPLIT / 8) & ~127u;  // multiple of nthr * U
             if (p.stream_mode) solo_write_stream<8, 2>(p, grp, env0, nenv, wl, nthr, 0, qm);
             else solo_write_noctrl<LG_WRITER_U>(p, grp, env0, nenv, wl, nthr, 0, qm);
             if (valid) solo_finish<DOM>(p, mode, env, st, scratch);
