@@ -132,3 +132,22 @@ def test_collect_rollout_replays_through_the_env(packed):
         lp = torch.log_softmax(logits, -1).gather(1, batch.actions[0][:, None]).squeeze(1)
     torch.testing.assert_close(batch.logprobs[0], lp, rtol=1e-4, atol=1e-5)
     torch.testing.assert_close(batch.values[0], value, rtol=1e-4, atol=1e-5)
+
+
+@pytest.mark.parametrize("case", [0, 2, 4])
+def test_numpy_env_bits_format(case):
+    """NumpyBatchEnv(obs_dtype="bits") returns the packed stream itself (lg_step_host, no expansion)."""
+    from paper_2408_12525_b200.env import NumpyBatchEnv
+    kw, n = CASES[case]
+    n = min(n, 5000)
+    cfg = EnvConfig(**kw)
+    dev = BatchEnv(cfg, n, seed=8, validate=False, obs_dtype="bits")
+    host = NumpyBatchEnv(cfg, n, seed=8, obs_dtype="bits")
+    assert np.array_equal(dev.reset().cpu().numpy(), host.reset())
+    rng = np.random.default_rng(case)
+    for t in range(3):
+        a = rng.integers(0, cfg.n_actions, size=n)
+        o1, r1, _, _ = dev.step(torch.from_numpy(a).cuda())
+        o2, r2, _, _ = host.step(a)
+        assert o2.dtype == np.int32 and np.array_equal(o1.cpu().numpy(), o2), t
+        assert np.array_equal(r1.cpu().numpy(), r2), t
