@@ -930,26 +930,24 @@ extern "C" int lg_unpack_host(const uint32_t *bits, int64_t n_elems, void *dst, 
     return LG_OK;
 }
 
-#ifndef LG_CONV1_EB
-#define LG_CONV1_EB 4  // envs per block iteration in conv1_bits_kernel
-#endif
 template <int KC, bool BF16>
 static int launch_conv1(const uint32_t *bits, long long B, int C, int OH, int OW, const float *w,
-                        const float *bias, int K, void *out, int relu, int nhwc, size_t smem, cudaStream_t s) {
+                        const float *bias, int K, void *out, int relu, int nhwc, int EB, size_t smem,
+                        cudaStream_t s) {
     Conv1Div dv;
     fastdiv_init(dv.oo, (uint32_t)(OH * OW));
     fastdiv_init(dv.pw, (uint32_t)(OW - 2));
     fastdiv_init(dv.np, (uint32_t)((OH - 2) * (OW - 2)));
     fastdiv_init(dv.g, (uint32_t)((C + 3) / 4));
-    auto fn = conv1_bits_kernel<KC, BF16, LG_CONV1_EB>;
+    auto fn = conv1_bits_kernel<KC, BF16>;
     CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int dev = 0, sms = 0, per = 0;
     CU(cudaGetDevice(&dev));
     CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, 256, smem));
     long long grid = (long long)sms * (per > 0 ? per : 1);
-    if (grid * LG_CONV1_EB > B) grid = (B + LG_CONV1_EB - 1) / LG_CONV1_EB;
-    fn<<<(unsigned)grid, 256, smem, s>>>(bits, B, C, OH, OW, w, bias, K, out, relu, nhwc, dv);
+    if (grid * EB > B) grid = (B + EB - 1) / EB;
+    fn<<<(unsigned)grid, 256, smem, s>>>(bits, B, C, OH, OW, w, bias, K, out, relu, nhwc, EB, dv);
     CU(cudaGetLastError());
     return LG_OK;
 }
@@ -967,18 +965,25 @@ extern "C" int lg_conv1_bits(const uint32_t *bits, int64_t n_envs, int C, int OH
     const int KC = (K + 3) / 4, KCt = KC <= 4 ? 4 : KC <= 8 ? 8 : 16;
     const size_t G = (size_t)((C + 3) / 4);
     const size_t table = G * 10 * 16 * (4 * KCt + 4) * sizeof(float);  // 9 tap tables + their sum
-    const size_t masks = (LG_CONV1_EB * G * OH * OW + 15) & ~(size_t)15;
-    const size_t words = ((size_t)LG_CONV1_EB * C * OH * OW + 31) / 32 + 1;
-    const size_t smem = table + masks + words * 4;
-    if (smem > 200 * 1024) {
+    // envs per block iteration: 4 (fewer barriers, fuller rounds), fewer when
+    // four large observations (masks + bits) do not fit in shared memory
+    int EB = 4;
+    size_t smem = 0;
+    for (; EB >= 1; EB /= 2) {
+        const size_t masks = ((size_t)EB * G * OH * OW + 15) & ~(size_t)15;
+        const size_t words = ((size_t)EB * C * OH * OW + 31) / 32 + 1;
+        smem = table + masks + words * 4;
+        if (smem <= 200 * 1024) break;
+    }
+    if (EB < 1) {
         set_err("conv1_bits: tables + one observation exceed shared memory (%zu bytes)", smem);
         return LG_EINVAL;
     }
     cudaStream_t s = (cudaStream_t)stream;
     long long B = (long long)n_envs;
 #define LG_CONV1(KCV)                                                                                   \
-    return out_bf16 ? launch_conv1<KCV, true>(bits, B, C, OH, OW, weight, bias, K, out, relu, nhwc, smem, s) \
-                    : launch_conv1<KCV, false>(bits, B, C, OH, OW, weight, bias, K, out, relu, nhwc, smem, s)
+    return out_bf16 ? launch_conv1<KCV, true>(bits, B, C, OH, OW, weight, bias, K, out, relu, nhwc, EB, smem, s) \
+                    : launch_conv1<KCV, false>(bits, B, C, OH, OW, weight, bias, K, out, relu, nhwc, EB, smem, s)
     if (KCt == 4) LG_CONV1(4);
     if (KCt == 8) LG_CONV1(8);
     LG_CONV1(16);

@@ -27,11 +27,11 @@ struct Conv1Div {  // runtime divisors of the index math (mul-hi + shift)
 // cells all carry the same channel mask -- the border around the map in an
 // egocentric window -- is one lookup instead of nine), the env's channel
 // mask per cell and group (bytes), and the env's bits.
-template <int KC, bool BF16, int EB>
+template <int KC, bool BF16>
 __global__ void __launch_bounds__(256) conv1_bits_kernel(const uint32_t *__restrict__ bits, long long B, int C,
                                                          int OH, int OW, const float *__restrict__ w,
                                                          const float *__restrict__ bias, int K, void *out,
-                                                         int relu, int nhwc, const Conv1Div dv) {
+                                                         int relu, int nhwc, int EB, const Conv1Div dv) {
     extern __shared__ __align__(16) float csm[];
     constexpr int KP = 4 * KC;  // padded output channels per table row
     constexpr int RS = KP + 4;  // row stride (floats): rows land 20 banks apart, not 16

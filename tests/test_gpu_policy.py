@@ -151,3 +151,25 @@ def test_numpy_env_bits_format(case):
         o2, r2, _, _ = host.step(a)
         assert o2.dtype == np.int32 and np.array_equal(o1.cpu().numpy(), o2), t
         assert np.array_equal(r1.cpu().numpy(), r2), t
+
+
+def test_conv1_bits_large_window_and_bad_arguments():
+    """A 64x64 dungeon window of 96 (C=8): four observations' masks + bits do not
+    fit in shared memory, so the kernel takes fewer envs per iteration."""
+    from paper_2408_12525_b200 import _lib
+    cfg = EnvConfig(domain="dungeon", max_width=64, max_height=64, obs_size=95)
+    n = 40
+    env = BatchEnv(cfg, n, seed=2, validate=False, obs_dtype="bits")
+    bits = env.reset()
+    shape = env.observation_shape
+    obs = unpack_obs(bits, n, shape)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    w = torch.randn((16, shape[0], 3, 3), device="cuda", generator=g)
+    b = torch.randn(16, device="cuda", generator=g)
+    want = F.relu(F.conv2d(obs.double(), w.double(), b.double())).float()
+    torch.testing.assert_close(conv1_bits(bits, n, shape, w, b), want, rtol=1e-5, atol=1e-5)
+    with pytest.raises(ValueError):
+        conv1_bits(bits, n, shape, torch.zeros((65, shape[0], 3, 3), device="cuda"), torch.zeros(65, device="cuda"))
+    with pytest.raises(ValueError):
+        _lib.check(_lib.load().lg_conv1_bits(None, n, shape[0], shape[1], shape[2], None, None, 16, None, 0, 1, 0,
+                                             None))
