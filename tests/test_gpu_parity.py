@@ -506,3 +506,35 @@ def test_packed_and_float32_copy_paths_agree(monkeypatch):
             off = (4 - raw.ctypes.data) % 16
             b._bufs["obs"] = raw[off:off + o2.nbytes].view(np.float32).reshape(o2.shape)
             assert b._bufs["obs"].ctypes.data % 16 == 4
+
+
+@pytest.mark.parametrize("domain,side,pins", [
+    ("maze", 48, ("player", "door")),
+    ("dungeon", 40, ("player", "key", "door")),
+    ("maze", 16, ("player", "door")),  # lane team of 16 (forced below)
+])
+def test_lane_team_first_touch_depths(domain, side, pins, monkeypatch):
+    """bfs_touch advances two BFS layers per round of team votes and resolves
+    the touched layer afterwards (repo:paper_2408_12525_b200/csrc/team.cuh):
+    path lengths of both parities, endpoint legs (dungeon) and unreachable
+    flags must equal the oracle's (problems.py:176-243) on every step."""
+    monkeypatch.setenv("LG_FORCE_TEAM", "1")
+    cfg = EnvConfig(domain=domain, max_width=side, max_height=side, obs_size=9, pinpoints=pins)
+    n = 128
+    env = BatchEnv(cfg, n, seed=3)
+    ref = O.OracleBatchEnv(cfg, n, seed=3)
+    assert np.array_equal(_np(env.reset()), ref.reset())
+    act = np.random.default_rng(5)
+    seen = set()
+    for t in range(20):
+        a = act.integers(0, cfg.n_actions, size=n)
+        o2, r2, d2, _ = ref.step(a)
+        o1, r1, d1, _ = env.step(a)
+        assert np.array_equal(_np(r1), r2), t
+        assert np.array_equal(_np(d1), d2), t
+        assert np.array_equal(_np(o1), o2), t
+        s1, s2 = env.state_dict(), ref.state_dict()
+        assert np.array_equal(s1["values"], s2["values"]), t
+        assert np.array_equal(s1["unreach"], s2["unreach"]), t
+        seen.update(int(v) % 2 for v in s2["values"][0] if v > 0)
+    assert seen == {0, 1}  # touched at even and at odd depths
