@@ -666,8 +666,17 @@ __device__ __forceinline__ uint64_t window_bits64(uint64_t gridrow, int c0, uint
     return win;
 }
 
+// A/B knobs for the team kernel's code size (instruction-cache pressure on
+// 64x64 maps): default keeps the renderer inlined and leaves the writers to nvcc.
+#ifndef LG_TEAM_RENDER_ATTR
+#define LG_TEAM_RENDER_ATTR __forceinline__
+#endif
+#ifndef LG_TEAM_WRITER_ATTR
+#define LG_TEAM_WRITER_ATTR
+#endif
+
 template <class G, int DOM>
-__device__ __forceinline__ void render_env(const Params &p, const Team<G> &t, const EnvRegs<G, DOM> &e,
+__device__ LG_TEAM_RENDER_ATTR void render_env(const Params &p, const Team<G> &t, const EnvRegs<G, DOM> &e,
                            unsigned char *es) {
     using Row = typename G::Row;
     constexpr int N = Dom<DOM>::N, NPL = Dom<DOM>::NPL;
@@ -758,7 +767,7 @@ __device__ __forceinline__ uint32_t bits_to_bytes4(uint32_t x) { return ((x & 0x
 
 // uint8 observation (opt-in, no control planes): 16 elements per 16-byte store.
 template <class G>
-__device__ void write_obs_team_u8(const Params &p, const Team<G> &t, long long env, const unsigned char *es) {
+__device__ LG_TEAM_WRITER_ATTR void write_obs_team_u8(const Params &p, const Team<G> &t, long long env, const unsigned char *es) {
     const uint32_t *img = reinterpret_cast<const uint32_t *>(es);
     const size_t base = (size_t)env * p.PE;
     uint8_t *out = reinterpret_cast<uint8_t *>(p.obs) + base;
@@ -781,7 +790,7 @@ __device__ void write_obs_team_u8(const Params &p, const Team<G> &t, long long e
 // [env*PE, env*PE + PE); words shared with a neighbouring env are OR-ed into
 // the zeroed stream, the ends of the batch are stored.
 template <class G>
-__device__ void write_obs_team_bits(const Params &p, const Team<G> &t, long long env, const unsigned char *es) {
+__device__ LG_TEAM_WRITER_ATTR void write_obs_team_bits(const Params &p, const Team<G> &t, long long env, const unsigned char *es) {
     const uint32_t *img = reinterpret_cast<const uint32_t *>(es);
     uint32_t *out = reinterpret_cast<uint32_t *>(p.obs);
     const uint32_t PE = p.PE;
@@ -807,7 +816,7 @@ __device__ void write_obs_team_bits(const Params &p, const Team<G> &t, long long
 }
 
 template <class G>
-__device__ void write_obs_team(const Params &p, const Team<G> &t, long long env, const unsigned char *es) {
+__device__ LG_TEAM_WRITER_ATTR void write_obs_team(const Params &p, const Team<G> &t, long long env, const unsigned char *es) {
     const uint32_t *img = reinterpret_cast<const uint32_t *>(es);
     const size_t base = (size_t)env * p.PE;
     float *out = p.obs + base;
