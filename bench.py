@@ -130,6 +130,45 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def rank_cpu_slice(local_rank: int, local_world: int, torch, dev):
+    """The host cores this rank should use: its share of the cores of its
+    GPU's NUMA node (ranks on the same node split them), else its share of
+    the process's allowed cores. Returns a sorted list of cpu ids."""
+    allowed = sorted(os.sched_getaffinity(0))
+    if local_world <= 1:
+        return allowed
+
+    def node_of(i):
+        try:
+            pr = torch.cuda.get_device_properties(i)
+            bus = f"{pr.pci_domain_id:04x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            with open(f"/sys/bus/pci/devices/{bus}/numa_node") as f:
+                return int(f.read())
+        except Exception:
+            return -1
+
+    def cpulist(node):
+        cpus = set()
+        try:
+            with open(f"/sys/devices/system/node/node{node}/cpulist") as f:
+                for part in f.read().strip().split(","):
+                    a, _, b = part.partition("-")
+                    cpus.update(range(int(a), int(b or a) + 1))
+        except Exception:
+            return []
+        return sorted(cpus & set(allowed))
+
+    nodes = [node_of(i) for i in range(min(local_world, torch.cuda.device_count()))]
+    mine = nodes[local_rank] if local_rank < len(nodes) else -1
+    pool = cpulist(mine) if mine >= 0 else []
+    peers = [i for i, n in enumerate(nodes) if n == mine] if pool else list(range(local_world))
+    if not pool:
+        pool = allowed
+    k = max(1, len(pool) // max(1, len(peers)))
+    j = peers.index(local_rank) if local_rank in peers else local_rank
+    return pool[j * k:(j + 1) * k] or pool
+
+
 def cpu_oracle_run(cfg, n_envs: int, steps: int, warmup: int, threads: int):
     """Time the CPU oracle (reference algorithm, C port) on the host cores."""
     import numpy as np
@@ -188,6 +227,11 @@ def main():
     ap.add_argument("--no-u8", action="store_true", help="skip the opt-in uint8-observation side run")
     ap.add_argument("--no-policy", action="store_true", help="skip the policy-rollout side run")
     ap.add_argument("--no-graph", action="store_true", help="time only the eager launch loop")
+    ap.add_argument("--burn-in", type=int, default=-1,
+                    help="untimed steps after warm-up (default: one full episode, 3*h*w)")
+    ap.add_argument("--stats-every", type=int, default=10,
+                    help="episode-stats all-reduce every S timed steps on a side stream (N > 1)")
+    ap.add_argument("--no-proxy", action="store_true", help="skip the single-GPU scaling proxy")
     ap.add_argument("--policy-envs", type=int, default=65536)
     ap.add_argument("--policy-steps", type=int, default=8)
     args = ap.parse_args()
@@ -214,12 +258,28 @@ def main():
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    if world > 1:
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    all_cpus = sorted(os.sched_getaffinity(0))
+    cpus = rank_cpu_slice(local_rank, local_world, torch, dev)
+    if local_world > 1:
+        # each rank expands its own observations on its own cores (no
+        # oversubscription: 8 ranks x all cores would thrash the host)
+        try:
+            os.sched_setaffinity(0, cpus)
+        except Exception:
+            pass
+        os.environ.setdefault("LG_HOST_THREADS", str(len(cpus)))
+    distributed = world > 1 or "TORCHELASTIC_RUN_ID" in os.environ or "MASTER_ADDR" in os.environ
+    if distributed:
+        # communicator setup is logged (stderr) so the rank count can be checked
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=dev)
     from paper_2408_12525_b200 import _lib
     from paper_2408_12525_b200.env import INFO_KEYS, BatchEnv, NumpyBatchEnv
 
-    from paper_2408_12525_b200.sharding import EpisodeStats, max_over_ranks, shard
+    from paper_2408_12525_b200.sharding import STAT_NAMES, EpisodeStats, max_over_ranks, shard
     offset, B = shard(global_b, world, rank)
     env = BatchEnv(cfg, B, seed=0, device=dev, global_offset=offset, validate=False)
     obs = env.new_obs()
@@ -238,7 +298,36 @@ def main():
 
     for i in range(args.warmup):
         one_step(i)
+    # Burn-in (untimed): run one full episode past warm-up, so the timed
+    # window is steady state with every env's first auto-reset behind it.
+    # Lockstep configs (fixed shape, no change budget: c1/c2/c4/c5) reset all
+    # envs on the same step, L = 3*h*w; that step's cost is timed here and
+    # reported as episode_boundary.
+    H, W = cfg.max_height, cfg.max_width
+    ep_len = int(cfg.max_steps or 3 * H * W)
+    burn = args.burn_in if args.burn_in >= 0 else ep_len
+    lockstep = not cfg.randomize_shape and not cfg.change_budget
+    bev = []
+    for i in range(burn):
+        j = args.warmup + i
+        if lockstep:
+            bev.append((j + 1, torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)))
+            bev[-1][1].record(stream)
+        one_step(j)
+        if lockstep:
+            bev[-1][2].record(stream)
     torch.cuda.synchronize()
+    boundary = None
+    if lockstep and bev:
+        times = {k: a.elapsed_time(b) for k, a, b in bev}
+        if ep_len in times:
+            steady = statistics.median(v for k, v in times.items() if k % ep_len)
+            t_reset = times[ep_len]
+            boundary = {"step": ep_len, "reset_step_ms": t_reset, "steady_step_ms": steady,
+                        "amortized_value": global_b * ep_len / (((ep_len - 1) * steady + t_reset) / 1e3),
+                        "note": "every env of the lockstep batch auto-resets on step 3*h*w; "
+                                "amortized = one episode cycle of L-1 steady steps + the reset step"}
+    t0_step = args.warmup + burn
     if world > 1:
         dist.barrier()
     clk = ClockSampler(local_rank)
@@ -250,16 +339,36 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    # N > 1: the episode counters are all-reduced every S steps on a side
+    # stream (NCCL over NVLink), off the step's critical path
+    side = torch.cuda.Stream(dev) if world > 1 else None
+    snap = torch.zeros_like(stats)
+    red_ev = []
     t_start.record(stream)
     for i in range(K):
-        env.random_actions(1_000_003 * (i + args.warmup) + 17, out=acts)
+        env.random_actions(1_000_003 * (i + t0_step) + 17, out=acts)
         ev[i][0].record(stream)
         env.step_raw(acts, obs, reward, done, info, stats)
         ev[i][1].record(stream)
+        if side is not None and (i + 1) % args.stats_every == 0:
+            side.wait_stream(stream)
+            with torch.cuda.stream(side):
+                r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                snap.copy_(stats)
+                r0.record(side)
+                dist.all_reduce(snap)
+                r1.record(side)
+                red_ev.append((r0, r1))
     t_end.record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    reduce_info = None
+    if red_ev:
+        rms = [a.elapsed_time(b) for a, b in red_ev]
+        reduce_info = {"every_steps": args.stats_every, "count": len(rms), "mean_ms": sum(rms) / len(rms),
+                       "max_ms": max(rms), "stream": "side (overlaps the step kernels)",
+                       "global_episodes_seen": float(snap[0])}
     elapsed_ms = t_start.elapsed_time(t_end)
     step_ms = sum(a.elapsed_time(b) for a, b in ev) / K
     elapsed_ms = max_over_ranks(elapsed_ms, dev)
@@ -271,7 +380,7 @@ def main():
         # once in a CUDA graph and replayed: no per-launch CPU gaps, which
         # matter for the small configs (c1: 64 envs, ~30 us kernels)
         g = torch.cuda.CUDAGraph()
-        base = args.warmup + K
+        base = t0_step + K
         with torch.cuda.graph(g):
             for i in range(K):
                 env.random_actions(1_000_003 * (base + i) + 17, out=acts)
@@ -286,15 +395,19 @@ def main():
         g1.record(stream)
         torch.cuda.synchronize()
         graph_ms = max_over_ranks(g0.elapsed_time(g1), dev)
-        elapsed_ms = min(elapsed_ms, graph_ms)
+        if world == 1:  # N > 1: the eager loop carries the stats all-reduce; it is the value
+            elapsed_ms = min(elapsed_ms, graph_ms)
     clocks = clk.stop()
     ep_stats.all_reduce()  # the episode-stats reduce (NCCL over NVLink when N > 1)
+    stats_host = [float(x) for x in stats.cpu()]
     errs = env.errors()
     if errs:
         raise SystemExit(f"device error flags {errs}")
     value = global_b * K / (elapsed_ms / 1e3)
 
-    bytes_step = algorithmic_bytes_per_env_step(env.observation_shape)
+    obs_shape = env.observation_shape
+    team = env._desc.team
+    bytes_step = algorithmic_bytes_per_env_step(obs_shape)
     peak, peak_kind = load_peaks()
     achieved_gbs = B * bytes_step / (step_ms / 1e3) / 1e9
 
@@ -305,13 +418,17 @@ def main():
     # (lg_step_host); LG_HOST_EXPAND=0 gives the plain float32 copy for contrast.
     import numpy as np
 
-    def e2e_run(obs_dtype: str, packed: bool):
+    def e2e_run(obs_dtype: str, packed: bool, fresh: bool = False):
         if packed:
             os.environ.pop("LG_HOST_EXPAND", None)  # the library's default choice
         else:
             os.environ["LG_HOST_EXPAND"] = "0"
         torch.cuda.empty_cache()
-        nenv = NumpyBatchEnv(cfg, B, seed=0, device=dev, global_offset=offset, pinned=True, copy=False,
+        # fresh=False: pinned output arrays reused across steps (the caller
+        # copies what it keeps, as ppo.collect_rollout does, ppo.py:131);
+        # fresh=True: new pageable numpy arrays every step, the reference's
+        # ownership contract (env.py:233)
+        nenv = NumpyBatchEnv(cfg, B, seed=0, device=dev, global_offset=offset, pinned=not fresh, copy=fresh,
                              obs_dtype=obs_dtype)
         nenv.reset()
         rng = np.random.default_rng(1)
@@ -322,6 +439,8 @@ def main():
         per = time.perf_counter() - t0
         # at least e2e_steps steps and ~0.3 s of them (small batches are microseconds per step)
         n_steps = max(args.e2e_steps, min(500, int(0.5 / max(per, 1e-6))))
+        if fresh and per > 0.5:
+            n_steps = 3
         if world > 1:
             n_steps = int(max_over_ranks(float(n_steps), dev))
         host_acts = [rng.integers(0, cfg.n_actions, size=B) for _ in range(n_steps)]
@@ -342,7 +461,9 @@ def main():
         out = {"value": global_b * n_steps / dt, "unit": UNIT,
                "h2d_bytes_per_step": B * 8, "d2h_bytes_per_step": d2h, "steps": n_steps,
                "pcie_d2h_gbs": d2h * n_steps / dt / 1e9,
-               "api": "NumpyBatchEnv.step -> lg_step_host (pinned)"}
+               "api": "NumpyBatchEnv.step -> lg_step_host " +
+                      ("(fresh pageable arrays every step, copy=True)" if fresh else
+                       "(pinned arrays reused across steps, copy=False)")}
         if use_packed:
             out["transfer"] = (f"packed 0/1 bit planes D2H, expanded to {obs_dtype} in the caller's array "
                                f"by {_lib.load().lg_host_threads()} host threads (non-temporal stores)")
@@ -355,6 +476,7 @@ def main():
         del obs
         e2e = e2e_run("float32", True)
         e2e["float32_copy"] = e2e_run("float32", False)
+        e2e["fresh_arrays"] = e2e_run("float32", True, fresh=True)
 
     # Side measurement (does not change the headline): the same workload with
     # the opt-in uint8 observation format (4x fewer bytes per env-step).
@@ -470,9 +592,54 @@ def main():
         pol["bits_obs_conv1_bits_bf16_nhwc"] = rollout_rate(
             "bits", lambda m, shp: PackedPolicy(m, shp, bf16=True, channels_last=True))
 
+    # Single-GPU proxy of the strong-scaling sweep (c5): the per-GPU shard of
+    # 2^20 envs at N = 2, 4, 8 run alone on this GPU (graph replay of K steps).
+    proxy = None
+    if world == 1 and not args.no_proxy and args.config == "c5":
+        del env
+        torch.cuda.empty_cache()
+        proxy = {"note": "per-GPU rate of the N-GPU shard, measured on one B200; "
+                         "projected speed-up = N * rate(shard) / value"}
+        for n_gpu in (2, 4, 8):
+            Bs = global_b // n_gpu
+            pe = BatchEnv(cfg, Bs, seed=0, device=dev, validate=False)
+            po = pe.new_obs()
+            pa = torch.empty(Bs, dtype=torch.int64, device=dev)
+            pr = torch.empty(Bs, dtype=torch.float64, device=dev)
+            pd = torch.empty(Bs, dtype=torch.bool, device=dev)
+            pe.reset(out=po)
+            for i in range(args.warmup):
+                pe.random_actions(i, out=pa)
+                pe.step_raw(pa, po, pr, pd)
+            gp = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gp):
+                for i in range(K):
+                    pe.random_actions(100 + i, out=pa)
+                    pe.step_raw(pa, po, pr, pd)
+            gp.replay()
+            torch.cuda.synchronize()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            gp.replay()
+            g1.record(stream)
+            torch.cuda.synchronize()
+            rate = Bs * K / (g0.elapsed_time(g1) / 1e3)
+            proxy[f"n{n_gpu}"] = {"envs_per_gpu": Bs, "per_gpu_value": rate,
+                                  "projected_speedup": n_gpu * rate / value}
+            del gp, pe, po, pa, pr, pd
+            torch.cuda.empty_cache()
+
+    if distributed:
+        dist.barrier()
+        dist.destroy_process_group()
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
+    if rank == 0 and not args.no_cpu_baseline:
+        # the oracle on all of the host's cores (rank 0, after the GPU work)
+        try:
+            os.sched_setaffinity(0, all_cpus)
+        except Exception:
+            pass
+        threads = len(all_cpus)
         n_cpu = args.cpu_envs or min(global_b, 65536)
         # size the sample to roughly cpu-seconds of work
         v0, dt0 = cpu_oracle_run(cfg, n_cpu, 2, 1, threads)
@@ -490,16 +657,15 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "u8/int32/f64 (obs f32)",
             "data": "synthetic (device uniform random actions; env streams SeedSequence(0).spawn)",
             "config": {"workload": workload, "config": args.config, "global_envs": global_b,
-                       "envs_per_gpu": B, "obs_shape": list(env.observation_shape),
-                       "parallelism": f"env-sharded x{world}",
+                       "envs_per_gpu": B, "obs_shape": list(obs_shape),
+                       "parallelism": f"env-sharded x{world}", "burn_in_steps": burn,
                        "l2": "no flush: per-step obs output (%.1f GB) >> 126 MB L2" %
-                             (B * 4 * env.observation_shape[0] * env.observation_shape[1] *
-                              env.observation_shape[2] / 1e9)},
+                             (B * 4 * obs_shape[0] * obs_shape[1] * obs_shape[2] / 1e9)},
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
                          "frac": achieved_gbs / peak, "traffic": load_traffic(args.config),
                          "peak_kind": peak_kind, "frac_of_8000_nominal": achieved_gbs / 8000.0,
-                         "kernel": (f"env_solo_kernel_{cfg.domain}" if env._desc.team == 1 else
-                                    f"env_kernel<team {env._desc.team}, {cfg.domain}>") + " (fused step + obs)",
+                         "kernel": (f"env_solo_kernel_{cfg.domain}" if team == 1 else
+                                    f"env_kernel<team {team}, {cfg.domain}>") + " (fused step + obs)",
                          "bytes_per_env_step": bytes_step, "step_kernel_ms": step_ms},
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -512,11 +678,14 @@ def main():
             "obs_uint8": u8,
             "policy_rollout": pol,
             "clocks": clocks,
-            "episode_stats": [float(x) for x in stats.cpu()],
+            "episode_stats": dict(zip(STAT_NAMES, stats_host)),
+            "episode_boundary": boundary,
+            "stats_all_reduce": reduce_info,
+            "scaling_proxy": proxy,
+            "host": {"cpus_used_by_rank0": len(cpus), "local_world": local_world,
+                     "comm": f"nccl x{world}" if distributed else "none"},
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -133,6 +133,11 @@ int lg_step(lg_env *env, const int64_t *actions_dev, void *obs_dev, double *rewa
 /* lg_step with flags: LG_STEP_NO_AUTO_RESET leaves finished envs as they are
  * (the scalar facade's _Core.step(auto_reset=False), env.py:611-630). */
 #define LG_STEP_NO_AUTO_RESET 1u
+/* LG_STEP_VALIDATE: check every action id on device first; if one is out of
+ * range, LG_FLAG_BAD_ACTION is raised and the step kernel returns without
+ * touching any env (the reference validates before mutating, env.py:358-361).
+ * Read the verdict with lg_errors (one 4-byte read, the call's only sync). */
+#define LG_STEP_VALIDATE 2u
 int lg_step_flags(lg_env *env, const int64_t *actions_dev, void *obs_dev, double *reward_dev,
                   uint8_t *done_dev, const lg_info *info, double *stats_dev, uint32_t flags, void *stream);
 /* BatchEnv.observe (env.py:587-588). */

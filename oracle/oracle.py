@@ -320,6 +320,13 @@ class OracleBatchEnv:
                              *[_ptr(x) for x in bufs], 1))
         return bufs
 
+    def step_no_obs_info(self, actions):
+        """step() without the observation: (reward, done, info) (parity helper)."""
+        rw, dn, tm, er, el, es, fl = self.step_no_obs(actions)
+        info = {"terminal": tm.astype(bool), "episode_reward": er, "episode_length": el,
+                "episode_start_loss": es, "final_loss": fl}
+        return rw, dn.astype(bool), info
+
     def observe(self, out: np.ndarray | None = None) -> np.ndarray:
         if out is None:
             out = np.empty((self.n_envs,) + self.observation_shape, dtype=np.float32)

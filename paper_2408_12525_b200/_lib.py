@@ -14,6 +14,7 @@ LIB_PATH = os.environ.get("LG_LIB_PATH") or os.path.join(_PKG, "libpcgrl_b200.so
 LG_OK, LG_EINVAL, LG_ECUDA = 0, 1, 2
 FLAG_BAD_ACTION, FLAG_NO_EDITABLE, FLAG_PINPOINTS = 1, 2, 4
 STEP_NO_AUTO_RESET = 1
+STEP_VALIDATE = 2
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64

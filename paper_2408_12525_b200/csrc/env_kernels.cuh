@@ -117,7 +117,17 @@ struct Params {
     unsigned *aux;  // [1] device flag: an imported env has an active frozen cell
     int early;      // solo warp mode: render + store half the outputs before the recompute
     int coop;       // solo block mode: the warp renders its envs' images together
+    int gate;       // validated step (LG_STEP_VALIDATE): skip the launch when the action
+                    // check kernel flagged an out-of-range action (no mutation, env.py:358-361)
 };
+
+// Validated steps: the reference rejects a bad action batch before mutating
+// anything (env.py:358-361). check_actions_kernel runs first on the stream;
+// every thread of the step kernel then reads the same flag word and the whole
+// launch returns before touching state.
+__device__ __forceinline__ bool gate_closed(const Params &p) {
+    return p.gate && (*reinterpret_cast<volatile const unsigned *>(p.err) & FLAG_BAD_ACTION);
+}
 
 __device__ __forceinline__ void rng_load(const Params &p, long long env, Pcg &g) {
     const ulonglong2 s = p.rs[2 * env], b = p.rs[2 * env + 1], inc = p.ri[env];
@@ -861,6 +871,7 @@ __global__ void __launch_bounds__(64, G::MINB) env_kernel(const Params p, int mo
     const long long env = (long long)blockIdx.x * E + ti;
     unsigned char *es = smem + (size_t)ti * p.env_smem;
     uint16_t *uf = reinterpret_cast<uint16_t *>(es);  // aliases the bit image (phases differ)
+    if (gate_closed(p)) return;
 
     if (env < p.B) {
         EnvRegs<G, DOM> e;
@@ -948,6 +959,7 @@ __global__ void __launch_bounds__(64, G::MINB) env_kernel(const Params p, int mo
                 } else {
                     nxt = serp_next(t, ed, e.pr, e.pc);
                 }
+                nxt = max(nxt, 0);  // no editable cell left (imported state): stay well-formed
                 e.pos_idx = nidx;
                 e.pr = nxt >> 6;
                 e.pc = nxt & 63;

@@ -13,6 +13,7 @@
 #include <functional>
 #include <mutex>
 #include <thread>
+#include <sched.h>
 #include <vector>
 
 namespace lg_host {
@@ -127,7 +128,12 @@ class Pool {
 Pool &pool() {
     // leaked on purpose: worker threads outlive static destruction at exit
     static Pool *p = [] {
+        // one worker per core this process may run on (a multi-GPU launcher
+        // gives each rank its own slice of the host's cores), LG_HOST_THREADS overrides
         int n = (int)std::thread::hardware_concurrency();
+        cpu_set_t cs;
+        CPU_ZERO(&cs);
+        if (sched_getaffinity(0, sizeof cs, &cs) == 0 && CPU_COUNT(&cs) > 0) n = CPU_COUNT(&cs);
         if (const char *v = std::getenv("LG_HOST_THREADS")) n = std::atoi(v);
         if (n < 1) n = 1;
         if (n > 256) n = 256;

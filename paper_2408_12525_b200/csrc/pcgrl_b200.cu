@@ -7,6 +7,8 @@
 
 #include <mutex>
 #include <new>
+#include <set>
+#include <utility>
 #include <vector>
 
 #include "../../include/pcgrl_b200.h"
@@ -36,6 +38,40 @@ extern "C" const char *lg_version(void) { return "pcgrl_b200 0.1 sm_100a"; }
         }                                                                  \
     } while (0)
 
+// Switches to the env's device for the duration of a call and restores the
+// caller's current device afterwards (a library call must not leave the
+// process on another GPU).
+struct DeviceGuard {
+    int prev = -1;
+    cudaError_t err = cudaSuccess;
+    explicit DeviceGuard(int dev) {
+        err = cudaGetDevice(&prev);
+        if (err == cudaSuccess && prev != dev) err = cudaSetDevice(dev);
+        else if (err == cudaSuccess) prev = -1;  // already current: nothing to restore
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+#define DEVICE_GUARD(dev)       \
+    DeviceGuard _dg(dev);       \
+    CU(_dg.err)
+
+// The dynamic shared memory limit is a per-device function attribute: raise it
+// once per (kernel, device) pair, on the current device.
+static cudaError_t smem_attr(const void *fn, int bytes = 200 * 1024) {
+    static std::mutex mu;
+    static std::set<std::pair<const void *, int>> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> g(mu);
+    if (done.count({fn, dev})) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.insert({fn, dev});
+    return e;
+}
+
 // ---------------------------------------------------------------------------
 // auxiliary kernels
 // ---------------------------------------------------------------------------
@@ -64,6 +100,17 @@ __global__ void random_actions_kernel(long long B, long long goffset, unsigned l
     if (b >= B) return;
     uint64_t x = splitmix64(seed * 0xD1B54A32D192ED03ULL ^ splitmix64((uint64_t)(goffset + b)));
     out[b] = (long long)(((unsigned __int128)x * (unsigned long long)n_actions) >> 64);
+}
+
+// Validated steps (env.py:358-361): flags an out-of-range action before the
+// step kernel runs; the step kernel (Params::gate) then returns untouched.
+__global__ void check_actions_kernel(long long B, const long long *a, long long n_actions, unsigned *err) {
+    bool bad = false;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < B; i += (long long)gridDim.x * blockDim.x) {
+        const long long v = a[i];
+        bad |= v < 0 || v >= n_actions;
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, (unsigned)FLAG_BAD_ACTION);
 }
 
 // state_dict export (env.py:535-559), team per env
@@ -330,13 +377,7 @@ static int dom_m(int d) { return d == 0 ? 2 : d == 1 ? 4 : 7; }
 
 template <class G, int DOM>
 static int launch_env_t(lg_env *e, const Params &p, int mode, cudaStream_t s) {
-    static std::once_flag once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(once, [] {
-        attr_err = cudaFuncSetAttribute(env_kernel<G, DOM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        200 * 1024);
-    });
-    CU(attr_err);
+    CU(smem_attr((const void *)env_kernel<G, DOM>));
     int E = e->threads / G::TEAM;
     long long grid = (e->B + E - 1) / E;
     Params q = p;
@@ -349,16 +390,8 @@ static int launch_env_t(lg_env *e, const Params &p, int mode, cudaStream_t s) {
 
 template <int DOM>
 static int launch_solo_t(lg_env *e, const Params &p, int mode, cudaStream_t s) {
-    static std::once_flag once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(once, [] {
-        attr_err = cudaFuncSetAttribute(SoloKernel<DOM>::fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        200 * 1024);
-        if (attr_err == cudaSuccess)
-            attr_err = cudaFuncSetAttribute(SoloKernel<DOM>::fn_small,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    });
-    CU(attr_err);
+    CU(smem_attr((const void *)SoloKernel<DOM>::fn));
+    CU(smem_attr((const void *)SoloKernel<DOM>::fn_small));
     long long grid = (e->B + e->E - 1) / e->E;
     Params q = p;
     size_t smem = e->smem;
@@ -498,7 +531,7 @@ extern "C" int lg_create(const lg_config *cfg, int64_t n_envs, int64_t global_of
         set_err("at most 2^31-1 environments per device");
         return LG_EINVAL;
     }
-    CU(cudaSetDevice(device));
+    DEVICE_GUARD(device);
     lg_env *e = new (std::nothrow) lg_env();
     if (!e) {
         set_err("out of host memory");
@@ -693,7 +726,7 @@ extern "C" int lg_create(const lg_config *cfg, int64_t n_envs, int64_t global_of
 
 extern "C" int lg_destroy(lg_env *e) {
     if (!e) return LG_OK;
-    cudaSetDevice(e->device);
+    DeviceGuard dg(e->device);
     Params &p = e->base;
     void *ptrs[] = {p.rows, p.hot, p.mv, p.lossv, p.rs, p.ri, p.rb, p.mseed, p.err, p.aux,
                     e->d_act, e->d_obs, e->d_rew, e->d_done, e->d_term, e->d_er, e->d_es, e->d_fl, e->d_el,
@@ -766,7 +799,7 @@ static int run_mode(lg_env *e, int mode, const long long *actions, void *obs, do
         set_err("step needs actions, reward and done buffers");
         return LG_EINVAL;
     }
-    CU(cudaSetDevice(e->device));
+    DEVICE_GUARD(e->device);
     Params p = e->base;
     p.actions = actions;
     p.obs = reinterpret_cast<float *>(obs);  // uint8 bytes when obs_u8
@@ -783,6 +816,14 @@ static int run_mode(lg_env *e, int mode, const long long *actions, void *obs, do
     p.reset_mask = mask;
     p.no_auto_reset = (flags & LG_STEP_NO_AUTO_RESET) ? 1 : 0;
     if (obs_bits) p.obs_bits = 1;
+    if (mode == MODE_STEP && (flags & LG_STEP_VALIDATE)) {
+        const long long n = e->B;
+        unsigned grid = (unsigned)((n + 255) / 256);
+        if (grid > 148u * 8u) grid = 148u * 8u;
+        check_actions_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(n, actions, e->n_actions, p.err);
+        CU(cudaGetLastError());
+        p.gate = 1;
+    }
     if (p.obs_bits && obs && packed_needs_zero(e)) {
         const size_t words = ((size_t)e->B * p.PE + 31) / 32;
         CU(cudaMemsetAsync(obs, 0, words * 4, (cudaStream_t)stream));
@@ -839,33 +880,61 @@ extern "C" int lg_step_host(lg_env *e, const int64_t *actions_host, void *obs_ho
         set_err("step_host needs actions, reward and done buffers");
         return LG_EINVAL;
     }
-    CU(cudaSetDevice(e->device));
+    DEVICE_GUARD(e->device);
     size_t B = (size_t)e->B;
     const size_t n_elems = B * (size_t)e->C * e->OH * e->OW;
     size_t obs_bytes = n_elems * (e->base.obs_u8 ? 1 : sizeof(float));
     const bool dev_bits = e->base.obs_bits;  // the env's own format is the packed stream
     const bool packed = obs_host && (dev_bits || packed_ok(e));
+    // Staging buffers are allocated into locals and committed to the env only
+    // when every allocation succeeded, so a failed call leaves no half-set
+    // state behind for the next one to launch into.
     if (!e->d_act) {
-        CU(cudaMalloc((void **)&e->d_act, B * 8));
-        CU(cudaMalloc((void **)&e->d_rew, B * 8));
-        CU(cudaMalloc((void **)&e->d_done, B));
-        CU(cudaMalloc((void **)&e->d_term, B));
-        CU(cudaMalloc((void **)&e->d_er, B * 8));
-        CU(cudaMalloc((void **)&e->d_es, B * 8));
-        CU(cudaMalloc((void **)&e->d_fl, B * 8));
-        CU(cudaMalloc((void **)&e->d_el, B * 8));
+        void *q[8] = {};
+        const size_t sz[8] = {B * 8, B * 8, B, B, B * 8, B * 8, B * 8, B * 8};
+        cudaError_t err = cudaSuccess;
+        for (int i = 0; i < 8 && err == cudaSuccess; i++) err = cudaMalloc(&q[i], sz[i]);
+        if (err != cudaSuccess) {
+            for (void *x : q)
+                if (x) cudaFree(x);
+            set_err("CUDA allocation failed: %s", cudaGetErrorString(err));
+            return LG_ECUDA;
+        }
+        e->d_act = (long long *)q[0];
+        e->d_rew = (double *)q[1];
+        e->d_done = (unsigned char *)q[2];
+        e->d_term = (unsigned char *)q[3];
+        e->d_er = (double *)q[4];
+        e->d_es = (double *)q[5];
+        e->d_fl = (double *)q[6];
+        e->d_el = (long long *)q[7];
     }
     if (packed && !e->d_bits) {
-        e->bits_bytes = ((n_elems + 31) / 32) * 4;
+        const size_t bits_bytes = ((n_elems + 31) / 32) * 4;
         const char *cm = getenv("LG_EXPAND_CHUNK_MB");
         size_t chunk = (size_t)(cm ? atof(cm) * (1 << 20) : 8.0 * (1 << 20));
         chunk = chunk < 4096 ? 4096 : (chunk & ~(size_t)63);
+        const size_t nchunks = dev_bits ? 0 : (bits_bytes + chunk - 1) / chunk;
+        uint32_t *d_bits = nullptr;
+        uint8_t *h_bits = nullptr;
+        std::vector<cudaEvent_t> evs(nchunks, nullptr);
+        cudaError_t err = cudaMalloc((void **)&d_bits, bits_bytes);
+        if (err == cudaSuccess && !dev_bits) err = cudaHostAlloc((void **)&h_bits, bits_bytes, cudaHostAllocDefault);
+        for (size_t i = 0; i < nchunks && err == cudaSuccess; i++)
+            err = cudaEventCreateWithFlags(&evs[i], cudaEventDisableTiming);
+        if (err != cudaSuccess) {
+            if (d_bits) cudaFree(d_bits);
+            if (h_bits) cudaFreeHost(h_bits);
+            for (cudaEvent_t ev : evs)
+                if (ev) cudaEventDestroy(ev);
+            set_err("CUDA allocation failed: %s", cudaGetErrorString(err));
+            return LG_ECUDA;
+        }
+        e->bits_bytes = bits_bytes;
         e->chunk_bytes = chunk;
-        size_t nchunks = (e->bits_bytes + chunk - 1) / chunk;
-        CU(cudaMalloc((void **)&e->d_bits, e->bits_bytes));
-        if (!dev_bits) CU(cudaHostAlloc((void **)&e->h_bits, e->bits_bytes, cudaHostAllocDefault));
-        e->chunk_ev.resize(dev_bits ? 0 : nchunks);
-        for (auto &ev : e->chunk_ev) CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        e->d_bits = d_bits;
+        e->h_bits = h_bits;
+        e->chunk_ev = std::move(evs);
     }
     if (obs_host && !packed && !e->d_obs) CU(cudaMalloc((void **)&e->d_obs, obs_bytes));
     cudaStream_t s = (cudaStream_t)stream;
@@ -995,7 +1064,7 @@ extern "C" int lg_export_state(lg_env *e, const lg_state *dst, void *stream) {
         set_err("null argument");
         return LG_EINVAL;
     }
-    CU(cudaSetDevice(e->device));
+    DEVICE_GUARD(e->device);
     return launch_state(e, *dst, true, (cudaStream_t)stream);
 }
 
@@ -1004,7 +1073,7 @@ extern "C" int lg_import_state(lg_env *e, const lg_state *src, void *stream) {
         set_err("null argument");
         return LG_EINVAL;
     }
-    CU(cudaSetDevice(e->device));
+    DEVICE_GUARD(e->device);
     cudaStream_t s = (cudaStream_t)stream;
     if (!e->frz_ok && !e->elide_ok) return launch_state(e, *src, false, s);
     // the import kernel flags envs whose frozen plane is not their border plane
@@ -1023,7 +1092,7 @@ extern "C" int lg_errors(lg_env *e, uint32_t *flags, void *stream) {
         set_err("null argument");
         return LG_EINVAL;
     }
-    CU(cudaSetDevice(e->device));
+    DEVICE_GUARD(e->device);
     cudaStream_t s = (cudaStream_t)stream;
     CU(cudaMemcpyAsync(flags, e->base.err, 4, cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
@@ -1036,7 +1105,7 @@ extern "C" int lg_random_actions(lg_env *e, int64_t *actions, uint64_t seed, voi
         set_err("null argument");
         return LG_EINVAL;
     }
-    CU(cudaSetDevice(e->device));
+    DEVICE_GUARD(e->device);
     random_actions_kernel<<<(unsigned)((e->B + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
         e->B, e->offset, seed, e->n_actions, (long long *)actions);
     CU(cudaGetLastError());
@@ -1048,13 +1117,7 @@ static int launch_metrics_t(long long n, int H, int W, const uint8_t *tiles, con
                             uint64_t *rng, int64_t *values, uint8_t *unreach, cudaStream_t s) {
     int E = 256 / G::TEAM;
     size_t smem = (size_t)E * G::ROWS * G::RUNS * 2;
-    static std::once_flag once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(once, [] {
-        attr_err = cudaFuncSetAttribute(metrics_kernel<G, DOM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        200 * 1024);
-    });
-    CU(attr_err);
+    CU(smem_attr((const void *)metrics_kernel<G, DOM>));
     metrics_kernel<G, DOM><<<(unsigned)((n + E - 1) / E), 256, smem, s>>>(n, H, W, tiles, active, rng,
                                                                            values, unreach);
     CU(cudaGetLastError());

@@ -962,6 +962,7 @@ __device__ __forceinline__ void solo_begin(const Params &p, int mode, long long 
             } else {
                 nxt = solo_serp_next(ed, e.pr, e.pc);
             }
+            nxt = max(nxt, 0);  // no editable cell left (imported state): stay well-formed
             e.pos_idx = nidx;
             e.pr = nxt >> 4;
             e.pc = nxt & 15;
@@ -1051,6 +1052,7 @@ __device__ __forceinline__ void env_solo_body(const Params &p, int mode) {
     extern __shared__ __align__(16) uint32_t smem_w[];
     const int E = p.solo_E, T = blockDim.x, tid = threadIdx.x;
     constexpr bool warp_mode = WARP == 1;  // the host launches this kernel only when E == T
+    if (gate_closed(p)) return;
     (void)E;
     // warp mode (large batches): warp w owns 32 consecutive envs and writes
     // their outputs; block mode (small batches): E < T envs per block and all

@@ -95,12 +95,12 @@ class BatchEnv:
             self.device = torch.device("cuda", torch.cuda.current_device())
         self.validate = validate
         self._global_offset = int(global_offset)
-        self._seed = int(seed)
+        self._seed = check_seed(seed)
         handle = ctypes.c_void_p()
         cfgc = make_lg_config(config, obs_dtype)
         self.obs_dtype = obs_dtype
         _lib.check(lib.lg_create(ctypes.byref(cfgc), int(n_envs), int(global_offset),
-                                 int(seed) & ((1 << 64) - 1), self.device.index, ctypes.byref(handle)))
+                                 self._seed, self.device.index, ctypes.byref(handle)))
         self._h = handle
         desc = _lib.LgDesc()
         _lib.check(lib.lg_describe(self._h, ctypes.byref(desc)))
@@ -168,6 +168,7 @@ class BatchEnv:
         return obs
 
     def _actions(self, actions):
+        """-> (device int64 actions, whether the range still needs the device check)."""
         t = self._torch
         if isinstance(actions, t.Tensor):
             a = actions
@@ -175,35 +176,44 @@ class BatchEnv:
                 raise ValueError(f"expected {self._n} actions, got shape {tuple(a.shape)}")
             if a.device != self.device or a.dtype != t.int64:
                 a = a.to(device=self.device, dtype=t.int64)
-            a = a.contiguous()
-            if self.validate:
-                lo, hi = int(a.min()), int(a.max())
-                if lo < 0 or hi >= self.n_actions:
-                    raise ValueError("action id out of range")
-            return a
+            return a.contiguous(), True
         a = np.asarray(actions, dtype=np.int64)
         if a.shape != (self._n,):
             raise ValueError(f"expected {self._n} actions, got shape {a.shape}")
         if a.size and (a.min() < 0 or a.max() >= self.n_actions):
             raise ValueError("action id out of range")
-        return t.from_numpy(np.ascontiguousarray(a)).to(self.device, non_blocking=False)
+        return t.from_numpy(np.ascontiguousarray(a)).to(self.device, non_blocking=False), False
 
-    def step(self, actions, *, out=None, stats=None, with_obs: bool = True):
-        """One transition (env.py:521-525): ``(obs, reward, done, info)``."""
+    def step(self, actions, *, out=None, stats=None, with_obs: bool = True, checked: bool = False):
+        """One transition (env.py:521-525): ``(obs, reward, done, info)``.
+
+        With ``validate`` (the default), device actions are range-checked on
+        the device before the step kernel runs -- a bad batch raises
+        ``ValueError`` and leaves every env untouched, as env.py:358-361 --
+        and the auto-reset error flags (pinpoint overflow, no editable cell;
+        ``reset_rows``, env.py:315-316, grid.py:213-214) are read back: one
+        4-byte device->host read per step. ``validate=False`` (throughput) or
+        ``checked=True`` (the caller guarantees the range, e.g. actions
+        sampled from the policy) skips it; flags then surface on
+        ``check_errors()``."""
         if not self._started:
             raise RuntimeError("reset() the batch before stepping")
         t = self._torch
-        a = self._actions(actions)
+        a, device_check = self._actions(actions)
+        validate = self.validate and not checked
         obs = (self.new_obs() if out is None else out) if with_obs else None
         reward = t.empty(self._n, dtype=t.float64, device=self.device)
         done = t.empty(self._n, dtype=t.bool, device=self.device)
         info = self._info_buffers()
         ci = _lib.LgInfo(*[_ptr(info[k]) for k in INFO_KEYS])
+        flags = _lib.STEP_VALIDATE if (validate and device_check) else 0
         with t.cuda.device(self.device):
-            _lib.check(_lib.load().lg_step(
+            _lib.check(_lib.load().lg_step_flags(
                 self._h, _ptr(a), _ptr(obs) if obs is not None else None, _ptr(reward), _ptr(done),
-                ctypes.byref(ci), _ptr(stats) if stats is not None else None,
+                ctypes.byref(ci), _ptr(stats) if stats is not None else None, flags,
                 _stream(t, self.device)))
+        if validate:
+            self.check_errors()
         return obs, reward, done, info
 
     def step_raw(self, actions, obs, reward, done, info=None, stats=None) -> None:
@@ -377,10 +387,22 @@ def _rng_row(st: dict) -> np.ndarray:
                     dtype=np.uint64)
 
 
+def check_seed(seed) -> int:
+    """``SeedSequence(seed)`` takes any non-negative int and raises on negative
+    ones (env.py:591-594); the device streams take the 64-bit seeds, so larger
+    ones are refused instead of silently masked."""
+    s = int(seed)
+    if s < 0:
+        raise ValueError("seed must be a non-negative integer")
+    if s >= 1 << 64:
+        raise ValueError("seeds >= 2**64 are not supported on device")
+    return s
+
+
 def spawn_streams(seed: int, n: int, offset: int = 0) -> np.ndarray:
     """Host SeedSequence(seed).spawn(...)[offset:offset+n] PCG64 states ([n, 6] uint64)."""
     out = np.zeros((n, 6), dtype=np.uint64)
-    _lib.check(_lib.load().lg_seed_streams(int(seed), int(offset), int(n),
+    _lib.check(_lib.load().lg_seed_streams(check_seed(seed), int(offset), int(n),
                                            out.ctypes.data_as(ctypes.c_void_p)))
     return out
 

@@ -223,7 +223,7 @@ def collect_rollout(policy, env, length: int, sampler, obs):
             out_actions[t] = actions
             out_logprobs[t] = logp
             out_values[t] = value.float()
-            obs, reward, done, info = env.step(actions)
+            obs, reward, done, info = env.step(actions, checked=True)  # sampled: in range
             out_rewards[t] = reward
             out_dones[t] = done
             finished_sum.append(info["episode_reward"])

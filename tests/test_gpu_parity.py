@@ -218,8 +218,59 @@ def test_numpy_facade_and_errors():
     assert dev.errors() == 0
     strict = BatchEnv(cfg, 4, seed=0)
     strict.reset()
-    with pytest.raises(ValueError):
+    before = strict.state_dict()
+    with pytest.raises(ValueError, match="out of range"):
         strict.step(torch.tensor([0, 0, 7, 0], device="cuda"))
+    with pytest.raises(ValueError, match="out of range"):
+        strict.step(torch.tensor([0, -1, 1, 0], device="cuda"))
+    after = strict.state_dict()  # rejected before any mutation (env.py:358-361)
+    for k in ("tiles", "pos_idx", "t", "changes", "prev_loss", "rng"):
+        assert np.array_equal(before[k], after[k]), k
+    twin = O.OracleBatchEnv(cfg, 4, seed=0)
+    twin.reset()
+    a = np.array([1, 2, 0, 1])
+    o1, r1, _, _ = strict.step(torch.from_numpy(a).cuda())
+    o2, r2, _, _ = twin.step(a)
+    assert np.array_equal(_np(o1), o2) and np.array_equal(_np(r1), r2)
+
+
+def test_validated_step_raises_auto_reset_errors():
+    """An auto-reset that cannot place its pinpoints raises ValueError from
+    the step (reset_rows -> place_pinpoints, grid.py:213-214), as the
+    reference does; validate=False defers it to check_errors()."""
+    cfg = EnvConfig(domain="maze", max_width=6, max_height=6, obs_size=5, randomize_shape=True,
+                    pinpoints=("player",) * 10, max_steps=2)
+    n = 4
+    seed = next(s for s in range(100) if _resets_ok(cfg, n, s))
+    for validate in (True, False):
+        env = BatchEnv(cfg, n, seed=seed, validate=validate)
+        ref = O.OracleBatchEnv(cfg, n, seed=seed)
+        assert np.array_equal(_np(env.reset()), ref.reset())
+        raised = False
+        for t in range(400):
+            a = np.zeros(n, dtype=np.int64)
+            try:
+                ref.step(a)
+            except ValueError:
+                raised = True
+                if validate:
+                    with pytest.raises(ValueError, match="pinpoints"):
+                        env.step(a)
+                else:
+                    env.step(a)
+                    with pytest.raises(ValueError, match="pinpoints"):
+                        env.check_errors()
+                break
+            o1, r1, _, _ = env.step(a)
+        assert raised
+
+
+def _resets_ok(cfg, n, seed):
+    try:
+        O.OracleBatchEnv(cfg, n, seed=seed).reset()
+        return True
+    except ValueError:
+        return False
 
 
 def test_pinpoint_overflow_flags_error():
@@ -395,7 +446,12 @@ def test_random_config_fuzz_against_oracle(seed):
         a = act.integers(0, cfg.n_actions, size=n)
         try:
             o2, r2, d2, i2 = ref.step(a)
-        except ValueError:  # e.g. an auto-reset that cannot place its pinpoints
+        except ValueError as exc:
+            # an auto-reset that cannot place its pinpoints (grid.py:213-214):
+            # the validated device step raises the same error on this step;
+            # every earlier step was compared
+            with pytest.raises(ValueError, match=str(exc).split(":")[0][:20]):
+                env.step(a)
             return
         o1, r1, d1, i1 = env.step(a)
         assert np.array_equal(_np(r1), r2), (cfg, t)
