@@ -176,6 +176,14 @@ int lg_errors(lg_env *env, uint32_t *flags, void *stream);
  * actions in [0, n_actions) from a counter hash of (seed, global env index). */
 int lg_random_actions(lg_env *env, int64_t *actions_dev, uint64_t seed, void *stream);
 
+/* harness.first_episode_rewards (harness.py:48-61), the per-step update on
+ * device buffers of n envs: where done[b] && !seen[b], rewards[b] =
+ * episode_reward[b] (the step's info["episode_reward"]) and seen[b] = 1;
+ * n_seen (u64, device) counts the envs seen so far, so the caller polls one
+ * word every few steps instead of the masks. Stream-ordered. */
+int lg_first_episode(int64_t n, const uint8_t *done_dev, const double *episode_reward_dev, uint8_t *seen_dev,
+                     double *rewards_dev, uint64_t *n_seen_dev, void *stream);
+
 /* compute_metrics_batch (problems.py:105-129) on [B][H][W] stacks of tiles and
  * active masks; rng_dev [B][6] (advanced in place, binary only; may be NULL for
  * maze/dungeon); values_dev int64 [M][B], unreach_dev u8 [M][B]. */

@@ -113,6 +113,24 @@ __global__ void check_actions_kernel(long long B, const long long *a, long long 
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, (unsigned)FLAG_BAD_ACTION);
 }
 
+// harness.first_episode_rewards (harness.py:48-61), one step's worth: an env
+// that finishes its first episode records info["episode_reward"]; the
+// warp-aggregated count lets the host poll one word instead of the masks.
+__global__ void first_episode_kernel(long long B, const uint8_t *done, const double *ep_rew, uint8_t *seen,
+                                     double *out, unsigned long long *n_seen) {
+    const long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    bool first = false;
+    if (b < B) {
+        first = done[b] && !seen[b];
+        if (first) {
+            out[b] = ep_rew[b];
+            seen[b] = 1;
+        }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, first);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(n_seen, (unsigned long long)__popc(m));
+}
+
 // state_dict export (env.py:535-559), team per env
 template <class G, int DOM>
 __global__ void __launch_bounds__(256) export_kernel(const Params p, lg_state dst) {
@@ -1097,6 +1115,19 @@ extern "C" int lg_errors(lg_env *e, uint32_t *flags, void *stream) {
     CU(cudaMemcpyAsync(flags, e->base.err, 4, cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
     CU(cudaMemsetAsync(e->base.err, 0, 4, s));
+    return LG_OK;
+}
+
+extern "C" int lg_first_episode(int64_t n, const uint8_t *done, const double *episode_reward, uint8_t *seen,
+                                double *rewards, uint64_t *n_seen, void *stream) {
+    if (n < 0 || (n > 0 && (!done || !episode_reward || !seen || !rewards || !n_seen))) {
+        set_err("first_episode needs done, episode_reward, seen, rewards and n_seen buffers");
+        return LG_EINVAL;
+    }
+    if (n == 0) return LG_OK;
+    first_episode_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        n, done, episode_reward, seen, rewards, (unsigned long long *)n_seen);
+    CU(cudaGetLastError());
     return LG_OK;
 }
 

@@ -125,6 +125,63 @@ def init_policy(arch: ArchConfig, seed: int):
     return make_policy(arch)
 
 
+CHECKPOINT_FORMAT = "levelgen-checkpoint"
+CHECKPOINT_VERSION = 1
+
+
+@dataclass
+class Checkpoint:
+    """nets.Checkpoint (nets.py:204-239): ``meta`` JSON + named arrays, the
+    reference's on-disk ``.npz`` format (``param/<name>`` = model weights)."""
+    meta: dict
+    arrays: dict
+
+    @property
+    def arch(self) -> ArchConfig:
+        a = self.meta["arch"]
+        return ArchConfig(obs_size=a["obs_size"], in_channels=a["in_channels"], n_actions=a["n_actions"],
+                          conv_channels=tuple(a["conv_channels"]), fc_dims=tuple(a["fc_dims"]))
+
+    @property
+    def step(self) -> int:
+        return int(self.meta["step"])
+
+    def build_model(self, device=None):
+        torch = _torch()
+        model = make_policy(self.arch)
+        state = {k[len("param/"):]: torch.from_numpy(np.array(v, dtype=np.float32))
+                 for k, v in self.arrays.items() if k.startswith("param/")}
+        model.load_state_dict(state)
+        return model.to(device) if device is not None else model
+
+
+def save_checkpoint(path, model, *, env_config: dict, step: int, extra_meta: dict | None = None) -> str:
+    """nets.save_checkpoint (nets.py:242-270): little-endian float32 params."""
+    import json
+    from dataclasses import asdict
+    meta = {"format": CHECKPOINT_FORMAT, "version": CHECKPOINT_VERSION, "arch": asdict(model.arch),
+            "env": env_config, "step": int(step)}
+    if extra_meta:
+        meta.update(extra_meta)
+    arrays = {f"param/{k}": v.detach().cpu().numpy().astype("<f4") for k, v in model.state_dict().items()}
+    with open(path, "wb") as f:
+        np.savez(f, meta=np.array(json.dumps(meta)), **arrays)
+    return str(path)
+
+
+def load_checkpoint(path) -> Checkpoint:
+    """nets.load_checkpoint (nets.py:273-282), same format checks and errors."""
+    import json
+    with np.load(path, allow_pickle=False) as z:
+        meta = json.loads(str(z["meta"]))
+        if meta.get("format") != CHECKPOINT_FORMAT:
+            raise ValueError(f"{path}: not a recognized checkpoint")
+        if meta.get("version") != CHECKPOINT_VERSION:
+            raise ValueError(f"{path}: unsupported checkpoint version {meta.get('version')}")
+        arrays = {k: z[k] for k in z.files if k != "meta"}
+    return Checkpoint(meta=meta, arrays=arrays)
+
+
 def conv1_bits(bits, n_envs: int, obs_shape, weight, bias, *, out_dtype=None, relu: bool = True, out=None,
                channels_last: bool = False):
     """relu(conv2d(obs, weight, bias)) (3x3, valid) from the packed stream of a
@@ -233,4 +290,5 @@ def collect_rollout(policy, env, length: int, sampler, obs):
 
 
 __all__ = ["ArchConfig", "default_arch", "count_params", "make_policy", "init_policy", "conv1_bits",
+           "Checkpoint", "save_checkpoint", "load_checkpoint",
            "PackedPolicy", "RolloutBatch", "collect_rollout"]
