@@ -196,10 +196,25 @@ int lg_metrics(int domain, int max_h, int max_w, int64_t n, const uint8_t *tiles
  * straight from packed observation bits (LG_OBS_BITS layout, n_envs envs of
  * C x OH x OW elements). weight f32 [K][C][3][3], bias f32 [K] (device);
  * out [n_envs][K][OH-2][OW-2] (nhwc = 0) or [n_envs][OH-2][OW-2][K] (nhwc = 1,
- * the channels-last layout), float32 (out_bf16 = 0) or bfloat16 (1).
+ * the channels-last layout), float32 (out_bf16 = 0) or bfloat16 (1); nhwc = 2
+ * is the tensor-core tile layout lg_policy_trunk reads (K = 16, bfloat16).
  * 1 <= K <= 64, C <= 16. Stream-ordered. */
 int lg_conv1_bits(const uint32_t *bits_dev, int64_t n_envs, int C, int OH, int OW, const float *weight_dev,
                   const float *bias_dev, int K, void *out_dev, int out_bf16, int relu, int nhwc, void *stream);
+
+/* Policy consumer, the rest of the default ConvPolicy trunk (nets.py:150-183,
+ * conv_channels (16, 32), fc_dims (64,)) on the tensor cores (tcgen05, TMEM):
+ * conv2 (16 -> 32, 3x3 valid) + ReLU, the 64-wide FC + ReLU and both heads,
+ * for n_envs envs whose relu(conv1) is c1_tiles -- lg_conv1_bits with
+ * nhwc = 2 (tile layout: [ceil(n/128)][P1*P1][128 envs x 16 ch] bf16 UMMA
+ * core matrices), P1 = obs side - 2. w2 [9][512] and w3 [(P1-2)^2][2048]
+ * are the conv2 / FC weights in the same bf16 layout (the Python mirror packs
+ * them), b2 [32], b3 [64] f32; wh [n_actions + 1][64], bh [n_actions + 1] f32
+ * = policy-head rows then the value head. Writes logits f32 [n][n_actions]
+ * and value f32 [n]. n_actions <= 16. Stream-ordered. */
+int lg_policy_trunk(const void *c1_tiles, int64_t n_envs, int P1, const void *w2, const float *b2, const void *w3,
+                    const float *b3, const float *wh, const float *bh, int n_actions, float *logits, float *value,
+                    void *stream);
 
 /* Host SeedSequence(seed).spawn(offset+n)[offset+i] -> rng [n][6] (env.py:591-594). */
 int lg_seed_streams(uint64_t seed, int64_t offset, int64_t n, uint64_t *rng_host);

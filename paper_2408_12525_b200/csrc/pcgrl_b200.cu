@@ -16,6 +16,7 @@
 #include "host_expand.h"
 #include "policy_kernels.cuh"
 #include "solo_kernel.cuh"
+#include "trunk_kernel.cuh"
 
 using namespace lg;
 
@@ -1049,6 +1050,10 @@ extern "C" int lg_conv1_bits(const uint32_t *bits, int64_t n_envs, int C, int OH
         set_err("conv1_bits supports 1 <= C <= 16, 3 <= OH, OW and 1 <= K <= 64");
         return LG_EINVAL;
     }
+    if (nhwc == 2 && (K != 16 || !out_bf16 || OH != OW)) {
+        set_err("conv1_bits tile layout (lg_policy_trunk input) needs K = 16, bfloat16 output, square windows");
+        return LG_EINVAL;
+    }
     const int KC = (K + 3) / 4, KCt = KC <= 4 ? 4 : KC <= 8 ? 8 : 16;
     const size_t G = (size_t)((C + 3) / 4);
     const size_t table = G * 10 * 16 * (4 * KCt + 4) * sizeof(float);  // 9 tap tables + their sum
@@ -1075,6 +1080,43 @@ extern "C" int lg_conv1_bits(const uint32_t *bits, int64_t n_envs, int C, int OH
     if (KCt == 8) LG_CONV1(8);
     LG_CONV1(16);
 #undef LG_CONV1
+}
+
+extern "C" int lg_policy_trunk(const void *c1_tiles, int64_t n_envs, int P1, const void *w2, const float *b2,
+                               const void *w3, const float *b3, const float *wh, const float *bh, int n_actions,
+                               float *logits, float *value, void *stream) {
+    if (!c1_tiles || !w2 || !b2 || !w3 || !b3 || !wh || !bh || !logits || !value || n_envs < 1) {
+        set_err("policy_trunk needs every buffer and n_envs >= 1");
+        return LG_EINVAL;
+    }
+    if (P1 < 3 || P1 > 126 || n_actions < 1 || n_actions > TK_MAXNA) {
+        set_err("policy_trunk supports conv1 sides 3..126 and 1..%d actions", TK_MAXNA);
+        return LG_EINVAL;
+    }
+    const void *al[] = {c1_tiles, w2, w3};
+    for (const void *q : al)
+        if ((uintptr_t)q & 15) {
+            set_err("policy_trunk operand blocks must be 16-byte aligned");
+            return LG_EINVAL;
+        }
+    CU(smem_attr((const void *)trunk_kernel, (int)TK_SMEM));
+    TrunkParams tp;
+    tp.c1 = reinterpret_cast<const __nv_bfloat16 *>(c1_tiles);
+    tp.w2 = reinterpret_cast<const __nv_bfloat16 *>(w2);
+    tp.b2 = b2;
+    tp.w3 = reinterpret_cast<const __nv_bfloat16 *>(w3);
+    tp.b3 = b3;
+    tp.wh = wh;
+    tp.bh = bh;
+    tp.logits = logits;
+    tp.value = value;
+    tp.B = n_envs;
+    tp.P1 = P1;
+    tp.NA = n_actions;
+    const unsigned grid = (unsigned)((n_envs + 127) / 128);
+    trunk_kernel<<<grid, 192, TK_SMEM, (cudaStream_t)stream>>>(tp);
+    CU(cudaGetLastError());
+    return LG_OK;
 }
 
 extern "C" int lg_export_state(lg_env *e, const lg_state *dst, void *stream) {

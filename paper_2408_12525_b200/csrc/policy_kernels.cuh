@@ -134,6 +134,30 @@ __global__ void __launch_bounds__(256) conv1_bits_kernel(const uint32_t *__restr
                     }
                 }
             }
+            if (nhwc == 2) {  // tcgen05 tile layout (trunk_kernel.cuh): K = 16, bfloat16
+                // block [env / 128][px] of 128 envs x 16 channels as UMMA K-major
+                // core matrices: (k / 8, m / 8) -> 128 B of 8 rows x 8 channels
+                const int m = (int)(env & 127);
+                __nv_bfloat16 *blk = reinterpret_cast<__nv_bfloat16 *>(out) + ((size_t)(env >> 7) * NP + px) * 2048;
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    uint32_t wd[4];
+#pragma unroll
+                    for (int j = 0; j < 4; j++) {
+                        const float4 a4 = acc[2 * h + (j >> 1)];
+                        float a = (j & 1) ? a4.z : a4.x, b = (j & 1) ? a4.w : a4.y;
+                        if (relu) {
+                            a = a > 0.f ? a : 0.f;
+                            b = b > 0.f ? b : 0.f;
+                        }
+                        __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+                        wd[j] = *reinterpret_cast<uint32_t *>(&h2);
+                    }
+                    *reinterpret_cast<uint4 *>(blk + ((h * 16 + (m >> 3)) * 64 + (m & 7) * 8)) =
+                        make_uint4(wd[0], wd[1], wd[2], wd[3]);
+                }
+                continue;
+            }
             if (nhwc) {  // [env][px][k]: the pixel's K channels are contiguous (vector stores)
                 const size_t base = ((size_t)env * NP + px) * K;
                 if (BF16 && (K & 7) == 0) {

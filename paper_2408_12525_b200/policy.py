@@ -242,6 +242,89 @@ class PackedPolicy:
             return self.model.policy_head(h).float(), self.model.value_head(h).squeeze(-1).float()
 
 
+def pack_conv2_weight(weight):
+    """Conv2d(16 -> 32, 3x3) weight [32, 16, 3, 3] -> the trunk kernel's B
+    operands: per tap (dy, dx) an N = 32 x K = 16 bf16 block of UMMA K-major
+    core matrices, [9, 512] (csrc/trunk_kernel.cuh)."""
+    torch = _torch()
+    n, k = weight.shape[:2]
+    w = weight.detach().to(torch.float32).permute(2, 3, 0, 1).reshape(9, n // 8, 8, k // 8, 8)
+    return w.permute(0, 3, 1, 2, 4).reshape(9, n * k).to(torch.bfloat16).contiguous()
+
+
+def pack_fc_weight(weight, channels: int, side: int):
+    """Linear(channels * side^2 -> 64) weight [64, channels*side^2] (torch
+    flattens [C, H, W]) -> per conv2 pixel an N = 64 x K = channels bf16
+    block of UMMA K-major core matrices, [side^2, 64 * channels]."""
+    torch = _torch()
+    nout = weight.shape[0]
+    npx = side * side
+    w = weight.detach().to(torch.float32).reshape(nout, channels, npx).permute(2, 0, 1)  # [p][n][k]
+    w = w.reshape(npx, nout // 8, 8, channels // 8, 8).permute(0, 3, 1, 2, 4)
+    return w.reshape(npx, nout * channels).to(torch.bfloat16).contiguous()
+
+
+class TrunkPolicy:
+    """The default ConvPolicy (conv (16, 32), fc (64,); nets.py:150-183)
+    evaluated from packed observation bits on the GPU with two kernels and no
+    torch math: ``lg_conv1_bits`` writes relu(conv1) as bf16 tensor-core tiles,
+    ``lg_policy_trunk`` runs conv2 + ReLU, the FC + ReLU (tcgen05.mma, TMEM
+    accumulators) and both heads (fp32). bf16 operands, fp32 accumulation.
+    Call ``refresh()`` after the model's weights change (an optimizer step)."""
+
+    def __init__(self, model, obs_shape):
+        arch = model.arch
+        if tuple(arch.conv_channels) != (16, 32) or tuple(arch.fc_dims) != (64,):
+            raise ValueError("the fused trunk implements the default arch: conv (16, 32), fc (64,)")
+        if arch.n_actions > 16:
+            raise ValueError("the fused trunk's heads support at most 16 actions")
+        C, OH, OW = (int(x) for x in obs_shape)
+        if OH != OW or OH < 5:
+            raise ValueError("the fused trunk needs a square window of side >= 5")
+        self.model = model
+        self.obs_shape = (C, OH, OW)
+        self.P1 = OH - 2
+        self.refresh()
+
+    def refresh(self) -> None:
+        torch = _torch()
+        m = self.model
+        conv1, conv2, fc = m.trunk[0], m.trunk[2], m.trunk[5]
+        P2 = self.P1 - 2
+        with torch.no_grad():
+            self.w1 = conv1.weight.detach().float().contiguous()
+            self.b1 = conv1.bias.detach().float().contiguous()
+            self.w2 = pack_conv2_weight(conv2.weight)
+            self.b2 = conv2.bias.detach().float().contiguous()
+            self.w3 = pack_fc_weight(fc.weight, 32, P2)
+            self.b3 = fc.bias.detach().float().contiguous()
+            self.wh = torch.cat([m.policy_head.weight, m.value_head.weight]).detach().float().contiguous()
+            self.bh = torch.cat([m.policy_head.bias, m.value_head.bias]).detach().float().contiguous()
+
+    def conv1_tiles(self, bits, n_envs: int):
+        torch = _torch()
+        tiles = (n_envs + 127) // 128
+        out = torch.empty(tiles * self.P1 * self.P1 * 2048, dtype=torch.bfloat16, device=bits.device)
+        C, OH, OW = self.obs_shape
+        stream = ctypes.c_void_p(torch.cuda.current_stream(bits.device).cuda_stream)
+        p = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        _lib.check(_lib.load().lg_conv1_bits(p(bits), int(n_envs), C, OH, OW, p(self.w1), p(self.b1), 16, p(out),
+                                             1, 1, 2, stream))
+        return out
+
+    def __call__(self, bits, n_envs: int):
+        torch = _torch()
+        c1 = self.conv1_tiles(bits, n_envs)
+        na = self.model.arch.n_actions
+        logits = torch.empty((n_envs, na), dtype=torch.float32, device=bits.device)
+        value = torch.empty(n_envs, dtype=torch.float32, device=bits.device)
+        stream = ctypes.c_void_p(torch.cuda.current_stream(bits.device).cuda_stream)
+        p = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        _lib.check(_lib.load().lg_policy_trunk(p(c1), int(n_envs), self.P1, p(self.w2), p(self.b2), p(self.w3),
+                                               p(self.b3), p(self.wh), p(self.bh), na, p(logits), p(value), stream))
+        return logits, value
+
+
 @dataclass
 class RolloutBatch:
     """ppo.RolloutBatch (ppo.py:91-98), device tensors; obs in the env's format."""
@@ -261,7 +344,7 @@ def collect_rollout(policy, env, length: int, sampler, obs):
     episodes that finished (one host sync at the end, not one per step)."""
     torch = _torch()
     B = env.n_envs
-    packed = isinstance(policy, PackedPolicy)
+    packed = isinstance(policy, (PackedPolicy, TrunkPolicy))
     dev = env.device
     out_obs = torch.empty((length,) + tuple(obs.shape), dtype=obs.dtype, device=dev)
     out_actions = torch.empty((length, B), dtype=torch.int64, device=dev)
@@ -290,5 +373,5 @@ def collect_rollout(policy, env, length: int, sampler, obs):
 
 
 __all__ = ["ArchConfig", "default_arch", "count_params", "make_policy", "init_policy", "conv1_bits",
-           "Checkpoint", "save_checkpoint", "load_checkpoint",
+           "Checkpoint", "save_checkpoint", "load_checkpoint", "TrunkPolicy", "pack_conv2_weight", "pack_fc_weight",
            "PackedPolicy", "RolloutBatch", "collect_rollout"]

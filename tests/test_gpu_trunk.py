@@ -1,0 +1,104 @@
+"""The tensor-core policy trunk (tcgen05 + TMEM) against torch references
+(needs a B200).
+
+``TrunkPolicy`` = ``lg_conv1_bits`` (tile layout) + ``lg_policy_trunk``: the
+default ConvPolicy (nets.py:150-183) from packed observation bits, bf16
+operands with fp32 accumulation. Two references on the same observations:
+
+* the reference model in float32 (TF32 off) -- bf16 tolerance: the largest
+  logit/value error within 2% of the largest magnitude;
+* the same function with bf16 rounding at the kernel's rounding points
+  (conv1 output, weights, conv2 output) -- within 0.3%, which pins the
+  kernel's indexing (taps, pixel order, layouts) rather than bf16 noise.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+from paper_2408_12525_b200.config import EnvConfig  # noqa: E402
+from paper_2408_12525_b200.env import BatchEnv, unpack_obs  # noqa: E402
+from paper_2408_12525_b200.policy import (TrunkPolicy, collect_rollout, default_arch,  # noqa: E402
+                                          init_policy)
+
+pytestmark = pytest.mark.gpu
+
+
+def _no_tf32():
+    torch.backends.cudnn.allow_tf32 = False
+    torch.backends.cuda.matmul.allow_tf32 = False
+
+
+def _bf(x):
+    return x.to(torch.bfloat16).float()
+
+
+def emulated(model, obs):
+    """ConvPolicy forward with the kernel's bf16 rounding points."""
+    F = torch.nn.functional
+    c1w, c2w, fc = model.trunk[0], model.trunk[2], model.trunk[5]
+    h = _bf(torch.relu(F.conv2d(obs, c1w.weight, c1w.bias)))
+    h = _bf(torch.relu(F.conv2d(h, _bf(c2w.weight), c2w.bias)))
+    h = torch.relu(h.flatten(1) @ _bf(fc.weight).T + fc.bias)
+    return model.policy_head(h), model.value_head(h).squeeze(-1)
+
+
+CASES = [
+    (dict(domain="binary"), 300, 0),                                  # obs 31 (c5 shape), ragged last tile
+    (dict(domain="maze", representation="turtle"), 256, 1),           # 6 channels, 8 actions
+    (dict(domain="dungeon", max_width=8, max_height=8, obs_size=15), 129, 2),  # P2 = 11: ragged column chunk
+    (dict(domain="binary", max_width=5, max_height=5, obs_size=5), 40, 3),     # P2 = 1
+]
+
+
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_trunk_matches_torch(case):
+    _no_tf32()
+    kw, n, seed = CASES[case]
+    cfg = EnvConfig(**kw)
+    env = BatchEnv(cfg, n, seed=seed, obs_dtype="bits")
+    bits = env.reset()
+    for t in range(3):
+        bits, _, _, _ = env.step(env.random_actions(t))
+    shp = env.observation_shape
+    model = init_policy(default_arch(shp[1], shp[0], cfg.n_actions), seed=seed).cuda()
+    with torch.no_grad():  # a larger head so the logits are not all ~0
+        model.policy_head.weight.mul_(50.0)
+        model.policy_head.bias.uniform_(-0.1, 0.1)
+        model.trunk[2].bias.uniform_(-0.1, 0.1)
+        model.trunk[5].bias.uniform_(-0.1, 0.1)
+    pol = TrunkPolicy(model, shp)
+    lg, v = pol(bits, n)
+    obs = unpack_obs(bits, n, shp)
+    with torch.no_grad():
+        rl, rv = model(obs)
+        el, ev = emulated(model, obs)
+    for got, ref, emu in ((lg, rl, el), (v, rv, ev)):
+        scale = float(ref.abs().max())
+        assert float((got - emu).abs().max()) <= 3e-3 * scale + 1e-5, (float((got - emu).abs().max()), scale)
+        assert float((got - ref).abs().max()) <= 2e-2 * scale + 1e-5, (float((got - ref).abs().max()), scale)
+
+
+def test_trunk_rollout_and_refresh():
+    """collect_rollout (ppo.py:101-143) with the fused trunk; refresh() picks
+    up new weights."""
+    _no_tf32()
+    cfg = EnvConfig(domain="binary")
+    n = 4096
+    env = BatchEnv(cfg, n, seed=0, validate=False, obs_dtype="bits")
+    bits = env.reset()
+    shp = env.observation_shape
+    model = init_policy(default_arch(shp[1], shp[0], cfg.n_actions), seed=0).cuda()
+    pol = TrunkPolicy(model, shp)
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    batch, bits2, _ = collect_rollout(pol, env, 4, gen, bits)
+    assert batch.actions.shape == (4, n) and int(batch.actions.max()) < cfg.n_actions
+    assert env.errors() == 0
+    with torch.no_grad():
+        model.policy_head.bias.add_(1.0)
+    l0, _ = pol(bits2, n)
+    pol.refresh()
+    l1, _ = pol(bits2, n)
+    assert torch.allclose(l1 - l0, torch.ones_like(l0), atol=1e-4)

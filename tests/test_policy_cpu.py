@@ -46,3 +46,26 @@ def test_arch_validation_and_defaults():
         ArchConfig(7, 4, 1)
     with pytest.raises(ValueError):
         init_policy(ArchConfig(7, 4, 3), 0)(torch.zeros(2, 4, 5, 5))
+
+
+def test_trunk_weight_packing_layouts():
+    """pack_conv2_weight / pack_fc_weight put element (n, k) of each block at
+    ((k/8)*(N/8) + n/8)*64 + (n%8)*8 + k%8 (UMMA K-major core matrices,
+    csrc/trunk_kernel.cuh)."""
+    import torch
+    from paper_2408_12525_b200.policy import pack_conv2_weight, pack_fc_weight
+    w2 = torch.randn(32, 16, 3, 3)
+    p2 = pack_conv2_weight(w2).float()
+    side = 5
+    w3 = torch.randn(64, 32 * side * side)
+    p3 = pack_fc_weight(w3, 32, side).float()
+    g = torch.Generator().manual_seed(0)
+    for _ in range(200):
+        t, n, k = (int(torch.randint(9, (1,), generator=g)), int(torch.randint(32, (1,), generator=g)),
+                   int(torch.randint(16, (1,), generator=g)))
+        off = ((k // 8) * 4 + n // 8) * 64 + (n % 8) * 8 + k % 8
+        assert p2[t, off] == w2[n, k, t // 3, t % 3].bfloat16().float()
+        px, n, k = (int(torch.randint(side * side, (1,), generator=g)), int(torch.randint(64, (1,), generator=g)),
+                    int(torch.randint(32, (1,), generator=g)))
+        off = ((k // 8) * 8 + n // 8) * 64 + (n % 8) * 8 + k % 8
+        assert p3[px, off] == w3[n, k * side * side + px].bfloat16().float()
