@@ -1059,7 +1059,8 @@ extern "C" int lg_conv1_bits(const uint32_t *bits, int64_t n_envs, int C, int OH
     const size_t table = G * 10 * 16 * (4 * KCt + 4) * sizeof(float);  // 9 tap tables + their sum
     // envs per block iteration: 4 (fewer barriers, fuller rounds), fewer when
     // four large observations (masks + bits) do not fit in shared memory
-    int EB = 4;
+    // (tile layout: 32 envs, so a warp's stores cover whole 512-byte runs of a block)
+    int EB = nhwc == 2 ? 32 : 4;
     size_t smem = 0;
     for (; EB >= 1; EB /= 2) {
         const size_t masks = ((size_t)EB * G * OH * OW + 15) & ~(size_t)15;
@@ -1114,7 +1115,7 @@ extern "C" int lg_policy_trunk(const void *c1_tiles, int64_t n_envs, int P1, con
     tp.P1 = P1;
     tp.NA = n_actions;
     const unsigned grid = (unsigned)((n_envs + 127) / 128);
-    trunk_kernel<<<grid, 192, TK_SMEM, (cudaStream_t)stream>>>(tp);
+    trunk_kernel<<<grid, TK_THREADS, TK_SMEM, (cudaStream_t)stream>>>(tp);
     CU(cudaGetLastError());
     return LG_OK;
 }

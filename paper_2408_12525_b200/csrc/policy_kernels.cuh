@@ -93,8 +93,21 @@ __global__ void __launch_bounds__(256) conv1_bits_kernel(const uint32_t *__restr
             mk[i] = (uint8_t)m;
         }
         __syncthreads();
+        const int lg_eb = __ffs(EB) - 1;
         for (int it = threadIdx.x; it < ne * NP; it += blockDim.x) {
-            const int e = (int)fdiv(dv.np, (uint32_t)it), px = it - e * NP;
+            int e, px;
+            if (nhwc == 2) {  // envs fastest: a warp's 16-byte stores fill whole core-matrix rows
+                if (ne == EB) {
+                    e = it & (EB - 1);
+                    px = it >> lg_eb;
+                } else {
+                    px = it / ne;
+                    e = it - px * ne;
+                }
+            } else {
+                e = (int)fdiv(dv.np, (uint32_t)it);
+                px = it - e * NP;
+            }
             const long long env = env0 + e;
             const int y = (int)fdiv(dv.pw, (uint32_t)px), x = px - y * PW;
             float4 acc[KC];

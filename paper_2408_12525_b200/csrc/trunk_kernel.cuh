@@ -24,15 +24,19 @@
 //       weights W[n, c*P2*P2 + p] (torch flattens [C, H, W]),
 //       ((k/8)*8 + n/8)*64 + (n%8)*8 + k%8
 //
-// Warp roles (192 threads): warp 0 lane 0 = producer (cp.async.bulk of the
-// conv1 pixel blocks and FC weight blocks, mbarrier complete_tx); warp 1 =
-// TMEM allocator + lane 0 issues every tcgen05.mma/commit; warps 2..5 =
-// epilogue (tcgen05.ld of their TMEM lane quadrant, one env per thread).
+// Warp roles (320 threads): warp 0 = producers (lane 0: cp.async.bulk of the
+// conv1 pixel blocks, lane 1: the FC weight blocks; mbarrier complete_tx);
+// warp 1 = TMEM allocator + lane 0 issues every tcgen05.cp/mma/commit;
+// warps 2..9 = two epilogue groups (alternate conv2 pixels; tcgen05.ld of
+// their TMEM lane quadrant, one env per thread).
 //
-// Traversal: output columns in chunks of CW = 9 (11 conv1 columns), output
-// rows top to bottom; conv1 rows stream through a 4-row ring in shared memory,
-// so each conv1 block is loaded ~11/9 times and every tap's A operand is a
-// descriptor into the ring (no im2col copy).
+// Traversal: output columns in chunks of CW = 7 (9 conv1 columns), output
+// rows top to bottom. conv1 rows land in shared memory (2-row staging ring)
+// and are copied into a 4-row ring in TMEM (tcgen05.cp 128x256b per block):
+// conv2's A operands are read from TMEM (the "TS" MMA form), so the tensor
+// core's shared-memory reads per conv2 tap are the 1 KB weight block only,
+// not the 4 KB activation block. Each conv1 block is loaded ~9/7 times and
+// every tap's A operand is a TMEM address into the ring (no im2col copy).
 #pragma once
 #include <cuda_bf16.h>
 #include <stdint.h>
@@ -54,8 +58,13 @@ __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// A pipeline bug must not hang the GPU: after ~2^31 cycles (> 1 s) of waiting
+// on one phase the kernel traps (the launch fails with an error instead).
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    if (mbar_try(bar, parity)) return;
+    const long long t0 = clock64();
     while (!mbar_try(bar, parity)) {
+        if (clock64() - t0 > (1ll << 31)) __trap();
     }
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
@@ -92,6 +101,19 @@ __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b
         "l"(a), "l"(b), "r"(idesc), "r"(acc)
         : "memory");
 }
+// A operand from TMEM (a_tmem: 128 lanes x 8 columns per K = 16 step), B from shared memory
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                            uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+// shared memory (UMMA descriptor) -> TMEM, 128 rows x 256 bits: one 128 x 16 bf16 block
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+    asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
@@ -125,26 +147,35 @@ struct TrunkParams {
     int P1, NA;
 };
 
-constexpr int TK_CW = 9;                      // output columns per chunk
+constexpr int TK_CW = 7;                      // output columns per chunk
 constexpr int TK_RC = TK_CW + 2;              // conv1 columns per ring row
-constexpr int TK_RING = 4;                    // conv1 rows in flight
-constexpr int TK_W3 = 2;                      // FC weight blocks in flight
-constexpr int TK_A3 = 3;                      // conv2 activation blocks (FC A operand)
+constexpr int TK_SRING = 2;                   // conv1 rows staged in shared memory (bulk-copy landing)
+constexpr int TK_TRING = 4;                   // conv1 rows resident in TMEM (conv2 A operands)
+constexpr int TK_W3 = 8;                      // FC weight blocks in flight
+constexpr int TK_A3 = 4;                      // conv2 activation blocks (FC A operand)
 constexpr int TK_D2 = 4;                      // conv2 accumulator slots in TMEM (32 columns each)
 constexpr int TK_LAG = 2;                     // FC of pixel i is issued after conv2 of pixel i + LAG
+constexpr int TK_EPI = 2;                     // epilogue warp groups (pixel i -> group i % 2)
+constexpr int TK_THREADS = 64 + 128 * TK_EPI;
 constexpr int TK_MAXNA = 16;
 constexpr uint32_t TK_BLK = 4096;             // one 128 x 16 bf16 block
+// TMEM columns: conv1 ring (8 per block), conv2 accumulators, FC accumulator
+constexpr uint32_t TK_T_A = 0;
+constexpr uint32_t TK_T_D2 = TK_T_A + TK_TRING * TK_RC * 8;  // 288
+constexpr uint32_t TK_T_D3 = TK_T_D2 + TK_D2 * 32;           // 416
+static_assert(TK_T_D3 + 64 <= 512, "TMEM budget");
+static_assert(TK_D2 % TK_EPI == 0 && TK_A3 % TK_EPI == 0, "ring slots must map to one epilogue group");
 constexpr uint32_t TK_OFF_RING = 0;
-constexpr uint32_t TK_OFF_W2 = TK_OFF_RING + TK_RING * TK_RC * TK_BLK;  // 180224
-constexpr uint32_t TK_OFF_W3 = TK_OFF_W2 + 9 * 1024;                     // 189440
-constexpr uint32_t TK_OFF_A3 = TK_OFF_W3 + TK_W3 * 4096;                 // 197632
-constexpr uint32_t TK_OFF_HEAD = TK_OFF_A3 + TK_A3 * 8192;               // 222208
-constexpr uint32_t TK_OFF_BIAS = TK_OFF_HEAD + (TK_MAXNA + 1) * 64 * 4;  // 226560
+constexpr uint32_t TK_OFF_W2 = TK_OFF_RING + TK_SRING * TK_RC * TK_BLK;  // 73728
+constexpr uint32_t TK_OFF_W3 = TK_OFF_W2 + 9 * 1024;
+constexpr uint32_t TK_OFF_A3 = TK_OFF_W3 + TK_W3 * 4096;
+constexpr uint32_t TK_OFF_HEAD = TK_OFF_A3 + TK_A3 * 8192;
+constexpr uint32_t TK_OFF_BIAS = TK_OFF_HEAD + (TK_MAXNA + 1) * 64 * 4;
 constexpr uint32_t TK_OFF_BAR = (TK_OFF_BIAS + (32 + 64 + TK_MAXNA + 1) * 4 + 7) & ~7u;  // 8-byte aligned
-constexpr int TK_NBAR = 2 * TK_RING + 2 * TK_W3 + 2 * TK_D2 + 2 * TK_A3 + 2;
+constexpr int TK_NBAR = 2 * TK_SRING + 2 * TK_W3 + 2 * TK_D2 + 2 * TK_A3 + 2;
 constexpr uint32_t TK_SMEM = TK_OFF_BAR + TK_NBAR * 8 + 16;
 
-__global__ void __launch_bounds__(192, 1) trunk_kernel(const TrunkParams p) {
+__global__ void __launch_bounds__(TK_THREADS, 1) trunk_kernel(const TrunkParams p) {
     extern __shared__ __align__(1024) uint8_t sm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int P1 = p.P1, P2 = P1 - 2, NP1 = P1 * P1, NP2 = P2 * P2;
@@ -155,14 +186,14 @@ __global__ void __launch_bounds__(192, 1) trunk_kernel(const TrunkParams p) {
     const uint32_t b0 = tc::su32(bars);
     auto BAR = [&](int i) { return b0 + 8u * (uint32_t)i; };
     // barrier ids
-    const int C1F = 0, C1E = C1F + TK_RING, W3F = C1E + TK_RING, W3E = W3F + TK_W3, D2F = W3E + TK_W3,
+    const int C1F = 0, C1E = C1F + TK_SRING, W3F = C1E + TK_SRING, W3E = W3F + TK_W3, D2F = W3E + TK_W3,
               D2E = D2F + TK_D2, A3F = D2E + TK_D2, A3E = A3F + TK_A3, D3F = A3E + TK_A3, W2F = D3F + 1;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sm + TK_OFF_BAR + TK_NBAR * 8);
     float *head = reinterpret_cast<float *>(sm + TK_OFF_HEAD);
     float *bias2 = reinterpret_cast<float *>(sm + TK_OFF_BIAS), *bias3 = bias2 + 32, *biash = bias3 + 64;
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < TK_RING; i++) tc::mbar_init(BAR(C1F + i), 1), tc::mbar_init(BAR(C1E + i), 1);
+        for (int i = 0; i < TK_SRING; i++) tc::mbar_init(BAR(C1F + i), 1), tc::mbar_init(BAR(C1E + i), 1);
         for (int i = 0; i < TK_W3; i++) tc::mbar_init(BAR(W3F + i), 1), tc::mbar_init(BAR(W3E + i), 1);
         for (int i = 0; i < TK_D2; i++) tc::mbar_init(BAR(D2F + i), 1), tc::mbar_init(BAR(D2E + i), 128);
         for (int i = 0; i < TK_A3; i++) tc::mbar_init(BAR(A3F + i), 128), tc::mbar_init(BAR(A3E + i), 1);
@@ -174,8 +205,8 @@ __global__ void __launch_bounds__(192, 1) trunk_kernel(const TrunkParams p) {
     for (int i = threadIdx.x; i < 32; i += blockDim.x) bias2[i] = p.b2[i];
     for (int i = threadIdx.x; i < 64; i += blockDim.x) bias3[i] = p.b3[i];
     for (int i = threadIdx.x; i < p.NA + 1; i += blockDim.x) biash[i] = p.bh[i];
-    if (warp == 1) {  // TMEM: 4 x 32 conv2 columns + 64 FC columns -> 256
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(tc::su32(tmem_slot))
+    if (warp == 1) {  // TMEM: conv1 ring + conv2 accumulators + FC accumulator (480 of 512 columns)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(tc::su32(tmem_slot))
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -183,31 +214,34 @@ __global__ void __launch_bounds__(192, 1) trunk_kernel(const TrunkParams p) {
     __syncthreads();
     tc::tc_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t T_D3 = tmem + TK_D2 * 32;
+    const uint32_t T_D3 = tmem + TK_T_D3;
 
     if (warp == 0) {
-        if (lane == 0) {  // ---------------- producer ----------------
+        // ---------------- producers: lane 0 streams the conv1 rows, lane 1 the
+        // FC weight blocks (independent threads, so neither stream can block
+        // the other: the FC of a pixel is issued LAG pixels after its conv2)
+        if (lane == 0) {
             const uint8_t *c1 = reinterpret_cast<const uint8_t *>(p.c1) + (size_t)tile * NP1 * TK_BLK;
-            const uint8_t *w3 = reinterpret_cast<const uint8_t *>(p.w3);
             tc::mbar_expect_tx(BAR(W2F), 9 * 1024);
             tc::bulk_g2s(s0 + TK_OFF_W2, p.w2, 9 * 1024, BAR(W2F));
-            int L = 0, pix = 0;
-            auto load_row = [&](int cx, int r) {
-                const int slot = L % TK_RING;
-                if (L >= TK_RING) tc::mbar_wait(BAR(C1E + slot), (uint32_t)((L / TK_RING - 1) & 1));
+            int L = 0;
+            for (int cx = 0; cx < nch; cx++) {
                 const int ncol = min(TK_RC, P1 - cx * TK_CW);
-                tc::mbar_expect_tx(BAR(C1F + slot), (uint32_t)ncol * TK_BLK);
-                for (int j = 0; j < ncol; j++)
-                    tc::bulk_g2s(s0 + TK_OFF_RING + (uint32_t)(slot * TK_RC + j) * TK_BLK,
-                                 c1 + (size_t)(r * P1 + cx * TK_CW + j) * TK_BLK, TK_BLK, BAR(C1F + slot));
-                L++;
-            };
+                for (int r = 0; r < P1; r++, L++) {
+                    const int slot = L % TK_SRING;
+                    if (L >= TK_SRING) tc::mbar_wait(BAR(C1E + slot), (uint32_t)((L / TK_SRING - 1) & 1));
+                    tc::mbar_expect_tx(BAR(C1F + slot), (uint32_t)ncol * TK_BLK);
+                    for (int j = 0; j < ncol; j++)
+                        tc::bulk_g2s(s0 + TK_OFF_RING + (uint32_t)(slot * TK_RC + j) * TK_BLK,
+                                     c1 + (size_t)(r * P1 + cx * TK_CW + j) * TK_BLK, TK_BLK, BAR(C1F + slot));
+                }
+            }
+        } else if (lane == 1) {
+            const uint8_t *w3 = reinterpret_cast<const uint8_t *>(p.w3);
+            int pix = 0;
             for (int cx = 0; cx < nch; cx++) {
                 const int cw = min(TK_CW, P2 - cx * TK_CW);
-                load_row(cx, 0);
-                load_row(cx, 1);
-                for (int y = 0; y < P2; y++) {
-                    load_row(cx, y + 2);
+                for (int y = 0; y < P2; y++)
                     for (int xl = 0; xl < cw; xl++, pix++) {
                         const int slot = pix % TK_W3;
                         if (pix >= TK_W3) tc::mbar_wait(BAR(W3E + slot), (uint32_t)((pix / TK_W3 - 1) & 1));
@@ -215,14 +249,13 @@ __global__ void __launch_bounds__(192, 1) trunk_kernel(const TrunkParams p) {
                         tc::bulk_g2s(s0 + TK_OFF_W3 + slot * 4096u,
                                      w3 + (size_t)(y * P2 + cx * TK_CW + xl) * 4096, 4096, BAR(W3F + slot));
                     }
-                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ---------------- MMA issuer ----------------
             constexpr uint32_t ID2 = tc::idesc_bf16(128, 32), ID3 = tc::idesc_bf16(128, 64);
             tc::mbar_wait(BAR(W2F), 0);
-            int Lw = 0;  // conv1 rows waited for
+            int Lc = 0;  // conv1 rows copied into TMEM
             int pix = 0;
             auto fc = [&](int i) {  // D3 += relu(conv2)(pixel i) x W3(pixel i)
                 const int a = i % TK_A3, w = i % TK_W3;
@@ -239,10 +272,23 @@ __global__ void __launch_bounds__(192, 1) trunk_kernel(const TrunkParams p) {
             };
             for (int cx = 0; cx < nch; cx++) {
                 const int cw = min(TK_CW, P2 - cx * TK_CW);
+                const int ncol = min(TK_RC, P1 - cx * TK_CW);
                 const int L0 = cx * P1;
                 for (int y = 0; y < P2; y++) {
-                    for (; Lw <= L0 + y + 2; Lw++) tc::mbar_wait(BAR(C1F + Lw % TK_RING), (uint32_t)((Lw / TK_RING) & 1));
-                    tc::tc_after();
+                    // conv1 rows up to y + 2 into the TMEM ring: shared -> TMEM copies run
+                    // in issue order with the MMAs, so the slot of row L - TK_TRING (last
+                    // read by output row y - 2's MMAs, issued before) is free
+                    for (; Lc <= L0 + y + 2; Lc++) {
+                        const int ss = Lc % TK_SRING;
+                        tc::mbar_wait(BAR(C1F + ss), (uint32_t)((Lc / TK_SRING) & 1));
+                        tc::tc_after();
+                        const uint32_t ta = tmem + TK_T_A + (uint32_t)((Lc % TK_TRING) * TK_RC) * 8u;
+                        for (int j = 0; j < ncol; j++)
+                            tc::tmem_cp_128x256b(ta + j * 8u,
+                                                 tc::sdesc(s0 + TK_OFF_RING + (uint32_t)(ss * TK_RC + j) * TK_BLK,
+                                                           2048, 128));
+                        tc::mma_commit(BAR(C1E + ss));  // the shared slot is free once the copies land
+                    }
                     for (int xl = 0; xl < cw; xl++, pix++) {
                         const int s = pix % TK_D2;
                         if (pix >= TK_D2) {
@@ -252,33 +298,34 @@ __global__ void __launch_bounds__(192, 1) trunk_kernel(const TrunkParams p) {
 #pragma unroll
                         for (int t = 0; t < 9; t++) {
                             const int dy = t / 3, dx = t % 3;
-                            const uint32_t blk =
-                                s0 + TK_OFF_RING + (uint32_t)(((L0 + y + dy) % TK_RING) * TK_RC + xl + dx) * TK_BLK;
-                            tc::mma_bf16(tmem + s * 32, tc::sdesc(blk, 2048, 128),
-                                         tc::sdesc(s0 + TK_OFF_W2 + t * 1024u, 512, 128), ID2, t > 0 ? 1u : 0u);
+                            const uint32_t a_t =
+                                tmem + TK_T_A + (uint32_t)(((L0 + y + dy) % TK_TRING) * TK_RC + xl + dx) * 8u;
+                            tc::mma_bf16_ts(tmem + TK_T_D2 + s * 32, a_t,
+                                            tc::sdesc(s0 + TK_OFF_W2 + t * 1024u, 512, 128), ID2, t > 0 ? 1u : 0u);
                         }
                         tc::mma_commit(BAR(D2F + s));
                         if (pix >= TK_LAG) fc(pix - TK_LAG);
                     }
-                    tc::mma_commit(BAR(C1E + (L0 + y) % TK_RING));  // conv1 row y is no longer read
                 }
-                tc::mma_commit(BAR(C1E + (L0 + P2) % TK_RING));
-                tc::mma_commit(BAR(C1E + (L0 + P2 + 1) % TK_RING));
             }
             for (int i = max(pix - TK_LAG, 0); i < pix; i++) fc(i);
             tc::mma_commit(BAR(D3F));
         }
-    } else {  // ---------------- epilogue: warps 2..5, one env (TMEM lane) per thread ----------------
+    } else {  // ---------------- epilogue: TK_EPI groups of 4 warps, one env (TMEM lane) per thread ----------------
+        const int grp = (warp - 2) >> 2;  // pixel i is handled by group i % TK_EPI
         const int q = warp & 3;           // TMEM lane quadrant this warp may access
         const int m = q * 32 + lane;      // env row within the tile
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-        for (int i = 0; i < NP2; i++) {
+        float b2r[32];
+#pragma unroll
+        for (int c = 0; c < 32; c++) b2r[c] = bias2[c];
+        for (int i = grp; i < NP2; i += TK_EPI) {
             const int s = i % TK_D2, a = i % TK_A3;
             tc::mbar_wait(BAR(D2F + s), (uint32_t)((i / TK_D2) & 1));
             tc::tc_after();
             uint32_t r[32];
             __syncwarp();
-            tc::tmem_ld32(tmem + lane_off + s * 32, r);
+            tc::tmem_ld32(tmem + TK_T_D2 + lane_off + s * 32, r);
             tc::tmem_wait_ld();
             tc::tc_before();
             tc::mbar_arrive(BAR(D2E + s));
@@ -290,7 +337,7 @@ __global__ void __launch_bounds__(192, 1) trunk_kernel(const TrunkParams p) {
 #pragma unroll
                 for (int j = 0; j < 4; j++) {
                     const int c = kc * 8 + 2 * j;
-                    float x0 = __uint_as_float(r[c]) + bias2[c], x1 = __uint_as_float(r[c + 1]) + bias2[c + 1];
+                    float x0 = __uint_as_float(r[c]) + b2r[c], x1 = __uint_as_float(r[c + 1]) + b2r[c + 1];
                     x0 = x0 > 0.f ? x0 : 0.f;
                     x1 = x1 > 0.f ? x1 : 0.f;
                     __nv_bfloat162 h2 = __floats2bfloat162_rn(x0, x1);
@@ -302,30 +349,32 @@ __global__ void __launch_bounds__(192, 1) trunk_kernel(const TrunkParams p) {
             tc::fence_proxy_async();
             tc::mbar_arrive(BAR(A3F + a));
         }
-        tc::mbar_wait(BAR(D3F), 0);
-        tc::tc_after();
-        __syncwarp();
-        float h[64];
+        if (grp == 0) {
+            tc::mbar_wait(BAR(D3F), 0);
+            tc::tc_after();
+            __syncwarp();
+            float h[64];
 #pragma unroll
-        for (int half = 0; half < 2; half++) {
-            uint32_t r[32];
-            tc::tmem_ld32(T_D3 + lane_off + half * 32, r);
-            tc::tmem_wait_ld();
+            for (int half = 0; half < 2; half++) {
+                uint32_t r[32];
+                tc::tmem_ld32(T_D3 + lane_off + half * 32, r);
+                tc::tmem_wait_ld();
 #pragma unroll
-            for (int j = 0; j < 32; j++) {
-                const float v = __uint_as_float(r[j]) + bias3[half * 32 + j];
-                h[half * 32 + j] = v > 0.f ? v : 0.f;
+                for (int j = 0; j < 32; j++) {
+                    const float v = __uint_as_float(r[j]) + bias3[half * 32 + j];
+                    h[half * 32 + j] = v > 0.f ? v : 0.f;
+                }
             }
-        }
-        const long long env = tile * 128 + m;
-        if (env < p.B) {
-            for (int o = 0; o <= p.NA; o++) {
-                const float *wr = head + o * 64;
-                float acc = biash[o];
+            const long long env = tile * 128 + m;
+            if (env < p.B) {
+                for (int o = 0; o <= p.NA; o++) {
+                    const float *wr = head + o * 64;
+                    float acc = biash[o];
 #pragma unroll
-                for (int j = 0; j < 64; j++) acc = fmaf(h[j], wr[j], acc);
-                if (o < p.NA) p.logits[env * p.NA + o] = acc;
-                else p.value[env] = acc;
+                    for (int j = 0; j < 64; j++) acc = fmaf(h[j], wr[j], acc);
+                    if (o < p.NA) p.logits[env * p.NA + o] = acc;
+                    else p.value[env] = acc;
+                }
             }
         }
     }
@@ -333,7 +382,7 @@ __global__ void __launch_bounds__(192, 1) trunk_kernel(const TrunkParams p) {
     __syncthreads();
     if (warp == 1) {
         tc::tc_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
     }
 }
 

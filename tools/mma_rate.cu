@@ -1,0 +1,92 @@
+// mma_rate.cu -- tcgen05.mma issue rate for the policy trunk's shapes (B200).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_2408_12525_b200/csrc tools/mma_rate.cu -o tools/mma_rate
+// One CTA per SM; one thread issues R back-to-back bf16 MMAs (M = 128, K = 16,
+// N in {32, 64, 128, 256}) into one TMEM accumulator, A from shared memory (SS)
+// or TMEM (TS), then commits once. Prints cycles per MMA and the implied
+// per-SM MAC rate. Operands are zero (only timing matters).
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#include "trunk_kernel.cuh"
+
+using namespace lg;
+
+template <int N, bool TS, int NACC = 1, int CEVERY = 0>
+__global__ void __launch_bounds__(128, 1) rate_kernel(int R, long long *out) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ uint64_t bar, bar2;
+    __shared__ uint32_t slot;
+    const uint32_t s0 = tc::su32(sm);
+    for (int i = threadIdx.x; i < 32768 / 4; i += blockDim.x) reinterpret_cast<uint32_t *>(sm)[i] = 0;
+    tc::fence_proxy_async();
+    if (threadIdx.x == 0) {
+        tc::mbar_init(tc::su32(&bar), 1);
+        tc::mbar_init(tc::su32(&bar2), (1 << 20) - 1);
+        tc::fence_barrier_init();
+    }
+    if (threadIdx.x < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(tc::su32(&slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc::tc_before();
+    __syncthreads();
+    tc::tc_after();
+    const uint32_t tmem = slot;
+    if (threadIdx.x == 0) {
+        constexpr uint32_t ID = tc::idesc_bf16(128, N);
+        const uint64_t bd = tc::sdesc(s0 + 16384, (N / 8) * 128, 128);
+        const uint64_t ad = tc::sdesc(s0, 2048, 128);
+        if (TS) tc::tmem_cp_128x256b(tmem + 256, ad);
+        long long t0 = clock64();
+        for (int i = 0; i < R; i++) {
+            const uint32_t d = tmem + (uint32_t)((i % NACC) * (N < 64 ? N : 64));
+            if (TS) tc::mma_bf16_ts(d, tmem + 256, bd, ID, i >= NACC);
+            else tc::mma_bf16(d, ad, bd, ID, i >= NACC);
+            if (CEVERY && (i + 1) % CEVERY == 0) tc::mma_commit(tc::su32(&bar2));
+        }
+        tc::mma_commit(tc::su32(&bar));
+        tc::mbar_wait(tc::su32(&bar), 0);
+        long long t1 = clock64();
+        if (blockIdx.x == 0) out[0] = t1 - t0;
+    }
+    tc::tc_before();
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        tc::tc_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+}
+
+template <int N, bool TS, int NACC = 1, int CEVERY = 0>
+void run(long long *d) {
+    const int R = 4096;
+    cudaFuncSetAttribute(rate_kernel<N, TS, NACC, CEVERY>, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768);
+    rate_kernel<N, TS, NACC, CEVERY><<<148, 128, 32768>>>(R, d);
+    rate_kernel<N, TS, NACC, CEVERY><<<148, 128, 32768>>>(R, d);
+    long long c = 0;
+    cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+    cudaError_t e = cudaGetLastError();
+    printf("%s N=%3d acc=%d commit/%d: %.1f cycles/MMA, %.0f MAC/cycle/SM %s\n", TS ? "TS" : "SS", N, NACC, CEVERY, (double)c / R,
+           128.0 * N * 16 * R / c, e == cudaSuccess ? "" : cudaGetErrorString(e));
+}
+
+int main() {
+    long long *d;
+    cudaMalloc(&d, 8);
+    run<32, false>(d);
+    run<64, false>(d);
+    run<96, false>(d);
+    run<128, false>(d);
+    run<256, false>(d);
+    run<32, true>(d);
+    run<96, true>(d);
+    run<128, true>(d);
+    run<32, true, 4>(d);
+    run<32, true, 1, 1>(d);
+    run<32, true, 1, 2>(d);
+    run<32, true, 1, 4>(d);
+    run<32, true, 1, 9>(d);
+    run<32, true, 1, 18>(d);
+    run<128, true, 1, 9>(d);
+    return 0;
+}
