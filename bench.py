@@ -66,6 +66,19 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
+def load_tensor_peak():
+    """Dense bf16 TFLOP/s from MEASURED_PEAKS.json (cuBLAS), else the nominal 2250."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        for k in ("bf16_tflops", "tensor_bf16_tflops", "bf16_dense_tflops"):
+            if k in d:
+                return float(d[k])
+    except Exception:
+        pass
+    return 2250.0
+
+
 def load_traffic(config: str):
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
@@ -586,6 +599,28 @@ def main():
         del e, m0, conv, obs_f, bits_o
         torch.cuda.empty_cache()
 
+        # the default trunk on the tensor cores: lg_conv1_bits (bf16 tiles) +
+        # lg_policy_trunk (conv2 + FC as tcgen05 MMAs with TMEM accumulators, heads)
+        from paper_2408_12525_b200.policy import TrunkPolicy
+        e = BatchEnv(cfg, Bp, seed=0, device=dev, global_offset=offset, validate=False, obs_dtype="bits")
+        bits_o = e.reset()
+        shp = e.observation_shape
+        m0 = init_policy(default_arch(shp[1], shp[0], cfg.n_actions), seed=0).to(dev)
+        tp = TrunkPolicy(m0, shp)
+        c1t = tp.conv1_tiles(bits_o, Bp)
+        t_c1t = time_ms(lambda: tp.conv1_tiles(bits_o, Bp))
+        t_tp = time_ms(lambda: tp(bits_o, Bp)) - t_c1t
+        P2 = shp[1] - 4
+        tflop = Bp * (P2 * P2 * 32 * 16 * 9 * 2 + 32 * P2 * P2 * 64 * 2) / 1e12
+        tf_peak = load_tensor_peak()
+        pol["tcgen05_trunk"] = {
+            "conv1_tiles_ms": t_c1t, "conv1_tiles_gbs": c1t.numel() * 2 / t_c1t / 1e6,
+            "trunk_ms": t_tp, "trunk_tflops": tflop / (t_tp / 1e3), "tensor_peak_tflops": tf_peak,
+            "frac_of_tensor_peak": tflop / (t_tp / 1e3) / tf_peak if tf_peak else None,
+            "note": "conv2 (16->32, 3x3) + FC (32*P2^2 -> 64) algorithmic flops; bf16 operands, fp32 accumulate"}
+        del e, m0, tp, c1t, bits_o
+        torch.cuda.empty_cache()
+        pol["bits_obs_tcgen05_trunk"] = rollout_rate("bits", lambda m, shp: TrunkPolicy(m, shp))
         pol["float32_obs_torch_f32"] = rollout_rate("float32", lambda m, shp: m)
         pol["float32_obs_torch_bf16"] = rollout_rate("float32", autocast_policy)
         pol["bits_obs_conv1_bits_bf16"] = rollout_rate("bits", lambda m, shp: PackedPolicy(m, shp, bf16=True))

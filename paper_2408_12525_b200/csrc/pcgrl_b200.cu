@@ -1120,6 +1120,13 @@ extern "C" int lg_policy_trunk(const void *c1_tiles, int64_t n_envs, int P1, con
     return LG_OK;
 }
 
+#ifdef TK_PROF
+extern "C" int lg_trunk_prof(long long *host, int n_blocks) {
+    CU(cudaMemcpyFromSymbol(host, g_tk_prof, (size_t)n_blocks * 16 * sizeof(long long)));
+    return LG_OK;
+}
+#endif
+
 extern "C" int lg_export_state(lg_env *e, const lg_state *dst, void *stream) {
     if (!e || !dst) {
         set_err("null argument");

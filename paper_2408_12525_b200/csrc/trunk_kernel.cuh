@@ -19,24 +19,28 @@
 // Data layout (all bf16, prepared by conv1_bits_kernel / the host):
 //   c1  [ceil(B/128)][P1*P1][2048]: per pixel, 128 envs x 16 channels,
 //       element (m, k) at ((k/8)*16 + m/8)*64 + (m%8)*8 + k%8
-//   w2  [9 taps][512]: N = 32 out x K = 16 in, ((k/8)*4 + n/8)*64 + (n%8)*8 + k%8
+//   w2  [3 dy][1536]: N = 96 (taps dx = 2, 1, 0 x 32 out channels) x K = 16 in,
+//       element (n, k) at ((k/8)*12 + n/8)*64 + (n%8)*8 + k%8
 //   w3  [P2*P2][2048]: per conv2 pixel p, N = 64 x K = 32 channels, the FC
 //       weights W[n, c*P2*P2 + p] (torch flattens [C, H, W]),
 //       ((k/8)*8 + n/8)*64 + (n%8)*8 + k%8
 //
 // Warp roles (320 threads): warp 0 = producers (lane 0: cp.async.bulk of the
 // conv1 pixel blocks, lane 1: the FC weight blocks; mbarrier complete_tx);
-// warp 1 = TMEM allocator + lane 0 issues every tcgen05.cp/mma/commit;
-// warps 2..9 = two epilogue groups (alternate conv2 pixels; tcgen05.ld of
-// their TMEM lane quadrant, one env per thread).
+// warp 1 = TMEM allocator + MMA issuer (the warp runs the loop, an elected
+// lane issues every tcgen05.mma/commit); warps
+// 2..9 = two epilogue groups (alternate output rows; tcgen05.ld of their TMEM
+// lane quadrant, one env per thread).
 //
-// Traversal: output columns in chunks of CW = 7 (9 conv1 columns), output
-// rows top to bottom. conv1 rows land in shared memory (2-row staging ring)
-// and are copied into a 4-row ring in TMEM (tcgen05.cp 128x256b per block):
-// conv2's A operands are read from TMEM (the "TS" MMA form), so the tensor
-// core's shared-memory reads per conv2 tap are the 1 KB weight block only,
-// not the 4 KB activation block. Each conv1 block is loaded ~9/7 times and
-// every tap's A operand is a TMEM address into the ring (no im2col copy).
+// Traversal: output columns in chunks of CW = 7 (9 conv1 columns), output rows
+// top to bottom, conv1 rows streaming through a 4-row ring in shared memory.
+// tcgen05.mma costs >= 46 cycles per instruction for N <= 64 (tools/mma_rate.cu),
+// so conv2 is issued with N = 96: conv1 block (row y+dy, column c) times the
+// weights of the three taps (dy, 2), (dy, 1), (dy, 0) side by side lands on
+// output pixels c-2, c-1, c of row y in one MMA (narrower at the chunk edges).
+// One output row's 7 pixels are one accumulator row in TMEM (224 columns, two
+// rows double-buffered); every MMA accumulates into accumulators the epilogue
+// zeroes after reading them. 27 conv2 MMAs per 7 output pixels instead of 63.
 #pragma once
 #include <cuda_bf16.h>
 #include <stdint.h>
@@ -77,6 +81,12 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                  "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile("{\n.reg .b32 r;\n.reg .pred p;\nelect.sync r|p, 0xffffffff;\nselp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(pred));
+    return pred != 0;
 }
 __device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -130,6 +140,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         : "memory");
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// zero 32 consecutive columns of this warp's 32 lanes
+__device__ __forceinline__ void tmem_zero32(uint32_t taddr) {
+    const uint32_t z = 0;
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+        "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+        "r"(z)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 }  // namespace tc
 
@@ -147,56 +167,78 @@ struct TrunkParams {
     int P1, NA;
 };
 
+#ifdef TK_PROF  // cycle accounting of the MMA issuer and one epilogue thread (tools/trunk_prof.py)
+__device__ long long g_tk_prof[1024][16];
+#define TKP(k, v) (prof[k] += (v))
+#else
+#define TKP(k, v)
+#endif
 constexpr int TK_CW = 7;                      // output columns per chunk
 constexpr int TK_RC = TK_CW + 2;              // conv1 columns per ring row
-constexpr int TK_SRING = 2;                   // conv1 rows staged in shared memory (bulk-copy landing)
-constexpr int TK_TRING = 4;                   // conv1 rows resident in TMEM (conv2 A operands)
-constexpr int TK_W3 = 8;                      // FC weight blocks in flight
-constexpr int TK_A3 = 4;                      // conv2 activation blocks (FC A operand)
-constexpr int TK_D2 = 4;                      // conv2 accumulator slots in TMEM (32 columns each)
-constexpr int TK_LAG = 2;                     // FC of pixel i is issued after conv2 of pixel i + LAG
-constexpr int TK_EPI = 2;                     // epilogue warp groups (pixel i -> group i % 2)
+constexpr int TK_RING = 4;                    // conv1 rows in shared memory
+constexpr int TK_W3 = 8;                      // FC weight blocks in flight (released in pairs)
+constexpr int TK_EPI = 2;                     // epilogue warp groups (output row R -> group R % 2)
+constexpr int TK_A3G = 2;                     // conv2 activation blocks (FC A operand) per group
 constexpr int TK_THREADS = 64 + 128 * TK_EPI;
 constexpr int TK_MAXNA = 16;
 constexpr uint32_t TK_BLK = 4096;             // one 128 x 16 bf16 block
-// TMEM columns: conv1 ring (8 per block), conv2 accumulators, FC accumulator
-constexpr uint32_t TK_T_A = 0;
-constexpr uint32_t TK_T_D2 = TK_T_A + TK_TRING * TK_RC * 8;  // 288
-constexpr uint32_t TK_T_D3 = TK_T_D2 + TK_D2 * 32;           // 416
+// TMEM columns: one conv2 accumulator row (CW pixels x 32 channels) per epilogue group + FC accumulator
+constexpr uint32_t TK_T_ACC = 0;
+constexpr uint32_t TK_T_D3 = TK_T_ACC + TK_EPI * TK_CW * 32;  // 448
 static_assert(TK_T_D3 + 64 <= 512, "TMEM budget");
-static_assert(TK_D2 % TK_EPI == 0 && TK_A3 % TK_EPI == 0, "ring slots must map to one epilogue group");
+static_assert(TK_CW == 7, "conv2_row dispatch covers chunk widths 1..7");
 constexpr uint32_t TK_OFF_RING = 0;
-constexpr uint32_t TK_OFF_W2 = TK_OFF_RING + TK_SRING * TK_RC * TK_BLK;  // 73728
-constexpr uint32_t TK_OFF_W3 = TK_OFF_W2 + 9 * 1024;
+constexpr uint32_t TK_OFF_W2 = TK_OFF_RING + TK_RING * TK_RC * TK_BLK;  // 147456: 3 x [96 x 16] bf16
+constexpr uint32_t TK_OFF_W3 = TK_OFF_W2 + 3 * 3072;
 constexpr uint32_t TK_OFF_A3 = TK_OFF_W3 + TK_W3 * 4096;
-constexpr uint32_t TK_OFF_HEAD = TK_OFF_A3 + TK_A3 * 8192;
+constexpr uint32_t TK_OFF_HEAD = TK_OFF_A3 + TK_EPI * TK_A3G * 8192;
 constexpr uint32_t TK_OFF_BIAS = TK_OFF_HEAD + (TK_MAXNA + 1) * 64 * 4;
 constexpr uint32_t TK_OFF_BAR = (TK_OFF_BIAS + (32 + 64 + TK_MAXNA + 1) * 4 + 7) & ~7u;  // 8-byte aligned
-constexpr int TK_NBAR = 2 * TK_SRING + 2 * TK_W3 + 2 * TK_D2 + 2 * TK_A3 + 2;
+constexpr int TK_NBAR = 2 * TK_RING + TK_W3 + TK_W3 / 2 + 2 * TK_EPI + 2 * TK_EPI * TK_A3G + 2;
 constexpr uint32_t TK_SMEM = TK_OFF_BAR + TK_NBAR * 8 + 16;
+
+// One output row's conv2 (CW pixels): conv1 block (row y+dy, column c) x the
+// three taps (dy, 2..0) -> pixels c-2..c, N = 96 (narrower at the edges).
+// Fully unrolled so every offset and instruction descriptor is an immediate.
+template <int CW>
+__device__ __forceinline__ void conv2_row(uint32_t acc, const uint64_t (&dr)[3], uint64_t d_w2) {
+#pragma unroll
+    for (int dy = 0; dy < 3; dy++) {
+#pragma unroll
+        for (int c = 0; c < CW + 2; c++) {
+            const int xlo = c - 2 > 0 ? c - 2 : 0, xhi = c < CW - 1 ? c : CW - 1;
+            const int jb = xlo - c + 2, n = 32 * (xhi - xlo + 1);
+            tc::mma_bf16(acc + 32u * xlo, dr[dy] + ((uint32_t)c * TK_BLK >> 4),
+                         d_w2 + ((uint32_t)(dy * 3072 + jb * 512) >> 4), tc::idesc_bf16(128, n), 1u);
+        }
+    }
+}
 
 __global__ void __launch_bounds__(TK_THREADS, 1) trunk_kernel(const TrunkParams p) {
     extern __shared__ __align__(1024) uint8_t sm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int P1 = p.P1, P2 = P1 - 2, NP1 = P1 * P1, NP2 = P2 * P2;
+    const int P1 = p.P1, P2 = P1 - 2, NP1 = P1 * P1;
     const int nch = (P2 + TK_CW - 1) / TK_CW;
+    const int nrows = nch * P2;  // output rows over all chunks
     const long long tile = blockIdx.x;
     const uint32_t s0 = tc::su32(sm);
     uint64_t *bars = reinterpret_cast<uint64_t *>(sm + TK_OFF_BAR);
     const uint32_t b0 = tc::su32(bars);
     auto BAR = [&](int i) { return b0 + 8u * (uint32_t)i; };
     // barrier ids
-    const int C1F = 0, C1E = C1F + TK_SRING, W3F = C1E + TK_SRING, W3E = W3F + TK_W3, D2F = W3E + TK_W3,
-              D2E = D2F + TK_D2, A3F = D2E + TK_D2, A3E = A3F + TK_A3, D3F = A3E + TK_A3, W2F = D3F + 1;
+    const int C1F = 0, C1E = C1F + TK_RING, W3F = C1E + TK_RING, W3E = W3F + TK_W3, ACF = W3E + TK_W3 / 2,
+              ACE = ACF + TK_EPI, A3F = ACE + TK_EPI, A3E = A3F + TK_EPI * TK_A3G, D3F = A3E + TK_EPI * TK_A3G,
+              W2F = D3F + 1;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sm + TK_OFF_BAR + TK_NBAR * 8);
     float *head = reinterpret_cast<float *>(sm + TK_OFF_HEAD);
     float *bias2 = reinterpret_cast<float *>(sm + TK_OFF_BIAS), *bias3 = bias2 + 32, *biash = bias3 + 64;
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < TK_SRING; i++) tc::mbar_init(BAR(C1F + i), 1), tc::mbar_init(BAR(C1E + i), 1);
-        for (int i = 0; i < TK_W3; i++) tc::mbar_init(BAR(W3F + i), 1), tc::mbar_init(BAR(W3E + i), 1);
-        for (int i = 0; i < TK_D2; i++) tc::mbar_init(BAR(D2F + i), 1), tc::mbar_init(BAR(D2E + i), 128);
-        for (int i = 0; i < TK_A3; i++) tc::mbar_init(BAR(A3F + i), 128), tc::mbar_init(BAR(A3E + i), 1);
+        for (int i = 0; i < TK_RING; i++) tc::mbar_init(BAR(C1F + i), 1), tc::mbar_init(BAR(C1E + i), 1);
+        for (int i = 0; i < TK_W3; i++) tc::mbar_init(BAR(W3F + i), 1);
+        for (int i = 0; i < TK_W3 / 2; i++) tc::mbar_init(BAR(W3E + i), 1);
+        for (int i = 0; i < TK_EPI; i++) tc::mbar_init(BAR(ACF + i), 1), tc::mbar_init(BAR(ACE + i), 128);
+        for (int i = 0; i < TK_EPI * TK_A3G; i++) tc::mbar_init(BAR(A3F + i), 128), tc::mbar_init(BAR(A3E + i), 1);
         tc::mbar_init(BAR(D3F), 1);
         tc::mbar_init(BAR(W2F), 1);
         tc::fence_barrier_init();
@@ -205,7 +247,7 @@ __global__ void __launch_bounds__(TK_THREADS, 1) trunk_kernel(const TrunkParams 
     for (int i = threadIdx.x; i < 32; i += blockDim.x) bias2[i] = p.b2[i];
     for (int i = threadIdx.x; i < 64; i += blockDim.x) bias3[i] = p.b3[i];
     for (int i = threadIdx.x; i < p.NA + 1; i += blockDim.x) biash[i] = p.bh[i];
-    if (warp == 1) {  // TMEM: conv1 ring + conv2 accumulators + FC accumulator (480 of 512 columns)
+    if (warp == 1) {  // TMEM: two conv2 accumulator rows + the FC accumulator (512 columns)
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(tc::su32(tmem_slot))
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
@@ -219,17 +261,17 @@ __global__ void __launch_bounds__(TK_THREADS, 1) trunk_kernel(const TrunkParams 
     if (warp == 0) {
         // ---------------- producers: lane 0 streams the conv1 rows, lane 1 the
         // FC weight blocks (independent threads, so neither stream can block
-        // the other: the FC of a pixel is issued LAG pixels after its conv2)
+        // the other: a row's FCs are issued after the next row's conv2)
         if (lane == 0) {
             const uint8_t *c1 = reinterpret_cast<const uint8_t *>(p.c1) + (size_t)tile * NP1 * TK_BLK;
-            tc::mbar_expect_tx(BAR(W2F), 9 * 1024);
-            tc::bulk_g2s(s0 + TK_OFF_W2, p.w2, 9 * 1024, BAR(W2F));
+            tc::mbar_expect_tx(BAR(W2F), 3 * 3072);
+            tc::bulk_g2s(s0 + TK_OFF_W2, p.w2, 3 * 3072, BAR(W2F));
             int L = 0;
             for (int cx = 0; cx < nch; cx++) {
                 const int ncol = min(TK_RC, P1 - cx * TK_CW);
                 for (int r = 0; r < P1; r++, L++) {
-                    const int slot = L % TK_SRING;
-                    if (L >= TK_SRING) tc::mbar_wait(BAR(C1E + slot), (uint32_t)((L / TK_SRING - 1) & 1));
+                    const int slot = L % TK_RING;
+                    if (L >= TK_RING) tc::mbar_wait(BAR(C1E + slot), (uint32_t)((L / TK_RING - 1) & 1));
                     tc::mbar_expect_tx(BAR(C1F + slot), (uint32_t)ncol * TK_BLK);
                     for (int j = 0; j < ncol; j++)
                         tc::bulk_g2s(s0 + TK_OFF_RING + (uint32_t)(slot * TK_RC + j) * TK_BLK,
@@ -244,7 +286,8 @@ __global__ void __launch_bounds__(TK_THREADS, 1) trunk_kernel(const TrunkParams 
                 for (int y = 0; y < P2; y++)
                     for (int xl = 0; xl < cw; xl++, pix++) {
                         const int slot = pix % TK_W3;
-                        if (pix >= TK_W3) tc::mbar_wait(BAR(W3E + slot), (uint32_t)((pix / TK_W3 - 1) & 1));
+                        if (pix >= TK_W3 && (slot & 1) == 0)  // slots are released in pairs
+                            tc::mbar_wait(BAR(W3E + slot / 2), (uint32_t)((pix / TK_W3 - 1) & 1));
                         tc::mbar_expect_tx(BAR(W3F + slot), 4096);
                         tc::bulk_g2s(s0 + TK_OFF_W3 + slot * 4096u,
                                      w3 + (size_t)(y * P2 + cx * TK_CW + xl) * 4096, 4096, BAR(W3F + slot));
@@ -252,103 +295,170 @@ __global__ void __launch_bounds__(TK_THREADS, 1) trunk_kernel(const TrunkParams 
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // ---------------- MMA issuer ----------------
-            constexpr uint32_t ID2 = tc::idesc_bf16(128, 32), ID3 = tc::idesc_bf16(128, 64);
-            tc::mbar_wait(BAR(W2F), 0);
-            int Lc = 0;  // conv1 rows copied into TMEM
-            int pix = 0;
-            auto fc = [&](int i) {  // D3 += relu(conv2)(pixel i) x W3(pixel i)
-                const int a = i % TK_A3, w = i % TK_W3;
-                tc::mbar_wait(BAR(A3F + a), (uint32_t)((i / TK_A3) & 1));
-                tc::mbar_wait(BAR(W3F + w), (uint32_t)((i / TK_W3) & 1));
+        // ---------------- MMA issuer: the whole warp runs the loop (warp-uniform
+        // values stay in uniform registers), one elected lane issues ----------------
+#ifdef TK_PROF
+        long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tq = clock64(), t0 = tq;
+#define TKT(k)                          \
+    do {                                \
+        const long long _t = clock64(); \
+        TKP(k, _t - tq);                \
+        tq = _t;                        \
+    } while (0)
+#else
+#define TKT(k)
+#endif
+        constexpr uint32_t ID3 = tc::idesc_bf16(128, 64);
+        tc::mbar_wait(BAR(W2F), 0);
+        // descriptor bases; a shared-memory offset is added as (bytes >> 4)
+        const uint64_t d_ring = tc::sdesc(s0 + TK_OFF_RING, 2048, 128);
+        const uint64_t d_w2 = tc::sdesc(s0 + TK_OFF_W2, 1536, 128);
+        const uint64_t d_a3 = tc::sdesc(s0 + TK_OFF_A3, 2048, 128);
+        const uint64_t d_w3 = tc::sdesc(s0 + TK_OFF_W3, 1024, 128);
+        int Lw = 0;   // conv1 rows waited for
+        int pix = 0;  // FC pixels issued (global order)
+        int kg0 = 0, kg1 = 0;  // A3 blocks consumed per epilogue group
+        auto fc_row = [&](int R, int cw) {  // D3 += relu(conv2)(pixel) x W3(pixel) for row R's pixels
+            const int g = R % TK_EPI;
+            int &kg = g ? kg1 : kg0;
+            for (int j = 0; j < cw; j++, pix++, kg++) {
+                const int a = g * TK_A3G + kg % TK_A3G, w = pix % TK_W3;
+                TKT(0);
+                tc::mbar_wait(BAR(A3F + a), (uint32_t)((kg / TK_A3G) & 1));
+                TKT(1);
+                tc::mbar_wait(BAR(W3F + w), (uint32_t)((pix / TK_W3) & 1));
+                TKT(2);
                 tc::tc_after();
-                const uint32_t aa = s0 + TK_OFF_A3 + a * 8192u, ww = s0 + TK_OFF_W3 + w * 4096u;
-#pragma unroll
-                for (int k = 0; k < 2; k++)
-                    tc::mma_bf16(T_D3, tc::sdesc(aa + k * 4096u, 2048, 128), tc::sdesc(ww + k * 2048u, 1024, 128), ID3,
-                                 (i > 0 || k > 0) ? 1u : 0u);
-                tc::mma_commit(BAR(A3E + a));
-                tc::mma_commit(BAR(W3E + w));
-            };
-            for (int cx = 0; cx < nch; cx++) {
-                const int cw = min(TK_CW, P2 - cx * TK_CW);
-                const int ncol = min(TK_RC, P1 - cx * TK_CW);
-                const int L0 = cx * P1;
-                for (int y = 0; y < P2; y++) {
-                    // conv1 rows up to y + 2 into the TMEM ring: shared -> TMEM copies run
-                    // in issue order with the MMAs, so the slot of row L - TK_TRING (last
-                    // read by output row y - 2's MMAs, issued before) is free
-                    for (; Lc <= L0 + y + 2; Lc++) {
-                        const int ss = Lc % TK_SRING;
-                        tc::mbar_wait(BAR(C1F + ss), (uint32_t)((Lc / TK_SRING) & 1));
-                        tc::tc_after();
-                        const uint32_t ta = tmem + TK_T_A + (uint32_t)((Lc % TK_TRING) * TK_RC) * 8u;
-                        for (int j = 0; j < ncol; j++)
-                            tc::tmem_cp_128x256b(ta + j * 8u,
-                                                 tc::sdesc(s0 + TK_OFF_RING + (uint32_t)(ss * TK_RC + j) * TK_BLK,
-                                                           2048, 128));
-                        tc::mma_commit(BAR(C1E + ss));  // the shared slot is free once the copies land
+                if (tc::elect_one()) {
+                    tc::mma_bf16(T_D3, d_a3 + ((uint32_t)a * 8192u >> 4), d_w3 + ((uint32_t)w * 4096u >> 4), ID3,
+                                 pix > 0 ? 1u : 0u);
+                    tc::mma_bf16(T_D3, d_a3 + (((uint32_t)a * 8192u + 4096u) >> 4),
+                                 d_w3 + (((uint32_t)w * 4096u + 2048u) >> 4), ID3, 1u);
+                    tc::mma_commit(BAR(A3E + a));
+                    if (w & 1) tc::mma_commit(BAR(W3E + w / 2));
+                }
+                __syncwarp();
+            }
+        };
+        int R = 0, prev_cw = 0;
+        for (int cx = 0; cx < nch; cx++) {
+            const int cw = min(TK_CW, P2 - cx * TK_CW);
+            const int L0 = cx * P1;
+            for (int y = 0; y < P2; y++, R++) {
+                const int ab = R % TK_EPI;
+                TKT(0);
+                tc::mbar_wait(BAR(ACE + ab), (uint32_t)((R / TK_EPI) & 1));  // zeroed, drained
+                TKT(3);
+                for (; Lw <= L0 + y + 2; Lw++) tc::mbar_wait(BAR(C1F + Lw % TK_RING), (uint32_t)((Lw / TK_RING) & 1));
+                TKT(4);
+                tc::tc_after();
+                const uint32_t acc = tmem + TK_T_ACC + (uint32_t)ab * (TK_CW * 32);
+                const uint64_t dr[3] = {d_ring + ((uint32_t)(((L0 + y) % TK_RING) * TK_RC) * TK_BLK >> 4),
+                                        d_ring + ((uint32_t)(((L0 + y + 1) % TK_RING) * TK_RC) * TK_BLK >> 4),
+                                        d_ring + ((uint32_t)(((L0 + y + 2) % TK_RING) * TK_RC) * TK_BLK >> 4)};
+                if (tc::elect_one()) {
+                    switch (cw) {
+                    case 7: conv2_row<7>(acc, dr, d_w2); break;
+                    case 6: conv2_row<6>(acc, dr, d_w2); break;
+                    case 5: conv2_row<5>(acc, dr, d_w2); break;
+                    case 4: conv2_row<4>(acc, dr, d_w2); break;
+                    case 3: conv2_row<3>(acc, dr, d_w2); break;
+                    case 2: conv2_row<2>(acc, dr, d_w2); break;
+                    default: conv2_row<1>(acc, dr, d_w2); break;
                     }
-                    for (int xl = 0; xl < cw; xl++, pix++) {
-                        const int s = pix % TK_D2;
-                        if (pix >= TK_D2) {
-                            tc::mbar_wait(BAR(D2E + s), (uint32_t)((pix / TK_D2 - 1) & 1));
-                            tc::tc_after();
-                        }
-#pragma unroll
-                        for (int t = 0; t < 9; t++) {
-                            const int dy = t / 3, dx = t % 3;
-                            const uint32_t a_t =
-                                tmem + TK_T_A + (uint32_t)(((L0 + y + dy) % TK_TRING) * TK_RC + xl + dx) * 8u;
-                            tc::mma_bf16_ts(tmem + TK_T_D2 + s * 32, a_t,
-                                            tc::sdesc(s0 + TK_OFF_W2 + t * 1024u, 512, 128), ID2, t > 0 ? 1u : 0u);
-                        }
-                        tc::mma_commit(BAR(D2F + s));
-                        if (pix >= TK_LAG) fc(pix - TK_LAG);
+                    tc::mma_commit(BAR(ACF + ab));
+                    tc::mma_commit(BAR(C1E + (L0 + y) % TK_RING));  // conv1 row y is no longer read
+                    if (y == P2 - 1) {
+                        tc::mma_commit(BAR(C1E + (L0 + P2) % TK_RING));
+                        tc::mma_commit(BAR(C1E + (L0 + P2 + 1) % TK_RING));
                     }
                 }
+                __syncwarp();
+                if (R > 0) fc_row(R - 1, prev_cw);  // the previous row's FCs overlap this row's conv2
+                prev_cw = cw;
             }
-            for (int i = max(pix - TK_LAG, 0); i < pix; i++) fc(i);
-            tc::mma_commit(BAR(D3F));
         }
+        fc_row(R - 1, prev_cw);
+        if (tc::elect_one()) tc::mma_commit(BAR(D3F));
+        __syncwarp();
+#ifdef TK_PROF
+        TKT(0);
+        prof[7] = clock64() - t0;
+        if (lane == 0)
+            for (int k2 = 0; k2 < 8; k2++) g_tk_prof[blockIdx.x & 1023][k2] = prof[k2];
+#endif
     } else {  // ---------------- epilogue: TK_EPI groups of 4 warps, one env (TMEM lane) per thread ----------------
-        const int grp = (warp - 2) >> 2;  // pixel i is handled by group i % TK_EPI
+        const int grp = (warp - 2) >> 2;  // output row R is handled by group R % TK_EPI
         const int q = warp & 3;           // TMEM lane quadrant this warp may access
         const int m = q * 32 + lane;      // env row within the tile
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        const uint32_t acc = tmem + TK_T_ACC + lane_off + (uint32_t)grp * (TK_CW * 32);
         float b2r[32];
 #pragma unroll
         for (int c = 0; c < 32; c++) b2r[c] = bias2[c];
-        for (int i = grp; i < NP2; i += TK_EPI) {
-            const int s = i % TK_D2, a = i % TK_A3;
-            tc::mbar_wait(BAR(D2F + s), (uint32_t)((i / TK_D2) & 1));
+        // the accumulators start at zero (every conv2 MMA accumulates)
+        for (int j = 0; j < TK_CW; j++) tc::tmem_zero32(acc + 32u * j);
+        tc::tmem_wait_st();
+        tc::tc_before();
+        tc::mbar_arrive(BAR(ACE + grp));
+        int k = 0;  // A3 blocks produced by this group
+#ifdef TK_PROF
+        long long eprof[4] = {0, 0, 0, 0}, e0 = clock64();
+#endif
+        for (int R = grp; R < nrows; R += TK_EPI) {
+            const int cw = min(TK_CW, P2 - (R / P2) * TK_CW);
+#ifdef TK_PROF
+            long long ew = clock64();
+#endif
+            tc::mbar_wait(BAR(ACF + grp), (uint32_t)((R / TK_EPI) & 1));
+#ifdef TK_PROF
+            eprof[0] += clock64() - ew;
+#endif
             tc::tc_after();
-            uint32_t r[32];
             __syncwarp();
-            tc::tmem_ld32(tmem + TK_T_D2 + lane_off + s * 32, r);
-            tc::tmem_wait_ld();
-            tc::tc_before();
-            tc::mbar_arrive(BAR(D2E + s));
-            if (i >= TK_A3) tc::mbar_wait(BAR(A3E + a), (uint32_t)((i / TK_A3 - 1) & 1));
-            uint8_t *a3 = sm + TK_OFF_A3 + a * 8192u;
+            for (int j = 0; j < cw; j++, k++) {
+                uint32_t r[32];
+                tc::tmem_ld32(acc + 32u * j, r);
+                tc::tmem_wait_ld();
+                tc::tmem_zero32(acc + 32u * j);
+                const int a = grp * TK_A3G + k % TK_A3G;
+#ifdef TK_PROF
+                long long ea = clock64();
+#endif
+                if (k >= TK_A3G) tc::mbar_wait(BAR(A3E + a), (uint32_t)((k / TK_A3G - 1) & 1));
+#ifdef TK_PROF
+                eprof[1] += clock64() - ea;
+#endif
+                uint8_t *a3 = sm + TK_OFF_A3 + a * 8192u;
 #pragma unroll
-            for (int kc = 0; kc < 4; kc++) {  // 8 channels -> one 16-byte core-matrix row
-                uint32_t wd[4];
+                for (int kc = 0; kc < 4; kc++) {  // 8 channels -> one 16-byte core-matrix row
+                    uint32_t wd[4];
 #pragma unroll
-                for (int j = 0; j < 4; j++) {
-                    const int c = kc * 8 + 2 * j;
-                    float x0 = __uint_as_float(r[c]) + b2r[c], x1 = __uint_as_float(r[c + 1]) + b2r[c + 1];
-                    x0 = x0 > 0.f ? x0 : 0.f;
-                    x1 = x1 > 0.f ? x1 : 0.f;
-                    __nv_bfloat162 h2 = __floats2bfloat162_rn(x0, x1);
-                    wd[j] = *reinterpret_cast<uint32_t *>(&h2);
+                    for (int jj = 0; jj < 4; jj++) {
+                        const int c = kc * 8 + 2 * jj;
+                        float x0 = __uint_as_float(r[c]) + b2r[c], x1 = __uint_as_float(r[c + 1]) + b2r[c + 1];
+                        x0 = x0 > 0.f ? x0 : 0.f;
+                        x1 = x1 > 0.f ? x1 : 0.f;
+                        __nv_bfloat162 h2 = __floats2bfloat162_rn(x0, x1);
+                        wd[jj] = *reinterpret_cast<uint32_t *>(&h2);
+                    }
+                    *reinterpret_cast<uint4 *>(a3 + ((kc * 16 + (m >> 3)) * 128 + (m & 7) * 16)) =
+                        make_uint4(wd[0], wd[1], wd[2], wd[3]);
                 }
-                *reinterpret_cast<uint4 *>(a3 + ((kc * 16 + (m >> 3)) * 128 + (m & 7) * 16)) =
-                    make_uint4(wd[0], wd[1], wd[2], wd[3]);
+                tc::fence_proxy_async();
+                tc::mbar_arrive(BAR(A3F + a));
+                __syncwarp();
             }
-            tc::fence_proxy_async();
-            tc::mbar_arrive(BAR(A3F + a));
+            tc::tmem_wait_st();
+            tc::tc_before();
+            tc::mbar_arrive(BAR(ACE + grp));
         }
+#ifdef TK_PROF
+        if (threadIdx.x == 64 || threadIdx.x == 64 + 128) {
+            eprof[2] = clock64() - e0;
+            for (int k2 = 0; k2 < 3; k2++) g_tk_prof[blockIdx.x & 1023][8 + 4 * grp + k2] = eprof[k2];
+        }
+#endif
         if (grp == 0) {
             tc::mbar_wait(BAR(D3F), 0);
             tc::tc_after();
@@ -369,11 +479,11 @@ __global__ void __launch_bounds__(TK_THREADS, 1) trunk_kernel(const TrunkParams 
             if (env < p.B) {
                 for (int o = 0; o <= p.NA; o++) {
                     const float *wr = head + o * 64;
-                    float acc = biash[o];
+                    float a = biash[o];
 #pragma unroll
-                    for (int j = 0; j < 64; j++) acc = fmaf(h[j], wr[j], acc);
-                    if (o < p.NA) p.logits[env * p.NA + o] = acc;
-                    else p.value[env] = acc;
+                    for (int j = 0; j < 64; j++) a = fmaf(h[j], wr[j], a);
+                    if (o < p.NA) p.logits[env * p.NA + o] = a;
+                    else p.value[env] = a;
                 }
             }
         }

@@ -244,12 +244,14 @@ class PackedPolicy:
 
 def pack_conv2_weight(weight):
     """Conv2d(16 -> 32, 3x3) weight [32, 16, 3, 3] -> the trunk kernel's B
-    operands: per tap (dy, dx) an N = 32 x K = 16 bf16 block of UMMA K-major
-    core matrices, [9, 512] (csrc/trunk_kernel.cuh)."""
+    operands: per kernel row dy an N = 96 x K = 16 bf16 block of UMMA K-major
+    core matrices whose rows are the 32 output channels of taps (dy, 2),
+    (dy, 1), (dy, 0) in that order, [3, 1536] (csrc/trunk_kernel.cuh)."""
     torch = _torch()
     n, k = weight.shape[:2]
-    w = weight.detach().to(torch.float32).permute(2, 3, 0, 1).reshape(9, n // 8, 8, k // 8, 8)
-    return w.permute(0, 3, 1, 2, 4).reshape(9, n * k).to(torch.bfloat16).contiguous()
+    w = weight.detach().to(torch.float32).flip(3).permute(2, 3, 0, 1)  # [dy][2 - dx][n][k]
+    w = w.reshape(3, 3 * n // 8, 8, k // 8, 8)
+    return w.permute(0, 3, 1, 2, 4).reshape(3, 3 * n * k).to(torch.bfloat16).contiguous()
 
 
 def pack_fc_weight(weight, channels: int, side: int):

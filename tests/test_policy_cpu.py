@@ -51,7 +51,7 @@ def test_arch_validation_and_defaults():
 def test_trunk_weight_packing_layouts():
     """pack_conv2_weight / pack_fc_weight put element (n, k) of each block at
     ((k/8)*(N/8) + n/8)*64 + (n%8)*8 + k%8 (UMMA K-major core matrices,
-    csrc/trunk_kernel.cuh)."""
+    csrc/trunk_kernel.cuh); conv2 blocks hold three taps side by side (N = 96)."""
     import torch
     from paper_2408_12525_b200.policy import pack_conv2_weight, pack_fc_weight
     w2 = torch.randn(32, 16, 3, 3)
@@ -63,8 +63,10 @@ def test_trunk_weight_packing_layouts():
     for _ in range(200):
         t, n, k = (int(torch.randint(9, (1,), generator=g)), int(torch.randint(32, (1,), generator=g)),
                    int(torch.randint(16, (1,), generator=g)))
-        off = ((k // 8) * 4 + n // 8) * 64 + (n % 8) * 8 + k % 8
-        assert p2[t, off] == w2[n, k, t // 3, t % 3].bfloat16().float()
+        dy, dx = t // 3, t % 3
+        nn = (2 - dx) * 32 + n  # taps (dy, 2), (dy, 1), (dy, 0) side by side: N = 96
+        off = ((k // 8) * 12 + nn // 8) * 64 + (nn % 8) * 8 + k % 8
+        assert p2[dy, off] == w2[n, k, dy, dx].bfloat16().float()
         px, n, k = (int(torch.randint(side * side, (1,), generator=g)), int(torch.randint(64, (1,), generator=g)),
                     int(torch.randint(32, (1,), generator=g)))
         off = ((k // 8) * 8 + n // 8) * 64 + (n % 8) * 8 + k % 8
