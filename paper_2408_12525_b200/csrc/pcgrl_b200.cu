@@ -8,6 +8,7 @@
 #include <mutex>
 #include <new>
 #include <set>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -394,17 +395,40 @@ static void fastdiv_init(FastDiv &f, uint32_t d) {
 static int dom_n(int d) { return d == 0 ? 2 : d == 1 ? 4 : 6; }
 static int dom_m(int d) { return d == 0 ? 2 : d == 1 ? 4 : 7; }
 
+template <class G, int DOM, int S>
+static int launch_env_k(lg_env *e, const Params &q, int mode, cudaStream_t s) {
+    CU(smem_attr((const void *)env_kernel<G, DOM, S>));
+    const int E = e->threads / G::TEAM;
+    const long long grid = (e->B + E - 1) / E;
+    env_kernel<G, DOM, S><<<(unsigned)grid, e->threads, e->smem, s>>>(q, mode);
+    CU(cudaGetLastError());
+    return LG_OK;
+}
+
+// Specialised lane-team kernels (env_kernels.cuh, S = 1 + representation) for
+// "plain" configs: the BASELINE configs' (G, domain, representation) triples.
+template <class G, int DOM, int REP>
+static constexpr bool spec_enabled() {
+    return (std::is_same<G, G64>::value && DOM == 0 && REP == LG_NARROW) ||  // c4
+           (std::is_same<G, G16>::value && DOM == 1 && REP == LG_TURTLE);    // c2
+}
+
 template <class G, int DOM>
 static int launch_env_t(lg_env *e, const Params &p, int mode, cudaStream_t s) {
-    CU(smem_attr((const void *)env_kernel<G, DOM>));
-    int E = e->threads / G::TEAM;
-    long long grid = (e->B + E - 1) / E;
     Params q = p;
     const char *ea = getenv("LG_EARLY");
     q.early = ea ? ea[0] == '1' : 1;
-    env_kernel<G, DOM><<<(unsigned)grid, e->threads, e->smem, s>>>(q, mode);
-    CU(cudaGetLastError());
-    return LG_OK;
+    const char *ns = getenv("LG_NO_SPEC");
+    const bool plain = q.n_pins == 0 && q.n_ctrl == 0 && !q.det && !q.obs_u8 && !q.obs_bits && !(ns && ns[0] == '1');
+    if (plain) {
+        if constexpr (spec_enabled<G, DOM, LG_NARROW>())
+            if (q.rep == LG_NARROW) return launch_env_k<G, DOM, 1 + LG_NARROW>(e, q, mode, s);
+        if constexpr (spec_enabled<G, DOM, LG_TURTLE>())
+            if (q.rep == LG_TURTLE) return launch_env_k<G, DOM, 1 + LG_TURTLE>(e, q, mode, s);
+        if constexpr (spec_enabled<G, DOM, LG_WIDE>())
+            if (q.rep == LG_WIDE) return launch_env_k<G, DOM, 1 + LG_WIDE>(e, q, mode, s);
+    }
+    return launch_env_k<G, DOM, 0>(e, q, mode, s);
 }
 
 template <int DOM>
