@@ -129,19 +129,21 @@ __device__ __forceinline__ bool gate_closed(const Params &p) {
     return p.gate && (*reinterpret_cast<volatile const unsigned *>(p.err) & FLAG_BAD_ACTION);
 }
 
-// Specialised launches. S = 0: every EnvConfig (runtime flags). S = 1 + rep:
-// a "plain" config of representation rep -- no pinpoints, no controllable
-// metrics, no deterministic metrics, float32 observations (c1..c5 are all
-// plain). The flags become compile-time constants, so the dead paths leave
-// the kernel: a smaller instruction footprint and fewer branches for the
-// latency-bound lane-team kernels (c4 13.9k -> 9.8k SASS instructions,
-// 89 -> 99 M env-steps/s; c2 123 -> 132 M).
-template <int S> __device__ __forceinline__ int rep_of(const Params &p) { return S ? S - 1 : p.rep; }
-template <int S> __device__ __forceinline__ int nctrl_of(const Params &p) { return S ? 0 : p.n_ctrl; }
-template <int S> __device__ __forceinline__ int npins_of(const Params &p) { return S ? 0 : p.n_pins; }
-template <int S> __device__ __forceinline__ int det_of(const Params &p) { return S ? 0 : p.det; }
-template <int S> __device__ __forceinline__ int obs_u8_of(const Params &p) { return S ? 0 : p.obs_u8; }
-template <int S> __device__ __forceinline__ int obs_bits_of(const Params &p) { return S ? 0 : p.obs_bits; }
+// Specialised launches. S = 0: every EnvConfig (runtime flags). Otherwise
+// S & 3 = 1 + representation, with no controllable metrics, no deterministic
+// metrics and float32 observations; S & SPEC_NOPINS also fixes "no pinpoints"
+// (the BASELINE configs c1..c5 are all specialised). The flags become
+// compile-time constants, so the dead paths leave the kernel: a smaller
+// instruction footprint and fewer branches (c4 13.9k -> 9.8k SASS
+// instructions, 89 -> 99 M env-steps/s; c2 123 -> 132 M).
+constexpr int SPEC_NOPINS = 4;
+constexpr int spec_of(int rep, bool nopins) { return 1 + rep + (nopins ? SPEC_NOPINS : 0); }
+template <int S> __device__ __forceinline__ int rep_of(const Params &p) { return (S & 3) ? (S & 3) - 1 : p.rep; }
+template <int S> __device__ __forceinline__ int nctrl_of(const Params &p) { return (S & 3) ? 0 : p.n_ctrl; }
+template <int S> __device__ __forceinline__ int npins_of(const Params &p) { return (S & SPEC_NOPINS) ? 0 : p.n_pins; }
+template <int S> __device__ __forceinline__ int det_of(const Params &p) { return (S & 3) ? 0 : p.det; }
+template <int S> __device__ __forceinline__ int obs_u8_of(const Params &p) { return (S & 3) ? 0 : p.obs_u8; }
+template <int S> __device__ __forceinline__ int obs_bits_of(const Params &p) { return (S & 3) ? 0 : p.obs_bits; }
 
 __device__ __forceinline__ void rng_load(const Params &p, long long env, Pcg &g) {
     const ulonglong2 s = p.rs[2 * env], b = p.rs[2 * env + 1], inc = p.ri[env];

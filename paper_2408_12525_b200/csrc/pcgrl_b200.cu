@@ -405,12 +405,18 @@ static int launch_env_k(lg_env *e, const Params &q, int mode, cudaStream_t s) {
     return LG_OK;
 }
 
-// Specialised lane-team kernels (env_kernels.cuh, S = 1 + representation) for
-// "plain" configs: the BASELINE configs' (G, domain, representation) triples.
-template <class G, int DOM, int REP>
+// Specialised lane-team kernels (env_kernels.cuh, S = spec_of(rep, no pins))
+// for the BASELINE configs' (G, domain, representation) triples.
+template <class G, int DOM, int S>
 static constexpr bool spec_enabled() {
-    return (std::is_same<G, G64>::value && DOM == 0 && REP == LG_NARROW) ||  // c4
-           (std::is_same<G, G16>::value && DOM == 1 && REP == LG_TURTLE);    // c2
+    return (std::is_same<G, G64>::value && DOM == 0 && S == spec_of(LG_NARROW, true)) ||  // c4
+           (std::is_same<G, G16>::value && DOM == 1 && S == spec_of(LG_TURTLE, true));    // c2
+}
+
+// plain = the flags a specialised kernel fixes (no controls, no det metrics, float32 obs)
+static bool plain_launch(const Params &q) {
+    const char *ns = getenv("LG_NO_SPEC");
+    return q.n_ctrl == 0 && !q.det && !q.obs_u8 && !q.obs_bits && !(ns && ns[0] == '1');
 }
 
 template <class G, int DOM>
@@ -418,15 +424,18 @@ static int launch_env_t(lg_env *e, const Params &p, int mode, cudaStream_t s) {
     Params q = p;
     const char *ea = getenv("LG_EARLY");
     q.early = ea ? ea[0] == '1' : 1;
-    const char *ns = getenv("LG_NO_SPEC");
-    const bool plain = q.n_pins == 0 && q.n_ctrl == 0 && !q.det && !q.obs_u8 && !q.obs_bits && !(ns && ns[0] == '1');
-    if (plain) {
-        if constexpr (spec_enabled<G, DOM, LG_NARROW>())
-            if (q.rep == LG_NARROW) return launch_env_k<G, DOM, 1 + LG_NARROW>(e, q, mode, s);
-        if constexpr (spec_enabled<G, DOM, LG_TURTLE>())
-            if (q.rep == LG_TURTLE) return launch_env_k<G, DOM, 1 + LG_TURTLE>(e, q, mode, s);
-        if constexpr (spec_enabled<G, DOM, LG_WIDE>())
-            if (q.rep == LG_WIDE) return launch_env_k<G, DOM, 1 + LG_WIDE>(e, q, mode, s);
+    if (plain_launch(q)) {
+        const bool np = q.n_pins == 0;
+#define LG_TRY_SPEC(REP, NP)                                                                     \
+    if constexpr (spec_enabled<G, DOM, spec_of(REP, NP)>())                                     \
+        if (q.rep == REP && np == NP) return launch_env_k<G, DOM, spec_of(REP, NP)>(e, q, mode, s);
+        LG_TRY_SPEC(LG_NARROW, true)
+        LG_TRY_SPEC(LG_NARROW, false)
+        LG_TRY_SPEC(LG_TURTLE, true)
+        LG_TRY_SPEC(LG_TURTLE, false)
+        LG_TRY_SPEC(LG_WIDE, true)
+        LG_TRY_SPEC(LG_WIDE, false)
+#undef LG_TRY_SPEC
     }
     return launch_env_k<G, DOM, 0>(e, q, mode, s);
 }
@@ -450,8 +459,21 @@ static int launch_solo_t(lg_env *e, const Params &p, int mode, cudaStream_t s) {
         q.env_smem = e->slot_elide;
         smem = e->smem_elide;
     }
-    if (e->E == e->threads) SoloKernel<DOM>::fn<<<(unsigned)grid, e->threads, smem, s>>>(q, mode);
-    else SoloKernel<DOM>::fn_small<<<(unsigned)grid, e->threads, smem, s>>>(q, mode);
+    constexpr int S = SoloKernel<DOM>::spec;
+    const bool spec = S != 0 && plain_launch(q) && q.rep == (S & 3) - 1 && (!(S & SPEC_NOPINS) || q.n_pins == 0);
+    if (e->E == e->threads) {
+        if (spec) {
+            CU(smem_attr((const void *)SoloKernel<DOM>::fn_spec));
+            SoloKernel<DOM>::fn_spec<<<(unsigned)grid, e->threads, smem, s>>>(q, mode);
+        } else {
+            SoloKernel<DOM>::fn<<<(unsigned)grid, e->threads, smem, s>>>(q, mode);
+        }
+    } else if (spec) {
+        CU(smem_attr((const void *)SoloKernel<DOM>::fn_small_spec));
+        SoloKernel<DOM>::fn_small_spec<<<(unsigned)grid, e->threads, smem, s>>>(q, mode);
+    } else {
+        SoloKernel<DOM>::fn_small<<<(unsigned)grid, e->threads, smem, s>>>(q, mode);
+    }
     CU(cudaGetLastError());
     return LG_OK;
 }

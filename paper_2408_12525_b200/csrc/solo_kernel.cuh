@@ -51,7 +51,7 @@ __device__ __forceinline__ uint32_t *solo_plane(const Params &p, long long env, 
 // stream cost several times their size in write bandwidth (read/write
 // turnaround; tools/store_pattern.cu), so most steps read 72 bytes per env
 // instead of ~330.
-template <int DOM>
+template <int DOM, int S = 0>
 __device__ __forceinline__ void solo_load_hot(const Params &p, long long env, SoloEnv<DOM> &e) {
     constexpr int NPL = Dom<DOM>::NPL;
 #pragma unroll
@@ -85,7 +85,7 @@ __device__ __forceinline__ void solo_load_hot(const Params &p, long long env, So
 
 // vals: also the current metric values (control planes, repricing, export);
 // a recompute overwrites them, so a step only needs the targets.
-template <int DOM>
+template <int DOM, int S = 0>
 __device__ __forceinline__ void solo_load_cold(const Params &p, long long env, SoloEnv<DOM> &e, bool vals) {
     constexpr int M = Dom<DOM>::M;
     const int4 *mv = reinterpret_cast<const int4 *>(p.mv + env * 24);
@@ -118,16 +118,16 @@ __device__ __forceinline__ void solo_load_cold(const Params &p, long long env, S
     e.ep_reward = l0.y;
     e.ep_start_loss = l1.x;
     rng_load(p, env, e.g);
-    e.mseed = p.det ? p.mseed[env] : 0;
+    e.mseed = det_of<S>(p) ? p.mseed[env] : 0;
 }
 
-template <int DOM>
+template <int DOM, int S = 0>
 __device__ __forceinline__ void solo_load(const Params &p, long long env, SoloEnv<DOM> &e) {
-    solo_load_hot<DOM>(p, env, e);
-    solo_load_cold<DOM>(p, env, e, true);
+    solo_load_hot<DOM, S>(p, env, e);
+    solo_load_cold<DOM, S>(p, env, e, true);
 }
 
-template <int DOM>
+template <int DOM, int S = 0>
 __device__ __forceinline__ void solo_store(const Params &p, long long env, const SoloEnv<DOM> &e, bool rows_dirty,
                            bool planes_dirty, bool metrics_dirty, bool rng_dirty, bool cold = true) {
     constexpr int NPL = Dom<DOM>::NPL;
@@ -171,19 +171,19 @@ __device__ __forceinline__ void solo_store(const Params &p, long long env, const
     }
     if (rng_dirty) {
         rng_store(p, env, e.g);
-        if (p.det) p.mseed[env] = e.mseed;
+        if (det_of<S>(p)) p.mseed[env] = e.mseed;
     }
 }
 
-template <int DOM>
+template <int DOM, int S = 0>
 __device__ __forceinline__ void solo_recompute(const Params &p, SoloEnv<DOM> &e, void *uf, bool reset) {
     SoloK k;
     SB act = rect_sb(e.h, e.w);
     // _metric_rngs (env.py:327-330): the env stream, or a fresh default_rng(metric_seed)
     Pcg mg = e.g;
-    if (p.det) seedseq_pcg((uint64_t)e.mseed, false, 0, mg);
+    if (det_of<S>(p)) seedseq_pcg((uint64_t)e.mseed, false, 0, mg);
     compute_metrics<SoloK, DOM>(k, e.pl, act, mg, uf, e.val, e.unr);
-    if (!p.det) e.g = mg;
+    if (!det_of<S>(p)) e.g = mg;
     double l = loss_of<DOM>(p, e.val, e.unr, e.lo, e.hi);
     e.prev_loss = l;
     if (reset) {
@@ -216,7 +216,7 @@ __device__ __forceinline__ int solo_serp_next(const SB &ed, int r, int c) {
 }
 
 // set tile id `tile` (0..N-1) at (r, c) in the stored planes
-template <int DOM>
+template <int DOM, int S = 0>
 __device__ __forceinline__ void solo_set_tile(SoloEnv<DOM> &e, int r, int c, int tile) {
     constexpr int NPL = Dom<DOM>::NPL;
     const int wi = r >> 1;
@@ -232,7 +232,7 @@ __device__ __forceinline__ void solo_set_tile(SoloEnv<DOM> &e, int r, int c, int
 }
 
 // reset_rows for one env minus its final _recompute (env.py:284-325)
-template <int DOM>
+template <int DOM, int S = 0>
 __device__ __forceinline__ void solo_reset_setup(const Params &p, SoloEnv<DOM> &e) {
     constexpr int N = Dom<DOM>::N, NPL = Dom<DOM>::NPL, M = Dom<DOM>::M;
     Pcg &g = e.g;
@@ -271,7 +271,7 @@ __device__ __forceinline__ void solo_reset_setup(const Params &p, SoloEnv<DOM> &
             }
         }
     }
-    if (p.n_pins > 0) {  // place_pinpoints: Floyd over the h*w free cells (grid.py:194-225)
+    if (npins_of<S>(p) > 0) {  // place_pinpoints: Floyd over the h*w free cells (grid.py:194-225)
         int pop = h * w, k = p.n_pins;
         if (pop < k) {
             atomicOr(p.err, (unsigned)FLAG_PINPOINTS);
@@ -291,7 +291,7 @@ __device__ __forceinline__ void solo_reset_setup(const Params &p, SoloEnv<DOM> &
             }
             for (int i = 0; i < k; i++) {
                 int r = picks[i] / w, c = picks[i] - (picks[i] / w) * w;
-                solo_set_tile<DOM>(e, r, c, p.pins[i]);
+                solo_set_tile<DOM, S>(e, r, c, p.pins[i]);
                 const int wi = r >> 1;
                 const uint32_t bit = 1u << ((r & 1) * 16 + c);
 #pragma unroll
@@ -313,7 +313,7 @@ __device__ __forceinline__ void solo_reset_setup(const Params &p, SoloEnv<DOM> &
             lo = 4;
             hi = cap;
         }
-        for (int j = 0; j < p.n_ctrl; j++)
+        for (int j = 0; j < nctrl_of<S>(p); j++)
             if (p.ctrl[j] == m) lo = hi = (int)pcg_integers(g, 0, (int64_t)cap + 1);
 #pragma unroll
         for (int q = 0; q < 8; q++) {
@@ -321,7 +321,7 @@ __device__ __forceinline__ void solo_reset_setup(const Params &p, SoloEnv<DOM> &
             e.hi[q] = (q == m) ? hi : e.hi[q];
         }
     }
-    if (p.det) e.mseed = (long long)pcg_bounded(g, 0x7FFFFFFFFFFFFFFFULL);  // env.py:302-303
+    if (det_of<S>(p)) e.mseed = (long long)pcg_bounded(g, 0x7FFFFFFFFFFFFFFFULL);  // env.py:302-303
     SB ed = andnot(act, e.frz);  // _install_row (env.py:307-325)
     e.order_len = ed.count();
     int first = solo_serp_first(ed, 0);
@@ -403,13 +403,13 @@ struct BitW {
 // Render one env's 0/1 observation planes as a bit stream: into its private
 // slot (slot mode), or at bit offset `bit0` of the warp/block stream whose
 // bits are the concatenated outputs of consecutive envs (stream mode).
-template <int DOM>
+template <int DOM, int S = 0>
 __device__ __forceinline__ void solo_render(const Params &p, const SoloEnv<DOM> &e, uint32_t *slot, bool stream, uint32_t bit0,
                             bool last) {
     constexpr int N = Dom<DOM>::N, NPL = Dom<DOM>::NPL;
     const int OH = p.OH, OW = p.OW, H = p.H, W = p.W;
     int r0 = 0, c0 = 0;
-    if (p.rep != REP_WIDE) {
+    if (rep_of<S>(p) != REP_WIDE) {
         r0 = e.pr - p.half;
         c0 = e.pc - p.half;
     }
@@ -462,7 +462,7 @@ __device__ __forceinline__ void solo_render(const Params &p, const SoloEnv<DOM> 
     if (stream) return;  // stream mode is only used without control planes
     // control planes: (value - (lo+hi)/2) / cap, float64 -> float32 (env.py:224-232)
     float *ctrl = reinterpret_cast<float *>(slot + p.img_words);
-    for (int j = 0; j < p.n_ctrl; j++) {
+    for (int j = 0; j < nctrl_of<S>(p); j++) {
         int m = p.ctrl[j];
         int vm = 0, lm = 0, hm = 0;
 #pragma unroll
@@ -819,7 +819,7 @@ __device__ void solo_write_stream_bits(const Params &p, const uint32_t *st, long
 // each of its envs together -- lane l builds window rows l, l+32, ... of every
 // plane and ORs them into the zeroed slot -- instead of one lane streaming the
 // whole image bit by bit (the serial render was ~40% of c1's latency).
-template <int DOM>
+template <int DOM, int S = 0>
 __device__ __forceinline__ void solo_render_coop(const Params &p, const SoloEnv<DOM> &src, int owner, uint32_t *slot,
                                                  int lane) {
     constexpr int N = Dom<DOM>::N, NPL = Dom<DOM>::NPL;
@@ -835,7 +835,7 @@ __device__ __forceinline__ void solo_render_coop(const Params &p, const SoloEnv<
     const int OH = p.OH, OW = p.OW, H = p.H, W = p.W;
     for (int i = lane; i < p.env_smem; i += 32) slot[i] = 0u;  // the slot (elided or not)
     __syncwarp();
-    const int r0 = p.rep != REP_WIDE ? pr - p.half : 0, c0 = p.rep != REP_WIDE ? pc - p.half : 0;
+    const int r0 = rep_of<S>(p) != REP_WIDE ? pr - p.half : 0, c0 = rep_of<S>(p) != REP_WIDE ? pc - p.half : 0;
     const int jlo = c0 < 0 ? -c0 : 0;
     const int jhi = (W - c0) < OW ? (W - c0) : OW;
     const uint64_t full = OW >= 64 ? ~0ull : ((1ull << OW) - 1ull);
@@ -895,14 +895,14 @@ struct SoloStep {
 
 // load; apply the action (env.py:355-372); advance the scan position and t
 // (env.py:374-381: independent of the recompute)
-template <int DOM>
+template <int DOM, int S = 0>
 __device__ __forceinline__ void solo_begin(const Params &p, int mode, long long env, SoloStep<DOM> &st) {
     constexpr int N = Dom<DOM>::N;
     SoloEnv<DOM> &e = st.e;
-    solo_load_hot<DOM>(p, env, e);
+    solo_load_hot<DOM, S>(p, env, e);
     // control planes render the metric values; reset/recompute/reprice use everything
-    st.cold = (mode != MODE_STEP && mode != MODE_OBSERVE) || p.n_ctrl > 0;
-    if (st.cold) solo_load_cold<DOM>(p, env, e, true);
+    st.cold = (mode != MODE_STEP && mode != MODE_OBSERVE) || nctrl_of<S>(p) > 0;
+    if (st.cold) solo_load_cold<DOM, S>(p, env, e, true);
     st.rows_dirty = st.planes_dirty = st.metrics_dirty = st.rng_dirty = false;
     st.wrote = st.reset_now = st.ends = false;
     st.before = 0.0;
@@ -911,9 +911,9 @@ __device__ __forceinline__ void solo_begin(const Params &p, int mode, long long 
         bool ok = a >= 0 && a < p.n_actions;
         if (!ok) atomicOr(p.err, (unsigned)FLAG_BAD_ACTION);
         int r = e.pr, c = e.pc, tile = -1;
-        if (p.rep == REP_NARROW) {
+        if (rep_of<S>(p) == REP_NARROW) {
             if (ok && a != 0) tile = (int)a - 1;
-        } else if (p.rep == REP_TURTLE) {
+        } else if (rep_of<S>(p) == REP_TURTLE) {
             if (ok && a < 4) {
                 if (a == 0) r = r > 0 ? r - 1 : 0;
                 else if (a == 1) r = r < e.h - 1 ? r + 1 : e.h - 1;
@@ -946,14 +946,14 @@ __device__ __forceinline__ void solo_begin(const Params &p, int mode, long long 
                 }
             }
             bool editable = act && !fz;
-            st.wrote = tile != cur && (p.rep == REP_NARROW || editable);
+            st.wrote = tile != cur && (rep_of<S>(p) == REP_NARROW || editable);
         }
         if (st.wrote) {  // env.py:369-372
-            solo_set_tile<DOM>(e, r, c, tile);
+            solo_set_tile<DOM, S>(e, r, c, tile);
             st.planes_dirty = true;
             e.changes += 1;
         }
-        if (p.rep == REP_NARROW) {  // pos_idx = (pos_idx + 1) % order_len
+        if (rep_of<S>(p) == REP_NARROW) {  // pos_idx = (pos_idx + 1) % order_len
             SB ed = andnot(rect_sb(e.h, e.w), e.frz);
             int nidx = e.pos_idx + 1, nxt;
             if (nidx >= e.order_len) {
@@ -981,12 +981,12 @@ __device__ __forceinline__ void solo_begin(const Params &p, int mode, long long 
 
 // recompute (env.py:332-347), reward/done/info (env.py:373-390), auto-reset
 // (env.py:391-392), state write-back
-template <int DOM>
+template <int DOM, int S = 0>
 __device__ __forceinline__ void solo_finish(const Params &p, int mode, long long env, SoloStep<DOM> &st, void *slot) {
     SoloEnv<DOM> &e = st.e;
     if (mode == MODE_STEP) {
         if (!st.cold && (st.wrote || st.ends)) {
-            solo_load_cold<DOM>(p, env, e, false);
+            solo_load_cold<DOM, S>(p, env, e, false);
             st.cold = true;
         }
         st.before = e.prev_loss;
@@ -997,11 +997,11 @@ __device__ __forceinline__ void solo_finish(const Params &p, int mode, long long
     for (int pass = 0; pass < 2; pass++) {
         if (pass == 1) {
             if (!st.reset_now) break;
-            solo_reset_setup<DOM>(p, e);
+            solo_reset_setup<DOM, S>(p, e);
             st.rows_dirty = true;
         }
         if (pass == 1 || st.wrote) {
-            solo_recompute<DOM>(p, e, slot, pass == 1);  // _recompute (env.py:332-347)
+            solo_recompute<DOM, S>(p, e, slot, pass == 1);  // _recompute (env.py:332-347)
             st.metrics_dirty = st.rng_dirty = true;
         }
         if (pass == 0 && mode == MODE_STEP) {
@@ -1026,16 +1026,16 @@ __device__ __forceinline__ void solo_finish(const Params &p, int mode, long long
         }
     }
     if (mode != MODE_OBSERVE)
-        solo_store<DOM>(p, env, e, st.rows_dirty, st.planes_dirty, st.metrics_dirty, st.rng_dirty, st.cold);
+        solo_store<DOM, S>(p, env, e, st.rows_dirty, st.planes_dirty, st.metrics_dirty, st.rng_dirty, st.cold);
 }
 
-template <int DOM>
+template <int DOM, int S = 0>
 __device__ __forceinline__ void solo_env(const Params &p, int mode, long long env, uint32_t *slot, uint32_t *img,
                                          bool stream, uint32_t bit0, bool last) {
     SoloStep<DOM> st;
-    solo_begin<DOM>(p, mode, env, st);
-    solo_finish<DOM>(p, mode, env, st, slot);
-    if (p.obs) solo_render<DOM>(p, st.e, img, stream, bit0, last);
+    solo_begin<DOM, S>(p, mode, env, st);
+    solo_finish<DOM, S>(p, mode, env, st, slot);
+    if (p.obs) solo_render<DOM, S>(p, st.e, img, stream, bit0, last);
 }
 
 #ifndef LG_EARLY_SPLIT
@@ -1044,10 +1044,13 @@ __device__ __forceinline__ void solo_env(const Params &p, int mode, long long en
 #ifndef LG_DUNGEON_EARLY
 #define LG_DUNGEON_EARLY 0  // dungeon's warp kernel without the early-observation path (c3: spills)
 #endif
+#ifndef LG_DUNGEON_SPEC_EARLY
+#define LG_DUNGEON_SPEC_EARLY 1  // ... but the specialised one (c3) has the registers for it
+#endif
 // WARP = 1: the warp-mode kernel (E == blockDim: each warp owns 32 envs);
 // WARP = 0: the block-mode kernel (small batches). Two kernels, so neither
 // carries the other's code paths (register pressure, instruction footprint).
-template <int DOM, int WARP>
+template <int DOM, int WARP, int S = 0>
 __device__ __forceinline__ void env_solo_body(const Params &p, int mode) {
     extern __shared__ __align__(16) uint32_t smem_w[];
     const int E = p.solo_E, T = blockDim.x, tid = threadIdx.x;
@@ -1090,49 +1093,49 @@ __device__ __forceinline__ void env_solo_body(const Params &p, int mode) {
     // store the rest -- so a launch does not start with every warp computing
     // and no warp storing (one-wave batches: c3; the shards of a multi-GPU c5).
     // Not when an env of the warp ends this step (auto-reset changes its map).
-    if (warp_mode && (DOM != 2 || LG_DUNGEON_EARLY) && p.early && mode == MODE_STEP && p.obs && p.n_ctrl == 0 &&
-        !p.obs_u8 && !p.obs_bits &&
+    if (warp_mode && (DOM != 2 || LG_DUNGEON_EARLY || (S != 0 && LG_DUNGEON_SPEC_EARLY)) && p.early && mode == MODE_STEP &&
+        p.obs && nctrl_of<S>(p) == 0 && !obs_u8_of<S>(p) && !obs_bits_of<S>(p) &&
         (p.stream_mode || p.PB == p.PE) &&
         (reinterpret_cast<uintptr_t>(p.obs + (size_t)env0 * p.PE) & 31) == 0) {
         SoloStep<DOM> st;
-        if (valid) solo_begin<DOM>(p, mode, env, st);
+        if (valid) solo_begin<DOM, S>(p, mode, env, st);
         if (!__any_sync(0xffffffffu, valid && st.ends)) {
-            if (valid) solo_render<DOM>(p, st.e, img, p.stream_mode != 0, (uint32_t)local * p.PE, local == nenv - 1);
+            if (valid) solo_render<DOM, S>(p, st.e, img, p.stream_mode != 0, (uint32_t)local * p.PE, local == nenv - 1);
             __syncwarp();
             const uint32_t nv = (uint32_t)nenv * p.PE / 8;
             const uint32_t qm = (uint32_t)((uint64_t)nv * LG_EARLY_SPLIT / 8) & ~127u;  // multiple of nthr * U
             if (p.stream_mode) solo_write_stream<8, 2>(p, grp, env0, nenv, wl, nthr, 0, qm);
             else solo_write_noctrl<LG_WRITER_U>(p, grp, env0, nenv, wl, nthr, 0, qm);
-            if (valid) solo_finish<DOM>(p, mode, env, st, scratch);
+            if (valid) solo_finish<DOM, S>(p, mode, env, st, scratch);
             if (p.stream_mode) solo_write_stream<8, 2>(p, grp, env0, nenv, wl, nthr, qm);
             else solo_write_noctrl<LG_WRITER_U>(p, grp, env0, nenv, wl, nthr, qm);
             return;
         }
         if (valid) {
-            solo_finish<DOM>(p, mode, env, st, scratch);
-            solo_render<DOM>(p, st.e, img, p.stream_mode != 0, (uint32_t)local * p.PE, local == nenv - 1);
+            solo_finish<DOM, S>(p, mode, env, st, scratch);
+            solo_render<DOM, S>(p, st.e, img, p.stream_mode != 0, (uint32_t)local * p.PE, local == nenv - 1);
         }
-    } else if (!warp_mode && p.obs && !p.stream_mode && p.n_ctrl == 0 && p.coop) {
+    } else if (!warp_mode && p.obs && !p.stream_mode && nctrl_of<S>(p) == 0 && p.coop) {
         SoloStep<DOM> st;
         if (valid) {
-            solo_begin<DOM>(p, mode, env, st);
-            solo_finish<DOM>(p, mode, env, st, scratch);
+            solo_begin<DOM, S>(p, mode, env, st);
+            solo_finish<DOM, S>(p, mode, env, st, scratch);
         }
         // this warp's envs are its lanes 0..k-1 (env local = lane * nw + warp)
         const int mine = __popc(__ballot_sync(0xffffffffu, valid));
         for (int k = 0; k < mine; k++)
-            solo_render_coop<DOM>(p, st.e, k, grp + (size_t)(k * nw + warp) * p.env_smem, lane);
+            solo_render_coop<DOM, S>(p, st.e, k, grp + (size_t)(k * nw + warp) * p.env_smem, lane);
     } else if (valid) {
-        solo_env<DOM>(p, mode, env, scratch, img, p.stream_mode != 0, (uint32_t)local * p.PE, local == nenv - 1);
+        solo_env<DOM, S>(p, mode, env, scratch, img, p.stream_mode != 0, (uint32_t)local * p.PE, local == nenv - 1);
     }
     if (p.stream_mode) {
         if (!p.obs) return;
         if (warp_mode) __syncwarp();
         else __syncthreads();
         if (nenv <= 0) return;
-        if (p.obs_bits) {
+        if (obs_bits_of<S>(p)) {
             solo_write_stream_bits(p, grp, env0, nenv, wl, nthr);
-        } else if (p.obs_u8) {
+        } else if (obs_u8_of<S>(p)) {
             // env0 is a multiple of 32, so the warp's byte range is 32-byte aligned
             solo_write_stream_u8(p, grp, env0, nenv, wl, nthr);
         } else if ((reinterpret_cast<uintptr_t>(p.obs + (size_t)env0 * p.PE) & 31) == 0) {
@@ -1147,12 +1150,12 @@ __device__ __forceinline__ void env_solo_body(const Params &p, int mode) {
     if (warp_mode) __syncwarp();
     else __syncthreads();
     if (nenv <= 0) return;
-    if (p.obs_bits) {
+    if (obs_bits_of<S>(p)) {
         solo_write_bits(p, img, env0, nenv, wl, nthr);
         return;
     }
     const size_t first = (size_t)env0 * p.PE;
-    if (p.obs_u8) {
+    if (obs_u8_of<S>(p)) {
         const uintptr_t a = reinterpret_cast<uintptr_t>(reinterpret_cast<uint8_t *>(p.obs) + first);
         if ((a & 31) == 0) solo_write_u8<32>(p, img, env0, nenv, wl, nthr);
         else if ((a & 15) == 0) solo_write_u8<16>(p, img, env0, nenv, wl, nthr);
@@ -1189,6 +1192,17 @@ __global__ void __maxnreg__(128) env_solo_kernel_dungeon(const Params p, int mod
 __global__ void __maxnreg__(128) env_solo_kernel_binary_small(const Params p, int mode) { env_solo_body<0, 0>(p, mode); }
 __global__ void __maxnreg__(128) env_solo_kernel_maze_small(const Params p, int mode) { env_solo_body<1, 0>(p, mode); }
 __global__ void __maxnreg__(128) env_solo_kernel_dungeon_small(const Params p, int mode) { env_solo_body<2, 0>(p, mode); }
+// specialised (env_kernels.cuh spec_of): c5 / c1 (binary narrow, no pins), c3 (dungeon wide)
+constexpr int SOLO_SPEC_BINARY = spec_of(REP_NARROW, true), SOLO_SPEC_DUNGEON = spec_of(REP_WIDE, false);
+__global__ void __maxnreg__(LG_BINARY_NREG) env_solo_kernel_binary_s(const Params p, int mode) {
+    env_solo_body<0, 1, SOLO_SPEC_BINARY>(p, mode);
+}
+__global__ void __maxnreg__(128) env_solo_kernel_binary_small_s(const Params p, int mode) {
+    env_solo_body<0, 0, SOLO_SPEC_BINARY>(p, mode);
+}
+__global__ void __maxnreg__(128) env_solo_kernel_dungeon_s(const Params p, int mode) {
+    env_solo_body<2, 1, SOLO_SPEC_DUNGEON>(p, mode);
+}
 
 template <int DOM>
 struct SoloKernel;
@@ -1196,16 +1210,25 @@ template <>
 struct SoloKernel<0> {
     static constexpr auto fn = env_solo_kernel_binary;
     static constexpr auto fn_small = env_solo_kernel_binary_small;
+    static constexpr int spec = SOLO_SPEC_BINARY;
+    static constexpr auto fn_spec = env_solo_kernel_binary_s;
+    static constexpr auto fn_small_spec = env_solo_kernel_binary_small_s;
 };
 template <>
 struct SoloKernel<1> {
     static constexpr auto fn = env_solo_kernel_maze;
     static constexpr auto fn_small = env_solo_kernel_maze_small;
+    static constexpr int spec = 0;
+    static constexpr auto fn_spec = env_solo_kernel_maze;
+    static constexpr auto fn_small_spec = env_solo_kernel_maze_small;
 };
 template <>
 struct SoloKernel<2> {
     static constexpr auto fn = env_solo_kernel_dungeon;
     static constexpr auto fn_small = env_solo_kernel_dungeon_small;
+    static constexpr int spec = SOLO_SPEC_DUNGEON;
+    static constexpr auto fn_spec = env_solo_kernel_dungeon_s;
+    static constexpr auto fn_small_spec = env_solo_kernel_dungeon_small;  // block mode: generic
 };
 
 // ---- state export / import / metrics for the solo layout -------------------

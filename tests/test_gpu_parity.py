@@ -39,6 +39,14 @@ SMALL_CASES = ["c1_binary16_narrow_o31", "c2_maze16_turtle_o31", "c3_dungeon16_w
 
 
 @pytest.mark.parametrize("name", SMALL_CASES)
+def test_golden_env_case_generic_kernels(name, monkeypatch):
+    """The generic (runtime-flag) kernels on the cases the default launch
+    sends to a specialised kernel (env_kernels.cuh spec_of)."""
+    monkeypatch.setenv("LG_NO_SPEC", "1")
+    test_golden_env_case(name)
+
+
+@pytest.mark.parametrize("name", SMALL_CASES)
 def test_golden_env_case_lane_team_path(name, monkeypatch):
     """Maps <= 16x16 normally run one env per thread; force the lane-team
     kernel so both code paths are pinned on the same fixtures."""
@@ -297,12 +305,15 @@ WARP_MODE_CASES = [
 ]
 
 
-@pytest.mark.parametrize("layout", ["default", "stream", "slot"])
+@pytest.mark.parametrize("layout", ["default", "stream", "slot", "generic"])
 @pytest.mark.parametrize("case", range(len(WARP_MODE_CASES)))
 def test_large_batch_warp_mode_against_oracle(case, layout, monkeypatch):
     """Batches >= 4 warps/SM take the warp-mode store path; pin it to the oracle
-    with both shared-memory layouts (per-env slots, warp-wide bit stream)."""
-    if layout != "default":
+    with both shared-memory layouts (per-env slots, warp-wide bit stream), and
+    the generic kernel (LG_NO_SPEC=1) where the default launch is specialised."""
+    if layout == "generic":
+        monkeypatch.setenv("LG_NO_SPEC", "1")
+    elif layout != "default":
         monkeypatch.setenv("LG_STREAM", "1" if layout == "stream" else "0")
     kw, n, steps = WARP_MODE_CASES[case]
     cfg = EnvConfig(**kw)
