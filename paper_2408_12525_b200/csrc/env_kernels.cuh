@@ -872,6 +872,38 @@ __device__ LG_TEAM_WRITER_ATTR void write_obs_team(const Params &p, const Team<G
     for (uint32_t e = head + (n4 << 2) + t.lane; e < p.PE; e += G::TEAM) out[e] = team_elem(p, es, e);
 }
 
+// The specialised kernels' writer (no control planes: every element is a bit
+// of the image): 32-byte streaming stores (st.global.cs.v8.f32), 8 elements
+// from one funnel shift, after a head of at most 7 elements up to 32-byte
+// alignment (a c2 observation is 23,064 bytes, so env outputs start at any
+// multiple of 8 bytes).
+__device__ __forceinline__ void team_st_v8(float *ptr, const float *v) {
+    asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(ptr), "f"(v[0]), "f"(v[1]), "f"(v[2]),
+                 "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                 : "memory");
+}
+
+template <class G>
+__device__ LG_TEAM_WRITER_ATTR void write_obs_team_nc(const Params &p, const Team<G> &t, long long env, const unsigned char *es) {
+    const uint32_t *img = reinterpret_cast<const uint32_t *>(es);
+    const uint32_t PE = p.PE;
+    float *out = p.obs + (size_t)env * PE;
+    uint32_t head = (uint32_t)(((32u - (uint32_t)(reinterpret_cast<uintptr_t>(out) & 31u)) & 31u) >> 2);
+    if (head > PE) head = PE;
+    for (uint32_t e = t.lane; e < head; e += G::TEAM) out[e] = ((img[e >> 5] >> (e & 31)) & 1u) ? 1.0f : 0.0f;
+    const uint32_t n8 = (PE - head) >> 3;
+    for (uint32_t q = t.lane; q < n8; q += G::TEAM) {
+        const uint32_t le = head + (q << 3), wi = le >> 5;
+        const uint32_t x = __funnelshift_r(img[wi], img[wi + 1], le & 31);
+        float f[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) f[j] = (x & (1u << j)) ? 1.0f : 0.0f;
+        team_st_v8(out + le, f);
+    }
+    for (uint32_t e = head + (n8 << 3) + t.lane; e < PE; e += G::TEAM)
+        out[e] = ((img[e >> 5] >> (e & 31)) & 1u) ? 1.0f : 0.0f;
+}
+
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
@@ -992,6 +1024,7 @@ __global__ void __launch_bounds__(64, G::MINB) env_kernel(const Params p, int mo
                 t.sync();
                 if (obs_bits_of<S>(p)) write_obs_team_bits<G>(p, t, env, es);
                 else if (obs_u8_of<S>(p)) write_obs_team_u8<G>(p, t, env, es);
+                else if constexpr (S != 0) write_obs_team_nc<G>(p, t, env, es);
                 else write_obs_team<G>(p, t, env, es);
                 t.sync();  // the image doubles as union-find scratch
             }
@@ -1039,6 +1072,7 @@ __global__ void __launch_bounds__(64, G::MINB) env_kernel(const Params p, int mo
             t.sync();
             if (obs_bits_of<S>(p)) write_obs_team_bits<G>(p, t, env, es);
             else if (obs_u8_of<S>(p)) write_obs_team_u8<G>(p, t, env, es);
+            else if constexpr (S != 0) write_obs_team_nc<G>(p, t, env, es);
             else write_obs_team<G>(p, t, env, es);
         }
     }
