@@ -739,9 +739,12 @@ extern "C" int lg_create(const lg_config *cfg, int64_t n_envs, int64_t global_of
         e->E = e->threads / e->team;
         int rows = e->geo == 16 ? 16 : e->geo == 32 ? 32 : 64;
         int runs = e->geo == 64 ? 32 : 16;
-        size_t uf_bytes = (size_t)rows * runs * 2;
-        size_t scratch = uf_bytes > (size_t)p.img_words * 4 ? uf_bytes : (size_t)p.img_words * 4;
-        scratch = (scratch + 15) & ~(size_t)15;
+        // bit image, then union-find scratch (separate: the specialised kernels
+        // store part of the observation after the recompute), then control floats
+        const size_t uf_bytes = ((size_t)rows * runs * 2 + 15) & ~(size_t)15;
+        const size_t img_bytes = ((size_t)p.img_words * 4 + 15) & ~(size_t)15;
+        const size_t scratch = img_bytes + uf_bytes;
+        p.off_uf = (int)img_bytes;
         p.off_ctrl = (int)scratch;
         p.env_smem = (int)(scratch + 32);
         e->smem = (size_t)e->E * p.env_smem;
