@@ -748,6 +748,7 @@ __device__ LG_TEAM_RENDER_ATTR void render_env(const Params &p, const Team<G> &t
 #pragma unroll
             for (int q = 0; q < NPL; q++) any |= e.pl[q].r[k];
             const uint32_t rowoff = (uint32_t)i * OW;
+            LG_DCHECK((N + 1) * plane_bits + rowoff + OW <= (uint32_t)p.img_words * 32);
             uint64_t rows[N + 2];
             rows[0] = (uint64_t)(act & ~any);
 #pragma unroll

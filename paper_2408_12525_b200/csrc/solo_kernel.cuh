@@ -353,7 +353,13 @@ struct BitW {
     // stream; the first and a partial last word are shared with neighbouring
     // envs (rendered by other lanes) and are merged with atomicOr.
     bool stream, first, last;
+#ifdef LG_CHECKS
+    uint32_t lim = 0xFFFFFFFFu;  // words of the slot / stream (checked builds)
+#endif
     __device__ __forceinline__ void emit(uint32_t word) {
+#ifdef LG_CHECKS
+        LG_DCHECK((stream ? sidx(widx) : widx) < lim);
+#endif
         if (stream) {
             if (first) atomicOr(&dst[sidx(widx)], word);
             else dst[sidx(widx)] = word;
@@ -424,6 +430,9 @@ __device__ __forceinline__ void solo_render(const Params &p, const SoloEnv<DOM> 
     int n_in = g_hi > g_lo ? g_hi - g_lo : 0;
     int after = OH - before - n_in;
     BitW bw{slot, stream ? (bit0 >> 5) : 0u, 0, stream ? (int)(bit0 & 31) : 0, stream, true, last};
+#ifdef LG_CHECKS
+    bw.lim = stream ? (uint32_t)(p.stream_words > 0 ? p.stream_words : p.group_words) : (uint32_t)p.env_smem;
+#endif
     const uint32_t wm = mask16(W), am = mask16(e.w);
     // plane loop kept rolled (instruction-cache footprint). The stored plane
     // for `pl` is picked with an AND/OR mask, not a select: a select chain gets

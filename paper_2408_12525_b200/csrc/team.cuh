@@ -13,6 +13,20 @@
 #pragma once
 #include <stdint.h>
 
+// Debug builds (-DLG_CHECKS, tools/sanitize_cases.py): shared-memory index
+// bounds are checked on device and a violation traps the launch. compute-
+// sanitizer is closed on this GPU pool, so this is the out-of-bounds check.
+#ifdef LG_CHECKS
+#define LG_DCHECK(cond)         \
+    do {                        \
+        if (!(cond)) __trap();  \
+    } while (0)
+#else
+#define LG_DCHECK(cond) \
+    do {                \
+    } while (0)
+#endif
+
 namespace lg {
 
 template <int TEAM_, int RPL_, typename Row_, int MINB_ = 1>
@@ -286,6 +300,7 @@ __device__ __forceinline__ int count_regions_strips(const Team<G> &t, const Bd<G
     const Row K = (sA & (~Bv | sB)) | (sB & ~A);
     const int nk = popc(K);
     const int base = t.lane * G::BITS;
+    LG_DCHECK(base + nk <= G::TEAM * G::BITS);
     for (int i = 0; i < nk; i++) par[base + i] = (uint16_t)(base + i);
     const Row Kup = t.up(K), Bup = t.up(Bv);  // lane l-1: strip starts, row 2l-1
     t.sync();
@@ -297,6 +312,7 @@ __device__ __forceinline__ int count_regions_strips(const Team<G> &t, const Bd<G
         CS &= CS - 1;
         Row upto = (c == G::BITS - 1) ? ~Row(0) : ((Row(2) << c) - Row(1));
         int i1 = popc(K & upto) - 1, i2 = popc(Kup & upto) - 1;
+        LG_DCHECK(t.lane > 0 && i1 >= 0 && i1 < nk && i2 >= 0 && i2 < G::BITS);
         links += uf_unite(par, base + i1, base - G::BITS + i2);
     }
     return t.sum(nk - links);
@@ -314,6 +330,7 @@ __device__ __forceinline__ int count_regions(const Team<G> &t, const Bd<G> &pass
         int base = t.row(k) * G::RUNS;
         int i = 0;
         while (s) {
+            LG_DCHECK(i < G::RUNS);
             par[base + i] = (uint16_t)(base + i);
             i++;
             s &= s - 1;
@@ -342,6 +359,7 @@ __device__ __forceinline__ int count_regions(const Team<G> &t, const Bd<G> &pass
             CS &= CS - 1;
             Row upto = (c == G::BITS - 1) ? ~Row(0) : ((Row(2) << c) - Row(1));
             int ir = popc(SR & upto) - 1, ia = popc(SA & upto) - 1;
+            LG_DCHECK(ir >= 0 && ir < G::RUNS && ia >= 0 && ia < G::RUNS && row < G::ROWS);
             links += uf_unite(par, row * G::RUNS + ir, (row - 1) * G::RUNS + ia);
         }
     }
