@@ -102,18 +102,23 @@ class EnvConfig:
     def init_cdf(self) -> np.ndarray:
         """numpy ``Generator.choice`` cdf of the init weights (grid.py:153-191)."""
         d = self.domain_obj
-        weights = self.init_weights if self.init_weights else d.default_init_weights
-        vec = np.zeros(d.n_tiles, dtype=np.float64)
-        for key, w in weights.items():
-            tid = d.tile_id(key) if isinstance(key, str) else int(key)
-            if not 0 <= tid < d.n_tiles:
-                raise ValueError(f"weight for non-writable tile id {tid}")
-            if w < 0:
-                raise ValueError(f"negative weight for tile {key!r}")
-            vec[tid] = w
-        total = float(vec.sum())
-        if total <= 0:
-            raise ValueError("tile weights sum to zero")
-        cdf = (vec / total).cumsum()
+        cdf = normalize_weights(d, self.init_weights if self.init_weights else d.default_init_weights).cumsum()
         cdf /= cdf[-1]
         return cdf
+
+
+def normalize_weights(domain: Domain, weights) -> np.ndarray:
+    """grid.normalize_weights (grid.py:153-166): weights keyed by tile name or
+    id -> dense probability vector, with the reference's errors."""
+    vec = np.zeros(domain.n_tiles, dtype=np.float64)
+    for key, w in weights.items():
+        tid = domain.tile_id(key) if isinstance(key, str) else int(key)
+        if not 0 <= tid < domain.n_tiles:
+            raise ValueError(f"weight for non-writable tile id {tid}")
+        if w < 0:
+            raise ValueError(f"negative weight for tile {key!r}")
+        vec[tid] = w
+    total = float(vec.sum())
+    if total <= 0:
+        raise ValueError("tile weights sum to zero")
+    return vec / total

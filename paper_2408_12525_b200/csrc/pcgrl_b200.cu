@@ -12,6 +12,8 @@
 #include <utility>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/pcgrl_b200.h"
 #include "env_kernels.cuh"
 #include "host_expand.h"
@@ -58,6 +60,23 @@ struct DeviceGuard {
 #define DEVICE_GUARD(dev)       \
     DeviceGuard _dg(dev);       \
     CU(_dg.err)
+
+// NVTX ranges around every library call that launches work (nsys / ncu
+// --nvtx attribute kernels to them; without a tool attached they cost a
+// few nanoseconds).
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+static const char *mode_name(int mode) {
+    switch (mode) {
+    case MODE_STEP: return "lg_step";
+    case MODE_RESET: return "lg_reset";
+    case MODE_OBSERVE: return "lg_observe";
+    case MODE_RECOMPUTE: return "lg_recompute";
+    default: return "lg_reprice";
+    }
+}
 
 // The dynamic shared memory limit is a per-device function attribute: raise it
 // once per (kernel, device) pair, on the current device.
@@ -868,6 +887,7 @@ static int run_mode(lg_env *e, int mode, const long long *actions, void *obs, do
         return LG_EINVAL;
     }
     DEVICE_GUARD(e->device);
+    NvtxRange nv(mode_name(mode));
     Params p = e->base;
     p.actions = actions;
     p.obs = reinterpret_cast<float *>(obs);  // uint8 bytes when obs_u8
@@ -949,6 +969,7 @@ extern "C" int lg_step_host(lg_env *e, const int64_t *actions_host, void *obs_ho
         return LG_EINVAL;
     }
     DEVICE_GUARD(e->device);
+    NvtxRange nv("lg_step_host");
     size_t B = (size_t)e->B;
     const size_t n_elems = B * (size_t)e->C * e->OH * e->OW;
     size_t obs_bytes = n_elems * (e->base.obs_u8 ? 1 : sizeof(float));
@@ -1149,6 +1170,7 @@ extern "C" int lg_policy_trunk(const void *c1_tiles, int64_t n_envs, int P1, con
             set_err("policy_trunk operand blocks must be 16-byte aligned");
             return LG_EINVAL;
         }
+    NvtxRange nv("lg_policy_trunk");
     CU(smem_attr((const void *)trunk_kernel, (int)TK_SMEM));
     TrunkParams tp;
     tp.c1 = reinterpret_cast<const __nv_bfloat16 *>(c1_tiles);

@@ -5,7 +5,7 @@ ids in declaration order, ``border_id == n_tiles`` for out-of-map cells, the
 pinnable ("pivotal") tiles, the passable sets used by the path and region
 metrics, and the canonical metric order that fixes the loss accumulation
 order. These tables are compiled into the CUDA kernels as template
-constants (see ``csrc/domain.cuh``); this module is the host-side view.
+constants (``Dom<DOM>`` in ``csrc/env_kernels.cuh``); this module is the host-side view.
 """
 from __future__ import annotations
 
@@ -22,7 +22,7 @@ TILE_CHARS = {"air": ".", "wall": "#", "player": "P", "door": "D", "key": "K", "
 @dataclass(frozen=True)
 class Domain:
     name: str
-    code: int                       # kernel template id (csrc/domain.cuh)
+    code: int                       # kernel template id (Dom<code> in csrc/env_kernels.cuh)
     tiles: tuple[str, ...]
     pivotal: tuple[str, ...]
     path_passable: tuple[str, ...]
