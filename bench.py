@@ -252,6 +252,11 @@ def main():
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if "RANK" in os.environ:
+        # NCCL reads its debug settings once, when torch first touches it: set
+        # them before torch is imported (communicator INIT lines: rank count)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         args.gpus = world
@@ -284,11 +289,17 @@ def main():
         os.environ.setdefault("LG_HOST_THREADS", str(len(cpus)))
     distributed = world > 1 or "TORCHELASTIC_RUN_ID" in os.environ or "MASTER_ADDR" in os.environ
     if distributed:
-        # communicator setup is logged (stderr) so the rank count can be checked
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        # communicator setup is logged so the rank count can be checked. NCCL
+        # (and torch's NCCL banner) write to file descriptor 1: point it at
+        # stderr for the whole run and keep Python's stdout on the original
+        # descriptor, so stdout carries only the one JSON line.
+        sys.stdout.flush()
+        out_fd = os.dup(1)
+        os.dup2(2, 1)
+        sys.stdout = os.fdopen(out_fd, "w", buffering=1)
         dist.init_process_group("nccl", device_id=dev)
+        print(f"[bench] rank {rank}/{world}: NCCL communicator of {dist.get_world_size()} ranks on cuda:{local_rank}",
+              file=sys.stderr, flush=True)
     from paper_2408_12525_b200 import _lib
     from paper_2408_12525_b200.env import INFO_KEYS, BatchEnv, NumpyBatchEnv
 
