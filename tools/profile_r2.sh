@@ -8,7 +8,7 @@ for c in $cfgs; do
   case $c in
     c4|c2) k=regex:env_kernel ;;
     c3) k=regex:env_solo_kernel_dungeon ;;
-    c5s) k=regex:env_solo_kernel_binary ;;
+    c5s|c5) k=regex:env_solo_kernel_binary ;;
   esac
   extra=""; cc=$c
   if [ $c = c5s ]; then extra="--envs 131072"; cc=c5; fi
