@@ -240,6 +240,27 @@ __device__ __forceinline__ int team_count(const Team<G> &t, const Bd<G> &b) {
     return t.sum(b.count());
 }
 
+// Number of distinct connected components of `pass` among the cells of `rem`
+// (4-connected): BFS from the lowest remaining cell until every remaining cell
+// is reached or the component is exhausted, drop what it reached, repeat.
+template <class G>
+__device__ __forceinline__ int components_among(const Team<G> &t, Bd<G> rem, const Bd<G> &pass,
+                                                typename G::Row wm) {
+    int k = 0;
+    while (t.any(rem.nz())) {
+        ++k;
+        Bd<G> f = cell_board(t, lowest_cell(t, rem));
+        Bd<G> vis = f;
+        while (t.any(andnot(rem, vis).nz())) {
+            f = andnot(dilate(t, f, wm) & pass, vis);
+            if (!t.any(f.nz())) break;
+            vis = vis | f;
+        }
+        rem = andnot(rem, vis);
+    }
+    return k;
+}
+
 // Backend of the generic metric code for a lane team (team.cuh).
 template <class G>
 struct TeamK {
@@ -261,20 +282,52 @@ struct TeamK {
     __device__ __forceinline__ int regions(const B &pass, void *uf) const {
         return count_regions(t, pass, reinterpret_cast<uint16_t *>(uf));
     }
+    // Change of the region count (count_regions, pathfind.py:116-130) when cell
+    // x = (xr, xc) switched passability and nothing else changed: with G the
+    // passable set without x and k the number of components of G among x's
+    // passable neighbours, adding x merges them into one (1 - k), removing x
+    // splits its component into k (k - 1). Exact, and a few BFS layers on
+    // typical maps instead of a union-find over the whole grid.
+    static constexpr bool kIncRegions = true;
+    __device__ __forceinline__ int regions_delta(const B &pass_new, int xr, int xc, bool old_in) const {
+        const B x = cell_board(t, xr * 64 + xc);
+        const bool new_in = t.any((x & pass_new).nz());
+        if (new_in == old_in) return 0;
+        const B g = andnot(pass_new, x);
+        const int k = components_among(t, dilate(t, x, wm) & g, g, wm);
+        return new_in ? 1 - k : k - 1;
+    }
 };
 
 // compute_metrics_batch for one level (problems.py:105-243), generic over the
 // board backend K (lane team or single thread). pl: stored tile planes
 // (tile p+1), act: active mask, g: metric generator (binary draw only).
+// Incremental region count after a one-cell write (the lane-team kernels'
+// steps): the write position, whether the old tile was passable for the
+// region metric, and the (exact) count before the write.
+struct RegInc {
+    int xr, xc;
+    bool old_in;
+    int old_regions;
+};
+
+template <class K, class B>
+__device__ __forceinline__ int regions_of(const K &k, const B &pass, void *uf, const RegInc *inc) {
+    if constexpr (K::kIncRegions) {
+        if (inc) return inc->old_regions + k.regions_delta(pass, inc->xr, inc->xc, inc->old_in);
+    }
+    return k.regions(pass, uf);
+}
+
 template <class K, int DOM>
 __device__ __forceinline__ void compute_metrics(const K &k, const typename K::B *pl, const typename K::B &act, Pcg &g,
-                                void *uf, int *val, int &unr) {
+                                void *uf, int *val, int &unr, const RegInc *inc = nullptr) {
     using B = typename K::B;
     unr = 0;
     if constexpr (DOM == 0) {
         // _binary_metrics (problems.py:136-173)
         B pass = andnot(act, pl[0]);
-        val[1] = k.regions(pass, uf);
+        val[1] = regions_of(k, pass, uf, inc);
         int cnt = k.count(pass);
         val[0] = 0;
         if (cnt > 0) {
@@ -292,7 +345,7 @@ __device__ __forceinline__ void compute_metrics(const K &k, const typename K::B 
         int np = k.count(players), nd = k.count(doors);
         val[2] = np;
         val[3] = nd;
-        val[1] = k.regions(pass, uf);
+        val[1] = regions_of(k, pass, uf, inc);
         int d = -1, dummy;
         if (np > 0 && nd > 0) k.template touch<false>(players, pass, doors, doors, false, d, dummy);
         bool bad = d < 0;
@@ -317,7 +370,7 @@ __device__ __forceinline__ void compute_metrics(const K &k, const typename K::B 
         val[6] = badn ? 0 : nearv;
         unr = (bad ? 1 : 0) | (badn ? 64 : 0);
         B open = andnot(andnot(act, pl[0]), enemy);  // AIR | PLAYER | KEY | DOOR
-        val[1] = k.regions(open, uf);
+        val[1] = regions_of(k, open, uf, inc);
     }
 }
 
@@ -343,16 +396,27 @@ __device__ __forceinline__ double loss_of(const Params &p, const int *val, int u
 }
 
 // _recompute (env.py:332-347)
+// unr bit: the stored region count is exact for the stored map (set by every
+// recompute, clear after a state import), so a step may update it incrementally
+constexpr int UNR_REGIONS_EXACT = 1 << 15;
+
+// passable for the region metric: binary AIR; maze all but WALL; dungeon all but WALL and ENEMY
+template <int DOM>
+__device__ __forceinline__ bool regions_pass_tile(int tile) {
+    return DOM == 0 ? tile == 0 : DOM == 1 ? tile != 1 : (tile != 1 && tile != 2);
+}
+
 template <class G, int DOM, int S = 0>
 __device__ __forceinline__ void recompute(const Params &p, const Team<G> &t, EnvRegs<G, DOM> &e, uint16_t *uf,
-                          bool reset) {
+                          bool reset, const RegInc *inc = nullptr) {
     using Row = typename G::Row;
     TeamK<G> k{t, low_mask<Row>(p.W)};
     Bd<G> act = rect_board(t, e.h, e.w);
     // _metric_rngs (env.py:327-330): the env stream, or a fresh default_rng(metric_seed)
     Pcg mg = e.g;
     if (det_of<S>(p)) seedseq_pcg((uint64_t)e.mseed, false, 0, mg);
-    compute_metrics<TeamK<G>, DOM>(k, e.pl, act, mg, uf, e.val, e.unr);
+    compute_metrics<TeamK<G>, DOM>(k, e.pl, act, mg, uf, e.val, e.unr, inc);
+    e.unr |= UNR_REGIONS_EXACT;
     if (!det_of<S>(p)) e.g = mg;
     double l = loss_of<DOM>(p, e.val, e.unr, e.lo, e.hi);
     e.prev_loss = l;
@@ -944,7 +1008,7 @@ __global__ void __launch_bounds__(64, G::MINB) env_kernel(const Params p, int mo
         bool rows_dirty = false, metrics_dirty = false, rng_dirty = false;
         bool wrote = false, reset_now = false;
         double before = 0.0;
-        int dirty_row = -1;
+        int dirty_row = -1, wcol = 0, wcur = 0;  // the write (row, column, old tile)
         if (mode == MODE_STEP) {
             long long a = p.actions[env];
             bool ok = a >= 0 && a < p.n_actions;
@@ -1001,6 +1065,8 @@ __global__ void __launch_bounds__(64, G::MINB) env_kernel(const Params p, int mo
                     for (int q = 0; q < NPL; q++) e.pl[q].r[k] = (e.pl[q].r[k] & ~m) | (q == tile - 1 ? m : Row(0));
                 }
                 dirty_row = r;
+                wcol = c;
+                wcur = cur;
                 e.changes += 1;
                 before = e.prev_loss;
             }
@@ -1058,7 +1124,11 @@ __global__ void __launch_bounds__(64, G::MINB) env_kernel(const Params p, int mo
                 rows_dirty = true;
             }
             if (pass == 1 || wrote) {
-                recompute<G, DOM, S>(p, t, e, uf, pass == 1);  // _recompute (env.py:332-347)
+                // a step's one-cell write updates the region count incrementally
+                // (TeamK::regions_delta) when the stored count is exact
+                RegInc ri{dirty_row, wcol, regions_pass_tile<DOM>(wcur), e.val[1]};
+                const bool inc = pass == 0 && mode == MODE_STEP && (e.unr & UNR_REGIONS_EXACT);
+                recompute<G, DOM, S>(p, t, e, uf, pass == 1, inc ? &ri : nullptr);  // _recompute (env.py:332-347)
                 metrics_dirty = rng_dirty = true;
             }
             if (pass == 0 && mode == MODE_STEP) {

@@ -91,6 +91,8 @@ __device__ __forceinline__ SB dilate_sb(const SB &f) {
 // Backend of the generic metric code (env_kernels.cuh) for one env per thread.
 struct SoloK {
     using B = SB;
+    static constexpr bool kIncRegions = false;  // register region count: cheap already
+    __device__ __forceinline__ int regions_delta(const SB &, int, int, bool) const { return 0; }
     __device__ __forceinline__ int count(const SB &b) const { return b.count(); }
     __device__ __forceinline__ SB cell(int flat) const {
         SB b;
