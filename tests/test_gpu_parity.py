@@ -605,3 +605,43 @@ def test_lane_team_first_touch_depths(domain, side, pins, monkeypatch):
         assert np.array_equal(s1["unreach"], s2["unreach"]), t
         seen.update(int(v) % 2 for v in s2["values"][0] if v > 0)
     assert seen == {0, 1}  # touched at even and at odd depths
+
+
+INC_CASES = [
+    # (EnvConfig kwargs, envs, steps): lane-team kernels whose steps update the
+    # region count incrementally (TeamK::regions_delta)
+    (dict(domain="binary", max_width=64, max_height=64, obs_size=7), 512, 150),    # c4 shape (G64)
+    (dict(domain="maze", representation="turtle"), 2048, 300),                     # c2 shape (G16)
+    (dict(domain="dungeon", max_width=30, max_height=24, obs_size=9,
+          pinpoints=("player", "key", "door")), 600, 200),                         # G32, dungeon open set
+    (dict(domain="binary", max_width=40, max_height=40, obs_size=5, randomize_shape=True,
+          max_steps=60), 600, 200),                                                # G64, resets mid-run
+]
+
+
+@pytest.mark.parametrize("case", range(len(INC_CASES)))
+def test_incremental_region_count_against_oracle(case):
+    """Every step's region count (and all other metrics) equals the oracle's
+    full recomputation, across auto-resets and after a state import (which
+    drops the 'count is exact' bit, so the next write recomputes in full)."""
+    kw, n, steps = INC_CASES[case]
+    cfg = EnvConfig(**kw)
+    env = BatchEnv(cfg, n, seed=case)
+    ref = O.OracleBatchEnv(cfg, n, seed=case)
+    assert np.array_equal(_np(env.reset()), ref.reset())
+    act = np.random.default_rng(100 + case)
+    for t in range(steps):
+        a = act.integers(0, cfg.n_actions, size=n)
+        _, r1, d1, _ = env.step(a)
+        _, r2, d2, _ = ref.step(a)
+        assert np.array_equal(_np(r1), r2), t
+        if t % 10 == 9:
+            s1, s2 = env.state_dict(), ref.state_dict()
+            assert np.array_equal(s1["values"], s2["values"]), t
+        if t == steps // 2:  # round-trip through a state import mid-run
+            twin = BatchEnv(cfg, n, seed=999)
+            twin.load_state_dict(env.state_dict())
+            env = twin
+    s1, s2 = env.state_dict(), ref.state_dict()
+    for k in ("tiles", "values", "unreach", "prev_loss", "rng"):
+        assert np.array_equal(s1[k], s2[k]), k
