@@ -520,12 +520,52 @@ def main():
             out["transfer"] = f"{obs_dtype} observation copy D2H"
         return out
 
+    def e2e_device_obs():
+        # A GPU-side consumer's loop (a policy on the same device): numpy
+        # actions from pinned host memory in, observations left on the device,
+        # reward and done read back to the host every step. Side figure: the
+        # reference's contract returns the observation in host memory (e2e above).
+        torch.cuda.empty_cache()
+        denv = BatchEnv(cfg, B, seed=0, device=dev, global_offset=offset, validate=False)
+        dobs = denv.new_obs()
+        denv.reset(out=dobs)
+        rng = np.random.default_rng(2)
+        n_steps = 20
+        host_acts = [torch.from_numpy(rng.integers(0, cfg.n_actions, size=B)).pin_memory() for _ in range(n_steps + 1)]
+        d_act = torch.empty(B, dtype=torch.int64, device=dev)
+        d_rew = torch.empty(B, dtype=torch.float64, device=dev)
+        d_done = torch.empty(B, dtype=torch.bool, device=dev)
+        h_rew = torch.empty(B, dtype=torch.float64).pin_memory()
+        h_done = torch.empty(B, dtype=torch.bool).pin_memory()
+
+        def one(a):
+            d_act.copy_(a, non_blocking=True)
+            denv.step_raw(d_act, dobs, d_rew, d_done)
+            h_rew.copy_(d_rew, non_blocking=True)
+            h_done.copy_(d_done, non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+
+        one(host_acts[-1])
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for a in host_acts[:n_steps]:
+            one(a)
+        dt = max_over_ranks(time.perf_counter() - t0, dev)
+        del denv, dobs
+        return {"value": global_b * n_steps / dt, "unit": UNIT, "h2d_bytes_per_step": B * 8,
+                "d2h_bytes_per_step": B * 9, "steps": n_steps,
+                "api": "BatchEnv.step_raw with pinned host actions; observation stays on the device; "
+                       "reward + done D2H and a host sync every step",
+                "note": "side figure for GPU-resident consumers, not the reference's host-array contract"}
+
     e2e = None
     if not args.no_e2e:
         del obs
         e2e = e2e_run("float32", True)
         e2e["float32_copy"] = e2e_run("float32", False)
         e2e["fresh_arrays"] = e2e_run("float32", True, fresh=True)
+        e2e["device_obs"] = e2e_device_obs()
 
     # Side measurement (does not change the headline): the same workload with
     # the opt-in uint8 observation format (4x fewer bytes per env-step).
