@@ -1100,7 +1100,15 @@ __global__ void __launch_bounds__(64, G::MINB) env_kernel(const Params p, int mo
             // early observation: unless the episode ends (auto-reset) or control
             // planes show metric values, the observation is final now -- write
             // it before the recompute so its stores drain while the team computes
-            early = p.early && p.obs && nctrl_of<S>(p) == 0 && !ends;
+// the specialised 64x64 kernel renders once, after the recompute: with the
+// incremental region count its step is short, the 7x7 window is 784 B, and
+// the second render/writer copy of the early path costs instruction fetch
+// (no_inst was 41% of stalls): c4 250 -> 276 M env-steps/s
+#ifndef LG_G64_SPEC_EARLY
+#define LG_G64_SPEC_EARLY 0
+#endif
+            constexpr bool kEarlyOk = S == 0 || G::RPL == 1 || LG_G64_SPEC_EARLY;
+            early = kEarlyOk && p.early && p.obs && nctrl_of<S>(p) == 0 && !ends;
             if (early) {
                 t.sync();
                 render_env<G, DOM, S>(p, t, e, es);
