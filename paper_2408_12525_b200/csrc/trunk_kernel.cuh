@@ -25,10 +25,10 @@
 //       weights W[n, c*P2*P2 + p] (torch flattens [C, H, W]),
 //       ((k/8)*8 + n/8)*64 + (n%8)*8 + k%8
 //
-// Warp roles (320 threads): warp 0 = producers (lane 0: cp.async.bulk of the
+// Warp roles (352 threads): warp 0 = producers (lane 0: cp.async.bulk of the
 // conv1 pixel blocks, lane 1: the FC weight blocks; mbarrier complete_tx);
-// warp 1 = TMEM allocator + MMA issuer (the warp runs the loop, an elected
-// lane issues every tcgen05.mma/commit); warps
+// warp 1 = TMEM allocator + conv2 MMA issuer and warp 10 = FC MMA issuer (each
+// warp runs its loop, an elected lane issues its tcgen05.mma/commit); warps
 // 2..9 = two epilogue groups (alternate output rows; tcgen05.ld of their TMEM
 // lane quadrant, one env per thread).
 //
@@ -179,7 +179,7 @@ constexpr int TK_RING = 4;                    // conv1 rows in shared memory
 constexpr int TK_W3 = 8;                      // FC weight blocks in flight (released in pairs)
 constexpr int TK_EPI = 2;                     // epilogue warp groups (output row R -> group R % 2)
 constexpr int TK_A3G = 2;                     // conv2 activation blocks (FC A operand) per group
-constexpr int TK_THREADS = 64 + 128 * TK_EPI;
+constexpr int TK_THREADS = 64 + 128 * TK_EPI + 32;  // + the FC issuer warp
 constexpr int TK_MAXNA = 16;
 constexpr uint32_t TK_BLK = 4096;             // one 128 x 16 bf16 block
 // TMEM columns: one conv2 accumulator row (CW pixels x 32 channels) per epilogue group + FC accumulator
@@ -204,8 +204,16 @@ template <int CW>
 __device__ __forceinline__ void conv2_row(uint32_t acc, const uint64_t (&dr)[3], uint64_t d_w2) {
 #pragma unroll
     for (int dy = 0; dy < 3; dy++) {
+        // blocks in stride-3 order (0, 3, 6, 1, 4, 7, 2, 5, 8): consecutive MMAs
+        // write disjoint accumulator ranges (block c covers pixels c-2..c)
 #pragma unroll
-        for (int c = 0; c < CW + 2; c++) {
+        for (int ci = 0; ci < CW + 2; ci++) {
+#ifndef TK_EXP_LINEAR_ORDER
+            constexpr int NB = CW + 2, G0 = (NB + 2) / 3, G1 = (NB + 1) / 3;
+            const int c = ci < G0 ? 3 * ci : ci < G0 + G1 ? 3 * (ci - G0) + 1 : 3 * (ci - G0 - G1) + 2;
+#else
+            const int c = ci;
+#endif
             const int xlo = c - 2 > 0 ? c - 2 : 0, xhi = c < CW - 1 ? c : CW - 1;
             const int jb = xlo - c + 2, n = 32 * (xhi - xlo + 1);
             tc::mma_bf16(acc + 32u * xlo, dr[dy] + ((uint32_t)c * TK_BLK >> 4),
@@ -308,39 +316,12 @@ __global__ void __launch_bounds__(TK_THREADS, 1) trunk_kernel(const TrunkParams 
 #else
 #define TKT(k)
 #endif
-        constexpr uint32_t ID3 = tc::idesc_bf16(128, 64);
         tc::mbar_wait(BAR(W2F), 0);
         // descriptor bases; a shared-memory offset is added as (bytes >> 4)
         const uint64_t d_ring = tc::sdesc(s0 + TK_OFF_RING, 2048, 128);
         const uint64_t d_w2 = tc::sdesc(s0 + TK_OFF_W2, 1536, 128);
-        const uint64_t d_a3 = tc::sdesc(s0 + TK_OFF_A3, 2048, 128);
-        const uint64_t d_w3 = tc::sdesc(s0 + TK_OFF_W3, 1024, 128);
         int Lw = 0;   // conv1 rows waited for
-        int pix = 0;  // FC pixels issued (global order)
-        int kg0 = 0, kg1 = 0;  // A3 blocks consumed per epilogue group
-        auto fc_row = [&](int R, int cw) {  // D3 += relu(conv2)(pixel) x W3(pixel) for row R's pixels
-            const int g = R % TK_EPI;
-            int &kg = g ? kg1 : kg0;
-            for (int j = 0; j < cw; j++, pix++, kg++) {
-                const int a = g * TK_A3G + kg % TK_A3G, w = pix % TK_W3;
-                TKT(0);
-                tc::mbar_wait(BAR(A3F + a), (uint32_t)((kg / TK_A3G) & 1));
-                TKT(1);
-                tc::mbar_wait(BAR(W3F + w), (uint32_t)((pix / TK_W3) & 1));
-                TKT(2);
-                tc::tc_after();
-                if (tc::elect_one()) {
-                    tc::mma_bf16(T_D3, d_a3 + ((uint32_t)a * 8192u >> 4), d_w3 + ((uint32_t)w * 4096u >> 4), ID3,
-                                 pix > 0 ? 1u : 0u);
-                    tc::mma_bf16(T_D3, d_a3 + (((uint32_t)a * 8192u + 4096u) >> 4),
-                                 d_w3 + (((uint32_t)w * 4096u + 2048u) >> 4), ID3, 1u);
-                    tc::mma_commit(BAR(A3E + a));
-                    if (w & 1) tc::mma_commit(BAR(W3E + w / 2));
-                }
-                __syncwarp();
-            }
-        };
-        int R = 0, prev_cw = 0;
+        int R = 0;
         for (int cx = 0; cx < nch; cx++) {
             const int cw = min(TK_CW, P2 - cx * TK_CW);
             const int L0 = cx * P1;
@@ -374,19 +355,47 @@ __global__ void __launch_bounds__(TK_THREADS, 1) trunk_kernel(const TrunkParams 
                     }
                 }
                 __syncwarp();
-                if (R > 0) fc_row(R - 1, prev_cw);  // the previous row's FCs overlap this row's conv2
-                prev_cw = cw;
+                TKT(5);
             }
         }
-        fc_row(R - 1, prev_cw);
-        if (tc::elect_one()) tc::mma_commit(BAR(D3F));
-        __syncwarp();
 #ifdef TK_PROF
         TKT(0);
         prof[7] = clock64() - t0;
         if (lane == 0)
             for (int k2 = 0; k2 < 8; k2++) g_tk_prof[blockIdx.x & 1023][k2] = prof[k2];
 #endif
+    } else if (warp == 2 + 4 * TK_EPI) {
+        // ---------------- FC issuer: a second MMA-issuing warp, so the FC's
+        // waits (epilogue activations, weight blocks) and commits never stall the
+        // conv2 issue (tcgen05.commit tracks the issuing thread's own MMAs) ----------------
+        constexpr uint32_t ID3 = tc::idesc_bf16(128, 64);
+        const uint64_t d_a3 = tc::sdesc(s0 + TK_OFF_A3, 2048, 128);
+        const uint64_t d_w3 = tc::sdesc(s0 + TK_OFF_W3, 1024, 128);
+        int pix = 0, kg0 = 0, kg1 = 0, R = 0;  // FC pixels issued; A3 blocks consumed per epilogue group
+        for (int cx = 0; cx < nch; cx++) {
+            const int cw = min(TK_CW, P2 - cx * TK_CW);
+            for (int y = 0; y < P2; y++, R++) {
+                const int g = R % TK_EPI;
+                int &kg = g ? kg1 : kg0;
+                for (int j = 0; j < cw; j++, pix++, kg++) {  // D3 += relu(conv2)(pixel) x W3(pixel)
+                    const int a = g * TK_A3G + kg % TK_A3G, w = pix % TK_W3;
+                    tc::mbar_wait(BAR(A3F + a), (uint32_t)((kg / TK_A3G) & 1));
+                    tc::mbar_wait(BAR(W3F + w), (uint32_t)((pix / TK_W3) & 1));
+                    tc::tc_after();
+                    if (tc::elect_one()) {
+                        tc::mma_bf16(T_D3, d_a3 + ((uint32_t)a * 8192u >> 4), d_w3 + ((uint32_t)w * 4096u >> 4), ID3,
+                                     pix > 0 ? 1u : 0u);
+                        tc::mma_bf16(T_D3, d_a3 + (((uint32_t)a * 8192u + 4096u) >> 4),
+                                     d_w3 + (((uint32_t)w * 4096u + 2048u) >> 4), ID3, 1u);
+                        tc::mma_commit(BAR(A3E + a));
+                        if (w & 1) tc::mma_commit(BAR(W3E + w / 2));
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+        if (tc::elect_one()) tc::mma_commit(BAR(D3F));
+        __syncwarp();
     } else {  // ---------------- epilogue: TK_EPI groups of 4 warps, one env (TMEM lane) per thread ----------------
         const int grp = (warp - 2) >> 2;  // output row R is handled by group R % TK_EPI
         const int q = warp & 3;           // TMEM lane quadrant this warp may access
@@ -442,8 +451,12 @@ __global__ void __launch_bounds__(TK_THREADS, 1) trunk_kernel(const TrunkParams 
                         __nv_bfloat162 h2 = __floats2bfloat162_rn(x0, x1);
                         wd[jj] = *reinterpret_cast<uint32_t *>(&h2);
                     }
+#ifndef TK_EXP_NO_A3_STORE  // timing experiments only
                     *reinterpret_cast<uint4 *>(a3 + ((kc * 16 + (m >> 3)) * 128 + (m & 7) * 16)) =
                         make_uint4(wd[0], wd[1], wd[2], wd[3]);
+#else
+                    if (wd[0] == 0x12345678u) *reinterpret_cast<uint4 *>(a3) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+#endif
                 }
                 tc::fence_proxy_async();
                 tc::mbar_arrive(BAR(A3F + a));

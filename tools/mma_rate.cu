@@ -100,6 +100,71 @@ __global__ void __launch_bounds__(128, 1) pattern_kernel(int R, long long *out) 
     }
 }
 
+// the trunk's conv2 rows exactly: 27 MMAs per row (3 dy x 9 blocks, N = 32/64/96
+// at the edges, D ranges overlapping), the conv1 ring cycling over 4 rows
+__global__ void __launch_bounds__(128, 1) conv2_rows_kernel(int rows, long long *out) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t slot;
+    const uint32_t s0 = tc::su32(sm);
+    for (int i = threadIdx.x; i < 200 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t *>(sm)[i] = 0;
+    tc::fence_proxy_async();
+    if (threadIdx.x == 0) {
+        tc::mbar_init(tc::su32(&bar), 1);
+        tc::fence_barrier_init();
+    }
+    if (threadIdx.x < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(tc::su32(&slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc::tc_before();
+    __syncthreads();
+    tc::tc_after();
+    const uint32_t tmem = slot;
+    if (threadIdx.x < 32) {
+        const uint64_t d_ring = tc::sdesc(s0, 2048, 128), d_w2 = tc::sdesc(s0 + 147456, 1536, 128);
+        long long t0 = clock64();
+        for (int y = 0; y < rows; y++) {
+            const uint32_t acc = tmem + (uint32_t)(y & 1) * 224u;
+            uint64_t dr[3];
+            for (int dy = 0; dy < 3; dy++) dr[dy] = d_ring + ((uint32_t)(((y + dy) & 3) * 9) * 4096u >> 4);
+            if (tc::elect_one()) {
+#pragma unroll
+                for (int dy = 0; dy < 3; dy++)
+#pragma unroll
+                    for (int c = 0; c < 9; c++) {
+                        const int xlo = c - 2 > 0 ? c - 2 : 0, xhi = c < 6 ? c : 6;
+                        const int jb = xlo - c + 2, n = 32 * (xhi - xlo + 1);
+                        tc::mma_bf16(acc + 32u * xlo, dr[dy] + ((uint32_t)c * 4096u >> 4),
+                                     d_w2 + ((uint32_t)(dy * 3072 + jb * 512) >> 4), tc::idesc_bf16(128, n), 1u);
+                    }
+            }
+            __syncwarp();
+        }
+        if (tc::elect_one()) tc::mma_commit(tc::su32(&bar));
+        __syncwarp();
+        tc::mbar_wait(tc::su32(&bar), 0);
+        if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = clock64() - t0;
+    }
+    tc::tc_before();
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        tc::tc_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+}
+
+void run_conv2_rows(long long *d) {
+    const int rows = 200;
+    cudaFuncSetAttribute(conv2_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    conv2_rows_kernel<<<148, 128, 200 * 1024>>>(rows, d);
+    conv2_rows_kernel<<<148, 128, 200 * 1024>>>(rows, d);
+    long long c = 0;
+    cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+    printf("conv2 rows: %.1f cycles/row, %.1f cycles/MMA %s\n", (double)c / rows, (double)c / rows / 27,
+           cudaGetErrorString(cudaGetLastError()));
+}
+
 template <bool VARN>
 void run_pattern(long long *d) {
     const int R = 4096;
@@ -128,8 +193,8 @@ int main() {
     long long *d;
     cudaMalloc(&d, 8);
     run<96, false>(d);
-    run<96, false, 4>(d);
     run_pattern<false>(d);
     run_pattern<true>(d);
+    run_conv2_rows(d);
     return 0;
 }

@@ -30,5 +30,5 @@ lib = _lib.load()
 lib.lg_trunk_prof.argtypes = [ctypes.c_void_p, ctypes.c_int]
 _lib.check(lib.lg_trunk_prof(buf.ctypes.data_as(ctypes.c_void_p), nb))
 m = buf.mean(0)
-print("issuer: issue %.0f  wA3F %.0f  wW3F %.0f  wACE %.0f  wC1F %.0f  total %.0f" % (m[0], m[1], m[2], m[3], m[4], m[7]))
+print("issuer: other %.0f  wA3F %.0f  wW3F %.0f  wACE %.0f  wC1F %.0f  conv2-issue %.0f  fc-issue %.0f  total %.0f" % (m[0], m[1], m[2], m[3], m[4], m[5], m[6], m[7]))
 print("epi0: wACF %.0f wA3E %.0f total %.0f | epi1: wACF %.0f wA3E %.0f total %.0f" % (m[8], m[9], m[10], m[12], m[13], m[14]))
