@@ -173,12 +173,21 @@ __device__ long long g_tk_prof[1024][16];
 #else
 #define TKP(k, v)
 #endif
-constexpr int TK_CW = 7;                      // output columns per chunk
+#ifndef TK_CHUNK
+#define TK_CHUNK 7
+#endif
+constexpr int TK_CW = TK_CHUNK;               // output columns per chunk
 constexpr int TK_RC = TK_CW + 2;              // conv1 columns per ring row
 constexpr int TK_RING = 4;                    // conv1 rows in shared memory
-constexpr int TK_W3 = 8;                      // FC weight blocks in flight (released in pairs)
+#ifndef TK_W3_SLOTS
+#define TK_W3_SLOTS 8
+#endif
+#ifndef TK_A3_SLOTS
+#define TK_A3_SLOTS 2
+#endif
+constexpr int TK_W3 = TK_W3_SLOTS;            // FC weight blocks in flight (released in pairs)
 constexpr int TK_EPI = 2;                     // epilogue warp groups (output row R -> group R % 2)
-constexpr int TK_A3G = 2;                     // conv2 activation blocks (FC A operand) per group
+constexpr int TK_A3G = TK_A3_SLOTS;           // conv2 activation blocks (FC A operand) per group
 constexpr int TK_THREADS = 64 + 128 * TK_EPI + 32;  // + the FC issuer warp
 constexpr int TK_MAXNA = 16;
 constexpr uint32_t TK_BLK = 4096;             // one 128 x 16 bf16 block
@@ -186,7 +195,7 @@ constexpr uint32_t TK_BLK = 4096;             // one 128 x 16 bf16 block
 constexpr uint32_t TK_T_ACC = 0;
 constexpr uint32_t TK_T_D3 = TK_T_ACC + TK_EPI * TK_CW * 32;  // 448
 static_assert(TK_T_D3 + 64 <= 512, "TMEM budget");
-static_assert(TK_CW == 7, "conv2_row dispatch covers chunk widths 1..7");
+static_assert(TK_CW <= 7, "conv2_row dispatch covers chunk widths 1..7");
 constexpr uint32_t TK_OFF_RING = 0;
 constexpr uint32_t TK_OFF_W2 = TK_OFF_RING + TK_RING * TK_RC * TK_BLK;  // 147456: 3 x [96 x 16] bf16
 constexpr uint32_t TK_OFF_W3 = TK_OFF_W2 + 3 * 3072;
@@ -196,6 +205,7 @@ constexpr uint32_t TK_OFF_BIAS = TK_OFF_HEAD + (TK_MAXNA + 1) * 64 * 4;
 constexpr uint32_t TK_OFF_BAR = (TK_OFF_BIAS + (32 + 64 + TK_MAXNA + 1) * 4 + 7) & ~7u;  // 8-byte aligned
 constexpr int TK_NBAR = 2 * TK_RING + TK_W3 + TK_W3 / 2 + 2 * TK_EPI + 2 * TK_EPI * TK_A3G + 2;
 constexpr uint32_t TK_SMEM = TK_OFF_BAR + TK_NBAR * 8 + 16;
+static_assert(TK_SMEM <= 227 * 1024, "shared memory budget");
 
 // One output row's conv2 (CW pixels): conv1 block (row y+dy, column c) x the
 // three taps (dy, 2..0) -> pixels c-2..c, N = 96 (narrower at the edges).
