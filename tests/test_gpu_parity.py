@@ -645,3 +645,21 @@ def test_incremental_region_count_against_oracle(case):
     s1, s2 = env.state_dict(), ref.state_dict()
     for k in ("tiles", "values", "unreach", "prev_loss", "rng"):
         assert np.array_equal(s1[k], s2[k]), k
+
+
+def test_envs_on_two_devices_in_one_process():
+    """The dynamic shared-memory limit is raised per (kernel, device): envs on
+    cuda:0 and cuda:1 in one process both launch kernels needing > 48 KB
+    (dungeon narrow obs 31 in solo warp mode: 62 KB per 64-thread block)."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    cfg = EnvConfig(domain="dungeon")
+    n = 20000
+    outs = []
+    for d in ("cuda:0", "cuda:1"):
+        env = BatchEnv(cfg, n, seed=1, device=d)
+        env.reset()
+        a = np.random.default_rng(0).integers(0, cfg.n_actions, size=n)
+        outs.append(_np(env.step(a)[0]))
+        assert torch.cuda.current_device() == 0  # the caller's device is restored
+    assert np.array_equal(outs[0], outs[1])
