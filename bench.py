@@ -274,8 +274,12 @@ def main():
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # LG_BENCH_SAME_DEVICE=1: every rank on cuda:0 -- a functional test of the
+    # N > 1 code path on a one-GPU box (tests/test_gpu_bench_contract.py, gloo);
+    # never a measurement
+    dev_index = 0 if os.environ.get("LG_BENCH_SAME_DEVICE") == "1" else local_rank
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
     all_cpus = sorted(os.sched_getaffinity(0))
     cpus = rank_cpu_slice(local_rank, local_world, torch, dev)
@@ -297,8 +301,12 @@ def main():
         out_fd = os.dup(1)
         os.dup2(2, 1)
         sys.stdout = os.fdopen(out_fd, "w", buffering=1)
-        dist.init_process_group("nccl", device_id=dev)
-        print(f"[bench] rank {rank}/{world}: NCCL communicator of {dist.get_world_size()} ranks on cuda:{local_rank}",
+        backend = os.environ.get("LG_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+        print(f"[bench] rank {rank}/{world}: {backend} communicator of {dist.get_world_size()} ranks on {dev}",
               file=sys.stderr, flush=True)
     from paper_2408_12525_b200 import _lib
     from paper_2408_12525_b200.env import INFO_KEYS, BatchEnv, NumpyBatchEnv
@@ -354,7 +362,7 @@ def main():
     t0_step = args.warmup + burn
     if world > 1:
         dist.barrier()
-    clk = ClockSampler(local_rank)
+    clk = ClockSampler(dev_index)
     clk.start()
     time.sleep(0.3)
     K = args.steps
@@ -797,7 +805,7 @@ def main():
             "stats_all_reduce": reduce_info,
             "scaling_proxy": proxy,
             "host": {"cpus_used_by_rank0": len(cpus), "local_world": local_world,
-                     "comm": f"nccl x{world}" if distributed else "none"},
+                     "comm": f"{os.environ.get('LG_BENCH_BACKEND', 'nccl')} x{world}" if distributed else "none"},
         }
         print(json.dumps(line), flush=True)
 

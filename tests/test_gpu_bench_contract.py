@@ -45,3 +45,25 @@ def test_reference_line():
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["cpu_baseline"]["value"] == d["value"] and d["cpu_baseline"]["kind"] == "port"
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+
+
+def test_two_rank_code_path_functional():
+    """The N > 1 path of bench.py under torchrun (2 ranks): shards, barriers,
+    the side-stream stats all-reduce every S steps, max-over-ranks timing and
+    one JSON line from rank 0. A functional test on a one-GPU box: both ranks
+    on cuda:0 with the gloo backend (LG_BENCH_SAME_DEVICE / LG_BENCH_BACKEND),
+    never a measurement."""
+    env = dict(os.environ, LG_BENCH_SAME_DEVICE="1", LG_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(ROOT, "bench.py"), "--gpus", "2",
+           "--envs", "16384", "--steps", "10", "--warmup", "3", "--stats-every", "5", "--no-policy", "--no-u8",
+           "--cpu-envs", "256", "--cpu-seconds", "0.5"]
+    out = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT, timeout=900, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["global_envs"] == 16384 and d["config"]["envs_per_gpu"] == 8192
+    assert d["stats_all_reduce"]["count"] == 2 and d["host"]["comm"] == "gloo x2"
+    assert d["cpu_baseline"]["value"] > 0 and d["e2e"]["value"] > 0
+    assert "communicator of 2 ranks" in out.stderr
