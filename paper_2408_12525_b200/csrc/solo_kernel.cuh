@@ -1053,6 +1053,9 @@ __device__ __forceinline__ void solo_env(const Params &p, int mode, long long en
 #ifndef LG_DUNGEON_EARLY
 #define LG_DUNGEON_EARLY 0  // dungeon's warp kernel without the early-observation path (c3: spills)
 #endif
+#ifndef LG_STREAM_U
+#define LG_STREAM_U 2  // 256-bit stores in flight per lane in the warp-stream writer
+#endif
 #ifndef LG_DUNGEON_SPEC_EARLY
 #define LG_DUNGEON_SPEC_EARLY 1  // ... but the specialised one (c3) has the registers for it
 #endif
@@ -1113,10 +1116,10 @@ __device__ __forceinline__ void env_solo_body(const Params &p, int mode) {
             __syncwarp();
             const uint32_t nv = (uint32_t)nenv * p.PE / 8;
             const uint32_t qm = (uint32_t)((uint64_t)nv * LG_EARLY_SPLIT / 8) & ~127u;  // multiple of nthr * U
-            if (p.stream_mode) solo_write_stream<8, 2>(p, grp, env0, nenv, wl, nthr, 0, qm);
+            if (p.stream_mode) solo_write_stream<8, LG_STREAM_U>(p, grp, env0, nenv, wl, nthr, 0, qm);
             else solo_write_noctrl<LG_WRITER_U>(p, grp, env0, nenv, wl, nthr, 0, qm);
             if (valid) solo_finish<DOM, S>(p, mode, env, st, scratch);
-            if (p.stream_mode) solo_write_stream<8, 2>(p, grp, env0, nenv, wl, nthr, qm);
+            if (p.stream_mode) solo_write_stream<8, LG_STREAM_U>(p, grp, env0, nenv, wl, nthr, qm);
             else solo_write_noctrl<LG_WRITER_U>(p, grp, env0, nenv, wl, nthr, qm);
             return;
         }
@@ -1148,7 +1151,7 @@ __device__ __forceinline__ void env_solo_body(const Params &p, int mode) {
             // env0 is a multiple of 32, so the warp's byte range is 32-byte aligned
             solo_write_stream_u8(p, grp, env0, nenv, wl, nthr);
         } else if ((reinterpret_cast<uintptr_t>(p.obs + (size_t)env0 * p.PE) & 31) == 0) {
-            solo_write_stream<8, 2>(p, grp, env0, nenv, wl, nthr);
+            solo_write_stream<8, LG_STREAM_U>(p, grp, env0, nenv, wl, nthr);
         } else {
             solo_write_stream<4, 2>(p, grp, env0, nenv, wl, nthr);
         }
