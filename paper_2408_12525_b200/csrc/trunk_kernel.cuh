@@ -214,16 +214,8 @@ template <int CW>
 __device__ __forceinline__ void conv2_row(uint32_t acc, const uint64_t (&dr)[3], uint64_t d_w2) {
 #pragma unroll
     for (int dy = 0; dy < 3; dy++) {
-        // blocks in stride-3 order (0, 3, 6, 1, 4, 7, 2, 5, 8): consecutive MMAs
-        // write disjoint accumulator ranges (block c covers pixels c-2..c)
 #pragma unroll
-        for (int ci = 0; ci < CW + 2; ci++) {
-#ifndef TK_EXP_LINEAR_ORDER
-            constexpr int NB = CW + 2, G0 = (NB + 2) / 3, G1 = (NB + 1) / 3;
-            const int c = ci < G0 ? 3 * ci : ci < G0 + G1 ? 3 * (ci - G0) + 1 : 3 * (ci - G0 - G1) + 2;
-#else
-            const int c = ci;
-#endif
+        for (int c = 0; c < CW + 2; c++) {
             const int xlo = c - 2 > 0 ? c - 2 : 0, xhi = c < CW - 1 ? c : CW - 1;
             const int jb = xlo - c + 2, n = 32 * (xhi - xlo + 1);
             tc::mma_bf16(acc + 32u * xlo, dr[dy] + ((uint32_t)c * TK_BLK >> 4),
@@ -461,12 +453,8 @@ __global__ void __launch_bounds__(TK_THREADS, 1) trunk_kernel(const TrunkParams 
                         __nv_bfloat162 h2 = __floats2bfloat162_rn(x0, x1);
                         wd[jj] = *reinterpret_cast<uint32_t *>(&h2);
                     }
-#ifndef TK_EXP_NO_A3_STORE  // timing experiments only
                     *reinterpret_cast<uint4 *>(a3 + ((kc * 16 + (m >> 3)) * 128 + (m & 7) * 16)) =
                         make_uint4(wd[0], wd[1], wd[2], wd[3]);
-#else
-                    if (wd[0] == 0x12345678u) *reinterpret_cast<uint4 *>(a3) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
-#endif
                 }
                 tc::fence_proxy_async();
                 tc::mbar_arrive(BAR(A3F + a));
