@@ -56,6 +56,25 @@ def algorithmic_bytes_per_env_step(obs_shape) -> int:
     return 4 * c * h * w + 8 + 8 + 1
 
 
+def kernel_name(cfg, team: int) -> str:
+    """The step kernel this config launches: the specialised instantiations
+    (pcgrl_b200.cu spec_enabled / SoloKernel::spec) for the plain float32 path,
+    else the generic one."""
+    plain = (not cfg.controllable and not cfg.deterministic_metrics
+             and os.environ.get("LG_NO_SPEC", "0")[:1] != "1")
+    nopins = not cfg.pinpoints
+    if team == 1:
+        spec = plain and ((cfg.domain == "binary" and cfg.representation == "narrow" and nopins)
+                          or (cfg.domain == "dungeon" and cfg.representation == "wide"))
+        return f"env_solo_kernel_{cfg.domain}" + ("_s" if spec else "")
+    if plain and nopins and cfg.domain == "binary" and cfg.representation == "narrow" \
+            and max(cfg.max_width, cfg.max_height) > 32:
+        return "env_kernel<G64, binary, spec narrow/no-pins>"
+    if plain and nopins and team == 16 and cfg.domain == "maze" and cfg.representation == "turtle":
+        return "env_kernel<G16, maze, spec turtle/no-pins>"
+    return f"env_kernel<team {team}, {cfg.domain}>"
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -783,8 +802,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
                          "frac": achieved_gbs / peak, "traffic": load_traffic(args.config),
                          "peak_kind": peak_kind, "frac_of_8000_nominal": achieved_gbs / 8000.0,
-                         "kernel": (f"env_solo_kernel_{cfg.domain}" if team == 1 else
-                                    f"env_kernel<team {team}, {cfg.domain}>") + " (fused step + obs)",
+                         "kernel": kernel_name(cfg, team) + " (fused step + obs)",
                          "bytes_per_env_step": bytes_step, "step_kernel_ms": step_ms,
                          "step_kernel_ms_from": "CUDA-graph replay of K step kernels (events around it)"
                          if kernel_graph_ms is not None and step_ms == kernel_graph_ms else "eager per-step events",
