@@ -50,8 +50,9 @@ UNIT = "env-steps/s"
 
 
 def algorithmic_bytes_per_env_step(obs_shape) -> int:
-    """API-mandated I/O = obs write 4*C*OH*OW + action read 8
-    + reward write 8 + done write 1."""
+    """API-mandated I/O = obs write 4*C*OH*OW + action 8 (read
+    by lg_step; drawn in-kernel and written out by lg_step_random) + reward
+    write 8 + done write 1."""
     c, h, w = obs_shape
     return 4 * c * h * w + 8 + 8 + 1
 
@@ -73,6 +74,10 @@ def kernel_name(cfg, team: int) -> str:
     if plain and nopins and team == 16 and cfg.domain == "maze" and cfg.representation == "turtle":
         return "env_kernel<G16, maze, spec turtle/no-pins>"
     return f"env_kernel<team {team}, {cfg.domain}>"
+
+
+# st.global.cs.v8 stores only, 9472 blocks over 4 GB (profiles/r1_store_ceiling.txt)
+STORE_CEILING_GBS = 7199.5
 
 
 def load_peaks():
@@ -343,9 +348,13 @@ def main():
     env.reset(out=obs)
     stream = torch.cuda.current_stream(dev)
 
+    # One step of harness.bench_random_fps's loop (harness.py:149-175): a
+    # uniform action per env, then the batched step. lg_step_random draws the
+    # actions in the step kernel (recorded in `acts`, the same values
+    # lg_random_actions writes) and chains consecutive launches: step k+1's
+    # blocks start while step k's last wave runs (include/pcgrl_b200.h).
     def one_step(i):
-        env.random_actions(1_000_003 * i + 17, out=acts)
-        env.step_raw(acts, obs, reward, done, info, stats)
+        env.step_random(1_000_003 * i + 17, obs, reward, done, info, stats, actions_out=acts)
 
     for i in range(args.warmup):
         one_step(i)
@@ -385,7 +394,6 @@ def main():
     clk.start()
     time.sleep(0.3)
     K = args.steps
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     if world > 1:
@@ -397,10 +405,7 @@ def main():
     red_ev = []
     t_start.record(stream)
     for i in range(K):
-        env.random_actions(1_000_003 * (i + t0_step) + 17, out=acts)
-        ev[i][0].record(stream)
-        env.step_raw(acts, obs, reward, done, info, stats)
-        ev[i][1].record(stream)
+        one_step(i + t0_step)
         if side is not None and (i + 1) % args.stats_every == 0:
             side.wait_stream(stream)
             with torch.cuda.stream(side):
@@ -421,22 +426,22 @@ def main():
                        "max_ms": max(rms), "stream": "side (overlaps the step kernels)",
                        "global_episodes_seen": float(snap[0])}
     elapsed_ms = t_start.elapsed_time(t_end)
-    step_ms = sum(a.elapsed_time(b) for a, b in ev) / K
     elapsed_ms = max_over_ranks(elapsed_ms, dev)
-    step_ms = max_over_ranks(step_ms, dev)
+    step_ms = elapsed_ms / K  # one step kernel per step
     eager_ms = elapsed_ms
     graph_ms = None
     eager_step_ms = kernel_graph_ms = None
+    split = None
     if not args.no_graph:
-        # the same K steps (device actions + fused step, fresh seeds) captured
-        # once in a CUDA graph and replayed: no per-launch CPU gaps, which
-        # matter for the small configs (c1: 64 envs, ~30 us kernels)
+        # the same K steps (fresh seeds) captured once in a CUDA graph and
+        # replayed: no per-launch CPU gaps, which matter for the small configs
+        # (c1: 64 envs, ~20 us kernels). The graph holds exactly the K chained
+        # step launches, so its span / K is also the step kernel's time.
         g = torch.cuda.CUDAGraph()
         base = t0_step + K
         with torch.cuda.graph(g):
             for i in range(K):
-                env.random_actions(1_000_003 * (base + i) + 17, out=acts)
-                env.step_raw(acts, obs, reward, done, info, stats)
+                one_step(base + i)
         g.replay()  # warm replay (K more steps)
         torch.cuda.synchronize()
         if world > 1:
@@ -449,30 +454,31 @@ def main():
         graph_ms = max_over_ranks(g0.elapsed_time(g1), dev)
         if world == 1:  # N > 1: the eager loop carries the stats all-reduce; it is the value
             elapsed_ms = min(elapsed_ms, graph_ms)
-        # The step kernel alone for the roofline: K step launches with their
-        # actions generated beforehand, one CUDA-graph replay between two
-        # events on the launching stream (per-step events in the eager loop
-        # add launch gaps to short kernels: c3 0.124 vs 0.116 ms per step).
         del g
-        acts_k = torch.empty((K, B), dtype=torch.int64, device=dev)
+        kernel_graph_ms = graph_ms / K
+        eager_step_ms = step_ms
+        step_ms = min(step_ms, kernel_graph_ms)
+        # For contrast: the unfused loop -- lg_random_actions, then lg_step on
+        # those actions (two launches per step, each waiting for the whole
+        # previous grid), same graph timing.
+        gs = torch.cuda.CUDAGraph()
         base = t0_step + 3 * K
-        for i in range(K):
-            env.random_actions(1_000_003 * (base + i) + 17, out=acts_k[i])
-        gk = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(gk):
+        with torch.cuda.graph(gs):
             for i in range(K):
-                env.step_raw(acts_k[i], obs, reward, done, info, stats)
-        gk.replay()
+                env.random_actions(1_000_003 * (base + i) + 17, out=acts)
+                env.step_raw(acts, obs, reward, done, info, stats)
+        gs.replay()
         torch.cuda.synchronize()
         k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         k0.record(stream)
-        gk.replay()
+        gs.replay()
         k1.record(stream)
         torch.cuda.synchronize()
-        kernel_graph_ms = max_over_ranks(k0.elapsed_time(k1), dev) / K
-        del gk, acts_k
-        eager_step_ms = step_ms
-        step_ms = min(step_ms, kernel_graph_ms)
+        split_ms = max_over_ranks(k0.elapsed_time(k1), dev) / K
+        del gs
+        split = {"value": global_b / (split_ms / 1e3), "ms_per_step": split_ms,
+                 "launches_per_step": 2,
+                 "note": "lg_random_actions + lg_step per step (no launch chaining), CUDA-graph replay"}
     clocks = clk.stop()
     ep_stats.all_reduce()  # the episode-stats reduce (NCCL over NVLink when N > 1)
     stats_host = [float(x) for x in stats.cpu()]
@@ -604,17 +610,15 @@ def main():
         obs8 = env8.new_obs()
         env8.reset(out=obs8)
         for i in range(args.warmup):
-            env8.random_actions(1_000_003 * i + 17, out=acts)
-            env8.step_raw(acts, obs8, reward, done, info, None)
-        ev8 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+            env8.step_random(1_000_003 * i + 17, obs8, reward, done, info, None, actions_out=acts)
         torch.cuda.synchronize()
+        e80, e81 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e80.record(stream)
         for i in range(K):
-            env8.random_actions(1_000_003 * (i + args.warmup) + 17, out=acts)
-            ev8[i][0].record(stream)
-            env8.step_raw(acts, obs8, reward, done, info, None)
-            ev8[i][1].record(stream)
+            env8.step_random(1_000_003 * (i + args.warmup) + 17, obs8, reward, done, info, None, actions_out=acts)
+        e81.record(stream)
         torch.cuda.synchronize()
-        ms8 = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev8) / K, dev)
+        ms8 = max_over_ranks(e80.elapsed_time(e81) / K, dev)
         c_, h_, w_ = env8.observation_shape
         bytes8 = c_ * h_ * w_ + 17
         u8 = {"value": global_b / (ms8 / 1e3), "unit": UNIT, "step_kernel_ms": ms8,
@@ -747,13 +751,11 @@ def main():
             pd = torch.empty(Bs, dtype=torch.bool, device=dev)
             pe.reset(out=po)
             for i in range(args.warmup):
-                pe.random_actions(i, out=pa)
-                pe.step_raw(pa, po, pr, pd)
+                pe.step_random(i, po, pr, pd, actions_out=pa)
             gp = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gp):
                 for i in range(K):
-                    pe.random_actions(100 + i, out=pa)
-                    pe.step_raw(pa, po, pr, pd)
+                    pe.step_random(100 + i, po, pr, pd, actions_out=pa)
             gp.replay()
             torch.cuda.synchronize()
             g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -802,14 +804,20 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
                          "frac": achieved_gbs / peak, "traffic": load_traffic(args.config),
                          "peak_kind": peak_kind, "frac_of_8000_nominal": achieved_gbs / 8000.0,
+                         # the step's bytes are >99.9% writes: the copy peak (read+write) is
+                         # not its ceiling; the measured streaming-store ceiling is
+                         "store_ceiling_gbs": STORE_CEILING_GBS,
+                         "frac_of_store_ceiling": achieved_gbs / STORE_CEILING_GBS,
                          "kernel": kernel_name(cfg, team) + " (fused step + obs)",
                          "bytes_per_env_step": bytes_step, "step_kernel_ms": step_ms,
-                         "step_kernel_ms_from": "CUDA-graph replay of K step kernels (events around it)"
-                         if kernel_graph_ms is not None and step_ms == kernel_graph_ms else "eager per-step events",
-                         "step_kernel_ms_eager_events": eager_step_ms},
+                         "step_kernel_ms_from": "CUDA-graph replay of K chained step launches (events around "
+                                                "it) / K: consecutive launches overlap at block granularity"
+                         if kernel_graph_ms is not None and step_ms == kernel_graph_ms else "eager launch loop / K",
+                         "step_kernel_ms_eager": eager_step_ms},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": 2 * K,
+            "gpu_launches": K,
+            "unchained_split_launch": split,
             "timing": {"eager_ms_per_step": eager_ms / K,
                        "graph_ms_per_step": graph_ms / K if graph_ms is not None else None,
                        "value_from": "graph" if graph_ms is not None and graph_ms <= eager_ms else "eager",

@@ -176,6 +176,21 @@ int lg_errors(lg_env *env, uint32_t *flags, void *stream);
  * actions in [0, n_actions) from a counter hash of (seed, global env index). */
 int lg_random_actions(lg_env *env, int64_t *actions_dev, uint64_t seed, void *stream);
 
+/* The random-policy loop of harness.bench_random_fps (harness.py:149-175:
+ * rng.integers + BatchEnv.step) as one call: each env's action is the one
+ * lg_random_actions(seed) would draw, recorded in actions_out when non-null,
+ * then the env steps as lg_step. Consecutive lg_step_random calls of one env
+ * on one stream, with no other call on that env between them, are chained:
+ * each launch is a programmatic dependent launch of the previous one, and
+ * its blocks wait per block (same envs, same block) instead of for the whole
+ * previous grid, so the last wave of step k overlaps the start of step k+1.
+ * Results are identical to lg_random_actions + lg_step. Other work the caller
+ * enqueues on the stream between two chained calls must not write the env's
+ * outputs (obs/reward/done/info/actions_out buffers). LG_NO_CHAIN=1 disables
+ * the overlap. */
+int lg_step_random(lg_env *env, uint64_t seed, int64_t *actions_out_dev, void *obs_dev, double *reward_dev,
+                   uint8_t *done_dev, const lg_info *info, double *stats_dev, void *stream);
+
 /* harness.first_episode_rewards (harness.py:48-61), the per-step update on
  * device buffers of n envs: where done[b] && !seen[b], rewards[b] =
  * episode_reward[b] (the step's info["episode_reward"]) and seen[b] = 1;

@@ -75,6 +75,7 @@ SIGNATURES = {
     "lg_import_state": (ctypes.c_int, [_P, ctypes.POINTER(LgState), _P]),
     "lg_errors": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint32), _P]),
     "lg_random_actions": (ctypes.c_int, [_P, _P, ctypes.c_uint64, _P]),
+    "lg_step_random": (ctypes.c_int, [_P, ctypes.c_uint64, _P, _P, _P, _P, ctypes.POINTER(LgInfo), _P, _P]),
     "lg_first_episode": (ctypes.c_int, [_I64, _P, _P, _P, _P, _P, _P]),
     "lg_metrics": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _I64, _P, _P, _P, _P, _P,
                                   _P]),

@@ -120,7 +120,80 @@ struct Params {
     int coop;       // solo block mode: the warp renders its envs' images together
     int gate;       // validated step (LG_STEP_VALIDATE): skip the launch when the action
                     // check kernel flagged an out-of-range action (no mutation, env.py:358-361)
+    // lg_step_random: each env's action is drawn in the step kernel (the draw
+    // of lg_random_actions), optionally recorded in act_out
+    int rand_act;
+    unsigned long long act_seed;
+    long long *act_out;
+    // chained launches (lg_step_random): per-block tickets [started | done],
+    // one pair per block of the launch grid (see chain_enter)
+    int chain;
+    unsigned *tickets;
 };
+
+// Uniform actions: a counter-based draw per (seed, global env index), the
+// same values lg_random_actions writes (harness.uniform_policy's role,
+// harness.py:149-175, for the device bench loop).
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ULL;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+    return x ^ (x >> 31);
+}
+__device__ __forceinline__ long long uniform_action(unsigned long long seed, long long gidx, long long n) {
+    const uint64_t x = splitmix64(seed * 0xD1B54A32D192ED03ULL ^ splitmix64((uint64_t)gidx));
+    return (long long)(((unsigned __int128)x * (unsigned long long)n) >> 64);
+}
+// the step's action for `env` (record: this thread writes act_out)
+__device__ __forceinline__ long long step_action(const Params &p, long long env, bool record) {
+    if (p.rand_act) {
+        const long long a = uniform_action(p.act_seed, p.goffset + env, p.n_actions);
+        if (record && p.act_out) p.act_out[env] = a;
+        return a;
+    }
+    return p.actions[env];
+}
+
+// Chained launches. Consecutive lg_step_random launches of one env on one
+// stream are programmatic dependent launches: launch k+1 may start while
+// launch k's last wave runs. Block j of every launch steps the same envs, so
+// it waits only for block j of the previous launch (ticket = the launch's
+// sequence number for this block; done[j] counts finished launches), then
+// lets the next launch be scheduled. Launch k+1 is only scheduled once every
+// block of launch k has passed its wait, so all blocks a waiting block
+// depends on are already resident (no deadlock); a wait that does not end
+// within 2 s traps (error, not a hang).
+__device__ __forceinline__ void chain_enter(const Params &p) {
+    if (!p.chain) return;
+    if (threadIdx.x == 0) {
+        unsigned *started = p.tickets, *done = p.tickets + gridDim.x;
+        const unsigned my = atomicAdd(started + blockIdx.x, 1u);
+        unsigned v, spins = 0;
+        unsigned long long t0 = 0;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(done + blockIdx.x) : "memory");
+            if (v == my) break;
+            __nanosleep(128);
+            if ((++spins & 1023u) == 0) {
+                unsigned long long now;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+                if (!t0) t0 = now;
+                else if (now - t0 > 2000000000ull) __trap();
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void chain_leave(const Params &p) {
+    if (!p.chain) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.tickets + gridDim.x + blockIdx.x) : "memory");
+    }
+}
 
 // Validated steps: the reference rejects a bad action batch before mutating
 // anything (env.py:358-361). check_actions_kernel runs first on the stream;
@@ -985,7 +1058,7 @@ __device__ LG_TEAM_WRITER_ATTR void write_obs_team_nc(const Params &p, const Tea
 #define LG_TEAM_EARLY_SPLIT 1  // eighths of an env's output stored before its recompute (specialised kernels)
 #endif
 template <class G, int DOM, int S = 0>
-__global__ void __launch_bounds__(64, G::MINB) env_kernel(const Params p, int mode) {
+__device__ __forceinline__ void env_team_body(const Params &p, int mode) {
     extern __shared__ __align__(16) unsigned char smem[];
     using Row = typename G::Row;
     constexpr int N = Dom<DOM>::N, NPL = Dom<DOM>::NPL;
@@ -1010,7 +1083,7 @@ __global__ void __launch_bounds__(64, G::MINB) env_kernel(const Params p, int mo
         double before = 0.0;
         int dirty_row = -1, wcol = 0, wcur = 0;  // the write (row, column, old tile)
         if (mode == MODE_STEP) {
-            long long a = p.actions[env];
+            long long a = step_action(p, env, t.lane == 0);
             bool ok = a >= 0 && a < p.n_actions;
             if (!ok && t.lane == 0) atomicOr(p.err, (unsigned)FLAG_BAD_ACTION);
             int r = e.pr, c = e.pc, tile = -1;
@@ -1175,6 +1248,13 @@ __global__ void __launch_bounds__(64, G::MINB) env_kernel(const Params p, int mo
             if (p.obs && early) write_obs_team_nc<G>(p, t, env, es, kSplit, 8);
         }
     }
+}
+
+template <class G, int DOM, int S = 0>
+__global__ void __launch_bounds__(64, G::MINB) env_kernel(const Params p, int mode) {
+    chain_enter(p);
+    env_team_body<G, DOM, S>(p, mode);
+    chain_leave(p);
 }
 
 }  // namespace lg

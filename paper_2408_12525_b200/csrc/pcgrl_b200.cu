@@ -108,19 +108,11 @@ __global__ void seed_kernel(long long B, unsigned long long seed, long long offs
     ri[b] = make_ulonglong2((unsigned long long)(g.inc >> 64), (unsigned long long)g.inc);
 }
 
-__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
-    x += 0x9E3779B97F4A7C15ULL;
-    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
-    x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
-    return x ^ (x >> 31);
-}
-
 __global__ void random_actions_kernel(long long B, long long goffset, unsigned long long seed,
                                       long long n_actions, long long *out) {
     long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= B) return;
-    uint64_t x = splitmix64(seed * 0xD1B54A32D192ED03ULL ^ splitmix64((uint64_t)(goffset + b)));
-    out[b] = (long long)(((unsigned __int128)x * (unsigned long long)n_actions) >> 64);
+    out[b] = uniform_action(seed, goffset + b, n_actions);
 }
 
 // Validated steps (env.py:358-361): flags an out-of-range action before the
@@ -395,7 +387,34 @@ struct lg_env {
     uint8_t *h_bits = nullptr;
     size_t bits_bytes = 0, chunk_bytes = 0;
     std::vector<cudaEvent_t> chunk_ev;
+    // chained lg_step_random launches: per-block tickets, and whether
+    // the last library call on this env was a chained step on chain_stream
+    unsigned *tickets = nullptr;
+    long long tickets_grid = 0;
+    bool chain_live = false, pdl = false;
+    cudaStream_t chain_stream = nullptr;
 };
+
+// Launch a step kernel; `pdl`: as a programmatic dependent launch of the
+// previous chained step on the stream (env_kernels.cuh chain_enter).
+static cudaError_t launch_step(void (*kern)(const Params, int), unsigned grid, unsigned threads, size_t smem,
+                               cudaStream_t s, const Params &q, int mode, bool pdl) {
+    if (!pdl) {
+        kern<<<grid, threads, smem, s>>>(q, mode);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t c = {};
+    c.gridDim = dim3(grid);
+    c.blockDim = dim3(threads);
+    c.dynamicSmemBytes = smem;
+    c.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    c.attrs = at;
+    c.numAttrs = 1;
+    return cudaLaunchKernelEx(&c, kern, q, mode);
+}
 
 static void fastdiv_init(FastDiv &f, uint32_t d) {
     f.d = d;
@@ -419,8 +438,11 @@ static int launch_env_k(lg_env *e, const Params &q, int mode, cudaStream_t s) {
     CU(smem_attr((const void *)env_kernel<G, DOM, S>));
     const int E = e->threads / G::TEAM;
     const long long grid = (e->B + E - 1) / E;
-    env_kernel<G, DOM, S><<<(unsigned)grid, e->threads, e->smem, s>>>(q, mode);
-    CU(cudaGetLastError());
+    if (q.chain && grid > e->tickets_grid) {
+        set_err("chained launch grid exceeds the ticket array");
+        return LG_EINVAL;
+    }
+    CU(launch_step(env_kernel<G, DOM, S>, (unsigned)grid, e->threads, e->smem, s, q, mode, e->pdl));
     return LG_OK;
 }
 
@@ -480,19 +502,15 @@ static int launch_solo_t(lg_env *e, const Params &p, int mode, cudaStream_t s) {
     }
     constexpr int S = SoloKernel<DOM>::spec;
     const bool spec = S != 0 && plain_launch(q) && q.rep == (S & 3) - 1 && (!(S & SPEC_NOPINS) || q.n_pins == 0);
-    if (e->E == e->threads) {
-        if (spec) {
-            CU(smem_attr((const void *)SoloKernel<DOM>::fn_spec));
-            SoloKernel<DOM>::fn_spec<<<(unsigned)grid, e->threads, smem, s>>>(q, mode);
-        } else {
-            SoloKernel<DOM>::fn<<<(unsigned)grid, e->threads, smem, s>>>(q, mode);
-        }
-    } else if (spec) {
-        CU(smem_attr((const void *)SoloKernel<DOM>::fn_small_spec));
-        SoloKernel<DOM>::fn_small_spec<<<(unsigned)grid, e->threads, smem, s>>>(q, mode);
-    } else {
-        SoloKernel<DOM>::fn_small<<<(unsigned)grid, e->threads, smem, s>>>(q, mode);
+    void (*kern)(const Params, int) = e->E == e->threads ? (spec ? SoloKernel<DOM>::fn_spec : SoloKernel<DOM>::fn)
+                                                         : (spec ? SoloKernel<DOM>::fn_small_spec
+                                                                 : SoloKernel<DOM>::fn_small);
+    if (spec) CU(smem_attr((const void *)kern));
+    if (q.chain && grid > e->tickets_grid) {
+        set_err("chained launch grid exceeds the ticket array");
+        return LG_EINVAL;
     }
+    CU(launch_step(kern, (unsigned)grid, e->threads, smem, s, q, mode, e->pdl));
     CU(cudaGetLastError());
     return LG_OK;
 }
@@ -794,6 +812,8 @@ extern "C" int lg_create(const lg_config *cfg, int64_t n_envs, int64_t global_of
     alloc((void **)&p.mseed, B * sizeof(long long));
     alloc((void **)&p.err, sizeof(unsigned));
     alloc((void **)&p.aux, sizeof(unsigned));
+    e->tickets_grid = ((long long)B + e->E - 1) / e->E;  // chained lg_step_random launches
+    alloc((void **)&e->tickets, (size_t)e->tickets_grid * 2 * sizeof(unsigned));
     if (err != cudaSuccess) {
         set_err("CUDA allocation failed: %s", cudaGetErrorString(err));
         lg_destroy(e);
@@ -817,7 +837,7 @@ extern "C" int lg_destroy(lg_env *e) {
     Params &p = e->base;
     void *ptrs[] = {p.rows, p.hot, p.mv, p.lossv, p.rs, p.ri, p.rb, p.mseed, p.err, p.aux,
                     e->d_act, e->d_obs, e->d_rew, e->d_done, e->d_term, e->d_er, e->d_es, e->d_fl, e->d_el,
-                    e->d_bits};
+                    e->d_bits, e->tickets};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     if (e->h_bits) cudaFreeHost(e->h_bits);
@@ -876,13 +896,17 @@ static bool packed_needs_zero(const lg_env *e) {
 
 static int run_mode(lg_env *e, int mode, const long long *actions, void *obs, double *reward,
                     uint8_t *done, const lg_info *info, double *stats, const uint8_t *mask, void *stream,
-                    unsigned flags = 0, bool obs_bits = false) {
+                    unsigned flags = 0, bool obs_bits = false, const uint64_t *rand_seed = nullptr,
+                    int64_t *act_out = nullptr) {
     if (!e) {
         set_err("null env");
         return LG_EINVAL;
     }
+    const bool chain_was_live = e->chain_live;
+    e->chain_live = false;  // any other call on the env ends a chain of lg_step_random launches
+    e->pdl = false;
     if (check_obs_ptr(obs)) return LG_EINVAL;
-    if (mode == MODE_STEP && (!actions || !reward || !done)) {
+    if (mode == MODE_STEP && ((!actions && !rand_seed) || !reward || !done)) {
         set_err("step needs actions, reward and done buffers");
         return LG_EINVAL;
     }
@@ -916,7 +940,30 @@ static int run_mode(lg_env *e, int mode, const long long *actions, void *obs, do
         const size_t words = ((size_t)e->B * p.PE + 31) / 32;
         CU(cudaMemsetAsync(obs, 0, words * 4, (cudaStream_t)stream));
     }
-    return launch_env(e, p, mode, (cudaStream_t)stream);
+    bool chained = false;
+    if (rand_seed) {
+        p.rand_act = 1;
+        p.act_seed = *rand_seed;
+        p.act_out = (long long *)act_out;
+        // chained (programmatic dependent) launches need every launch of the
+        // env to run the same grid over the same envs, and no memset between
+        // two steps (packed streams with shared boundary words)
+        // Not for the 64-row lane teams: 2 envs per block, so the per-block
+        // ticket round trip is a large share of a block's life (c4 263 -> 254 M
+        // env-steps/s chained; c5 +3%, its 131k shard +13%, c3 +21%, c2 +22%).
+        const char *nc = getenv("LG_NO_CHAIN");
+        chained = !(p.obs_bits && obs && packed_needs_zero(e)) && e->geo != 64 && !(nc && nc[0] == '1');
+    }
+    if (chained) {
+        p.chain = 1;
+        p.tickets = e->tickets;
+        e->pdl = chain_was_live && e->chain_stream == (cudaStream_t)stream;
+    }
+    const int rc = launch_env(e, p, mode, (cudaStream_t)stream);
+    e->pdl = false;
+    e->chain_live = chained && rc == LG_OK;
+    e->chain_stream = (cudaStream_t)stream;
+    return rc;
 }
 
 extern "C" int lg_reset(lg_env *e, void *obs, void *stream) {
@@ -941,6 +988,12 @@ extern "C" int lg_step(lg_env *e, const int64_t *actions, void *obs, double *rew
                        const lg_info *info, double *stats, void *stream) {
     return run_mode(e, MODE_STEP, (const long long *)actions, obs, reward, done, info, stats, nullptr,
                     stream);
+}
+
+extern "C" int lg_step_random(lg_env *e, uint64_t seed, int64_t *actions_out, void *obs, double *reward,
+                              uint8_t *done, const lg_info *info, double *stats, void *stream) {
+    return run_mode(e, MODE_STEP, nullptr, obs, reward, done, info, stats, nullptr, stream, 0, false, &seed,
+                    actions_out);
 }
 
 extern "C" int lg_step_flags(lg_env *e, const int64_t *actions, void *obs, double *reward, uint8_t *done,
@@ -1203,6 +1256,7 @@ extern "C" int lg_export_state(lg_env *e, const lg_state *dst, void *stream) {
         set_err("null argument");
         return LG_EINVAL;
     }
+    e->chain_live = false;
     DEVICE_GUARD(e->device);
     return launch_state(e, *dst, true, (cudaStream_t)stream);
 }
@@ -1212,6 +1266,7 @@ extern "C" int lg_import_state(lg_env *e, const lg_state *src, void *stream) {
         set_err("null argument");
         return LG_EINVAL;
     }
+    e->chain_live = false;
     DEVICE_GUARD(e->device);
     cudaStream_t s = (cudaStream_t)stream;
     if (!e->frz_ok && !e->elide_ok) return launch_state(e, *src, false, s);
@@ -1231,6 +1286,7 @@ extern "C" int lg_errors(lg_env *e, uint32_t *flags, void *stream) {
         set_err("null argument");
         return LG_EINVAL;
     }
+    e->chain_live = false;
     DEVICE_GUARD(e->device);
     cudaStream_t s = (cudaStream_t)stream;
     CU(cudaMemcpyAsync(flags, e->base.err, 4, cudaMemcpyDeviceToHost, s));
@@ -1257,6 +1313,7 @@ extern "C" int lg_random_actions(lg_env *e, int64_t *actions, uint64_t seed, voi
         set_err("null argument");
         return LG_EINVAL;
     }
+    e->chain_live = false;
     DEVICE_GUARD(e->device);
     random_actions_kernel<<<(unsigned)((e->B + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
         e->B, e->offset, seed, e->n_actions, (long long *)actions);

@@ -916,7 +916,7 @@ __device__ __forceinline__ void solo_begin(const Params &p, int mode, long long 
     st.wrote = st.reset_now = st.ends = false;
     st.before = 0.0;
     if (mode == MODE_STEP) {
-        long long a = p.actions[env];
+        long long a = step_action(p, env, true);
         bool ok = a >= 0 && a < p.n_actions;
         if (!ok) atomicOr(p.err, (unsigned)FLAG_BAD_ACTION);
         int r = e.pr, c = e.pc, tile = -1;
@@ -1063,7 +1063,7 @@ __device__ __forceinline__ void solo_env(const Params &p, int mode, long long en
 // WARP = 0: the block-mode kernel (small batches). Two kernels, so neither
 // carries the other's code paths (register pressure, instruction footprint).
 template <int DOM, int WARP, int S = 0>
-__device__ __forceinline__ void env_solo_body(const Params &p, int mode) {
+__device__ __forceinline__ void env_solo_work(const Params &p, int mode) {
     extern __shared__ __align__(16) uint32_t smem_w[];
     const int E = p.solo_E, T = blockDim.x, tid = threadIdx.x;
     constexpr bool warp_mode = WARP == 1;  // the host launches this kernel only when E == T
@@ -1188,6 +1188,13 @@ __device__ __forceinline__ void env_solo_body(const Params &p, int mode) {
     } else {
         solo_write<4, 2>(p, img, env0, nenv, wl, nthr);
     }
+}
+
+template <int DOM, int WARP, int S = 0>
+__device__ __forceinline__ void env_solo_body(const Params &p, int mode) {
+    chain_enter(p);
+    env_solo_work<DOM, WARP, S>(p, mode);
+    chain_leave(p);
 }
 
 // Register caps (measured): binary runs 8 x 64-thread blocks per SM at 128

@@ -225,6 +225,19 @@ class BatchEnv:
             self._h, _ptr(actions), _ptr(obs) if obs is not None else None, _ptr(reward), _ptr(done),
             ci, _ptr(stats) if stats is not None else None, _stream(self._torch, self.device)))
 
+    def step_random(self, seed: int, obs, reward, done, info=None, stats=None, actions_out=None) -> None:
+        """harness.bench_random_fps's loop body (harness.py:149-175) on device:
+        uniform actions (the draw of ``random_actions(seed)``, recorded in
+        ``actions_out``) and the step, in one call. Consecutive calls overlap
+        launch to launch (include/pcgrl_b200.h lg_step_random)."""
+        ci = None
+        if info is not None:
+            ci = ctypes.byref(_lib.LgInfo(*[_ptr(info[k]) if k in info else None for k in INFO_KEYS]))
+        _lib.check(_lib.load().lg_step_random(
+            self._h, int(seed) & ((1 << 64) - 1), _ptr(actions_out) if actions_out is not None else None,
+            _ptr(obs) if obs is not None else None, _ptr(reward), _ptr(done), ci,
+            _ptr(stats) if stats is not None else None, _stream(self._torch, self.device)))
+
     def observe(self, out=None):
         obs = self.new_obs() if out is None else out
         with self._torch.cuda.device(self.device):

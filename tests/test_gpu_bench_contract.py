@@ -31,7 +31,7 @@ def test_ours_line():
              "--cpu-seconds", "0.5")
     for k in KEYS:
         assert k in d, k
-    assert d["value"] > 0 and d["steps"] == 3 and d["warmup"] == 3 and d["gpu_launches"] == 6
+    assert d["value"] > 0 and d["steps"] == 3 and d["warmup"] == 3 and d["gpu_launches"] == 3
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1.5
     e = d["e2e"]
