@@ -187,7 +187,8 @@ int lg_random_actions(lg_env *env, int64_t *actions_dev, uint64_t seed, void *st
  * Results are identical to lg_random_actions + lg_step. Other work the caller
  * enqueues on the stream between two chained calls must not write the env's
  * outputs (obs/reward/done/info/actions_out buffers). LG_NO_CHAIN=1 disables
- * the overlap. */
+ * the overlap. Maps wider or taller than 32 (64-row lane teams) draw the
+ * actions with their own kernel and are not chained. */
 int lg_step_random(lg_env *env, uint64_t seed, int64_t *actions_out_dev, void *obs_dev, double *reward_dev,
                    uint8_t *done_dev, const lg_info *info, double *stats_dev, void *stream);
 

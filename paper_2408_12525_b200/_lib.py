@@ -101,6 +101,8 @@ def load(path: str = LIB_PATH):
             "`python -m paper_2408_12525_b200.build` (there is no CPU fallback)")
     lib = ctypes.CDLL(path)
     for name, (res, args) in SIGNATURES.items():
+        if os.environ.get("LG_LIB_PATH") and not hasattr(lib, name):
+            continue  # an older variant build (LG_LIB_PATH A/B runs): entry points it predates
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

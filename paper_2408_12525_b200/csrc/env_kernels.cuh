@@ -144,9 +144,12 @@ __device__ __forceinline__ long long uniform_action(unsigned long long seed, lon
     const uint64_t x = splitmix64(seed * 0xD1B54A32D192ED03ULL ^ splitmix64((uint64_t)gidx));
     return (long long)(((unsigned __int128)x * (unsigned long long)n) >> 64);
 }
-// the step's action for `env` (record: this thread writes act_out)
+// the step's action for `env` (record: this thread writes act_out). kRand =
+// false compiles the in-kernel draw out (the 64-row lane teams: the host
+// draws their actions with random_actions_kernel; see run_mode).
+template <bool kRand = true>
 __device__ __forceinline__ long long step_action(const Params &p, long long env, bool record) {
-    if (p.rand_act) {
+    if (kRand && p.rand_act) {
         const long long a = uniform_action(p.act_seed, p.goffset + env, p.n_actions);
         if (record && p.act_out) p.act_out[env] = a;
         return a;
@@ -1057,6 +1060,12 @@ __device__ LG_TEAM_WRITER_ATTR void write_obs_team_nc(const Params &p, const Tea
 #ifndef LG_TEAM_EARLY_SPLIT
 #define LG_TEAM_EARLY_SPLIT 1  // eighths of an env's output stored before its recompute (specialised kernels)
 #endif
+// Chained launches and in-kernel random actions are compiled into the lane
+// teams of one row per lane only: the 64-row kernel (c4) is bound by
+// instruction fetch, and the extra code measured 277 -> 264 M env-steps/s.
+template <class G>
+constexpr bool kTeamChain = G::RPL == 1;
+
 template <class G, int DOM, int S = 0>
 __device__ __forceinline__ void env_team_body(const Params &p, int mode) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -1083,7 +1092,7 @@ __device__ __forceinline__ void env_team_body(const Params &p, int mode) {
         double before = 0.0;
         int dirty_row = -1, wcol = 0, wcur = 0;  // the write (row, column, old tile)
         if (mode == MODE_STEP) {
-            long long a = step_action(p, env, t.lane == 0);
+            long long a = step_action<kTeamChain<G>>(p, env, t.lane == 0);
             bool ok = a >= 0 && a < p.n_actions;
             if (!ok && t.lane == 0) atomicOr(p.err, (unsigned)FLAG_BAD_ACTION);
             int r = e.pr, c = e.pc, tile = -1;
@@ -1252,9 +1261,9 @@ __device__ __forceinline__ void env_team_body(const Params &p, int mode) {
 
 template <class G, int DOM, int S = 0>
 __global__ void __launch_bounds__(64, G::MINB) env_kernel(const Params p, int mode) {
-    chain_enter(p);
+    if constexpr (kTeamChain<G>) chain_enter(p);
     env_team_body<G, DOM, S>(p, mode);
-    chain_leave(p);
+    if constexpr (kTeamChain<G>) chain_leave(p);
 }
 
 }  // namespace lg

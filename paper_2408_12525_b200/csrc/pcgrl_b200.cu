@@ -391,6 +391,7 @@ struct lg_env {
     // the last library call on this env was a chained step on chain_stream
     unsigned *tickets = nullptr;
     long long tickets_grid = 0;
+    long long *act_scratch = nullptr;  // geo 64: lg_step_random's actions when not recorded
     bool chain_live = false, pdl = false;
     cudaStream_t chain_stream = nullptr;
 };
@@ -814,6 +815,7 @@ extern "C" int lg_create(const lg_config *cfg, int64_t n_envs, int64_t global_of
     alloc((void **)&p.aux, sizeof(unsigned));
     e->tickets_grid = ((long long)B + e->E - 1) / e->E;  // chained lg_step_random launches
     alloc((void **)&e->tickets, (size_t)e->tickets_grid * 2 * sizeof(unsigned));
+    if (e->geo == 64) alloc((void **)&e->act_scratch, B * sizeof(long long));
     if (err != cudaSuccess) {
         set_err("CUDA allocation failed: %s", cudaGetErrorString(err));
         lg_destroy(e);
@@ -837,7 +839,7 @@ extern "C" int lg_destroy(lg_env *e) {
     Params &p = e->base;
     void *ptrs[] = {p.rows, p.hot, p.mv, p.lossv, p.rs, p.ri, p.rb, p.mseed, p.err, p.aux,
                     e->d_act, e->d_obs, e->d_rew, e->d_done, e->d_term, e->d_er, e->d_es, e->d_fl, e->d_el,
-                    e->d_bits, e->tickets};
+                    e->d_bits, e->tickets, e->act_scratch};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     if (e->h_bits) cudaFreeHost(e->h_bits);
@@ -941,6 +943,16 @@ static int run_mode(lg_env *e, int mode, const long long *actions, void *obs, do
         CU(cudaMemsetAsync(obs, 0, words * 4, (cudaStream_t)stream));
     }
     bool chained = false;
+    if (rand_seed && e->geo == 64) {
+        // 64-row lane teams (kTeamChain): the actions are drawn by their own
+        // kernel and the step reads them, no chaining
+        long long *a = act_out ? (long long *)act_out : e->act_scratch;
+        random_actions_kernel<<<(unsigned)((e->B + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+            e->B, e->offset, *rand_seed, e->n_actions, a);
+        CU(cudaGetLastError());
+        p.actions = a;
+        rand_seed = nullptr;
+    }
     if (rand_seed) {
         p.rand_act = 1;
         p.act_seed = *rand_seed;
@@ -948,11 +960,11 @@ static int run_mode(lg_env *e, int mode, const long long *actions, void *obs, do
         // chained (programmatic dependent) launches need every launch of the
         // env to run the same grid over the same envs, and no memset between
         // two steps (packed streams with shared boundary words)
-        // Not for the 64-row lane teams: 2 envs per block, so the per-block
-        // ticket round trip is a large share of a block's life (c4 263 -> 254 M
-        // env-steps/s chained; c5 +3%, its 131k shard +13%, c3 +21%, c2 +22%).
+        // (measured: c5 +3%, its 131k-env shard +13%, c3 +21%, c2 +22%; the
+        // 64-row lane teams, one env per 32-thread block, lost 4% and are
+        // not chained -- above)
         const char *nc = getenv("LG_NO_CHAIN");
-        chained = !(p.obs_bits && obs && packed_needs_zero(e)) && e->geo != 64 && !(nc && nc[0] == '1');
+        chained = !(p.obs_bits && obs && packed_needs_zero(e)) && !(nc && nc[0] == '1');
     }
     if (chained) {
         p.chain = 1;

@@ -61,6 +61,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--configs", default="c5:1048576,c5:524288,c5:262144,c5:131072,c3,c2,c4,c1")
+    ap.add_argument("--variants", default="split,random_unchained,chained")
     a = ap.parse_args()
     for item in a.configs.split(","):
         name, _, n = item.partition(":")
@@ -68,7 +69,7 @@ def main():
         B = int(n) if n else default_b
         cfg = EnvConfig(**kw)
         row = {"config": name, "envs": B}
-        for v in ("split", "random_unchained", "chained"):
+        for v in a.variants.split(","):
             ms = run(cfg, B, a.steps, v)
             row[v] = {"ms_per_step": round(ms, 5), "Menv_steps_per_s": round(B / ms / 1e3, 2)}
             torch.cuda.empty_cache()
