@@ -184,18 +184,18 @@ __device__ __forceinline__ void chain_enter(const Params &p) {
                 else if (now - t0 > 2000000000ull) __trap();
             }
         }
-        __threadfence();
     }
     __syncthreads();
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 __device__ __forceinline__ void chain_leave(const Params &p) {
     if (!p.chain) return;
+    // the barrier orders every thread's stores before thread 0's release (the
+    // semaphore pattern: bar.sync, then one st/red.release.gpu; the reader's
+    // ld.acquire.gpu, then bar.sync)
     __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
+    if (threadIdx.x == 0)
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.tickets + gridDim.x + blockIdx.x) : "memory");
-    }
 }
 
 // Validated steps: the reference rejects a bad action batch before mutating
