@@ -541,9 +541,11 @@ def main():
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
+        res = None
         for a in host_acts:
-            nenv.step(a)
+            res = nenv.step(a)  # a caller holds a step's arrays until the next step returns
         dt = max_over_ranks(time.perf_counter() - t0, dev)
+        del res
         del nenv
         os.environ.pop("LG_HOST_EXPAND", None)
         n_el = B * int(np.prod(env.observation_shape))

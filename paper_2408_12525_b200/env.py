@@ -420,14 +420,55 @@ def spawn_streams(seed: int, n: int, offset: int = 0) -> np.ndarray:
     return out
 
 
+class _Lease:
+    """Exposes one pooled block as a new ndarray (``np.asarray(lease)``): the
+    array's base is the lease, so the block goes back to its pool when the
+    caller has dropped the array and every view of it."""
+    __slots__ = ("__array_interface__", "block", "__weakref__")
+
+    def __init__(self, block):
+        self.block = block
+        self.__array_interface__ = block.__array_interface__
+
+
+class _HostPool:
+    """Fresh output arrays without fresh pages. The reference returns new
+    arrays every step (env.py:233); allocating them new makes every step
+    page-fault and zero its whole output (16 GB for c5) before the copy.
+    Here each step still returns arrays no earlier step returned and that the
+    caller alone owns, but their memory is recycled from arrays the caller
+    has released (at most ``keep`` idle blocks per key are retained)."""
+
+    def __init__(self, keep: int = 2):
+        self.keep = keep
+        self.free: dict[Any, list] = {}
+
+    def _release(self, key, block):
+        lst = self.free.setdefault(key, [])
+        if len(lst) < self.keep:
+            lst.append(block)
+
+    def take(self, shape, dtype) -> np.ndarray:
+        import weakref
+        key = (tuple(shape), np.dtype(dtype).str)
+        lst = self.free.get(key)
+        block = lst.pop() if lst else np.empty(shape, dtype)
+        lease = _Lease(block)
+        weakref.finalize(lease, self._release, key, block)
+        return np.asarray(lease)
+
+
 class NumpyBatchEnv:
     """Reference-shaped facade: numpy in, numpy out (env.py:486-588).
 
     Every ``step`` goes through ``lg_step_host``: the host->device copy of the
     actions and the device->host copies of obs/reward/done/info happen inside
-    the library call. Pass ``pinned=True`` to stage through page-locked
-    buffers (reused across steps; the arrays returned by ``step`` are then
-    overwritten by the next step unless ``copy=True``).
+    the library call. With ``copy=True`` (the default) each step returns new
+    arrays, as the reference does; their memory comes from arrays the caller
+    has released (``_HostPool``), so a step does not fault in fresh pages.
+    Pass ``pinned=True`` to stage through page-locked buffers (reused across
+    steps; the arrays returned by ``step`` are then overwritten by the next
+    step unless ``copy=True``).
     """
 
     def __init__(self, config: EnvConfig, n_envs: int, seed: int = 0, *, device: Any = None,
@@ -440,6 +481,7 @@ class NumpyBatchEnv:
         self._bufs = None
         self._args = None
         self._obs_seen = None
+        self._pool = _HostPool()
 
     config = property(lambda self: self.env.config)
     n_envs = property(lambda self: self.env.n_envs)
@@ -452,7 +494,7 @@ class NumpyBatchEnv:
         def mk(shape, dt):
             if self.pinned:
                 return t.empty(shape, dtype=dt, pin_memory=True).numpy()
-            return np.empty(shape, dtype=t.empty(0, dtype=dt).numpy().dtype)
+            return self._pool.take(shape, t.empty(0, dtype=dt).numpy().dtype)
         if self.env.obs_dtype == "bits":
             obs = mk(((B * int(np.prod(self.env.observation_shape)) + 31) // 32,), t.int32)
         else:

@@ -200,6 +200,37 @@ def test_state_dict_round_trip_and_reference_format():
     g.bit_generator.state = st["rng_states"][0]
 
 
+@pytest.mark.parametrize("n", [16, 16384])
+def test_numpy_facade_fresh_arrays_are_owned_by_the_caller(n):
+    """copy=True returns new arrays every step (env.py:233) from recycled
+    memory: arrays the caller keeps are never written again, released ones
+    are reused, and every step's values equal the oracle's."""
+    import gc
+    cfg = EnvConfig(domain="binary", max_width=8, max_height=8, obs_size=5, max_steps=9)
+    env = NumpyBatchEnv(cfg, n, seed=4)
+    ref = O.OracleBatchEnv(cfg, n, seed=4)
+    env.reset()
+    ref.reset()
+    act = np.random.default_rng(5)
+    kept, want, addrs = [], [], set()
+    for t in range(24):
+        a = act.integers(0, cfg.n_actions, size=n)
+        out = env.step(a)
+        exp = ref.step(a)
+        assert np.array_equal(out[0], exp[0]) and np.array_equal(out[1], exp[1]), t
+        assert all(np.array_equal(out[3][k], exp[3][k]) for k in exp[3]), t
+        if t % 3 == 0:  # keep every third step's arrays
+            kept.append(out)
+            want.append(exp)
+        addrs.add(out[0].ctypes.data)
+        del out
+        gc.collect()
+    for o, e in zip(kept, want):  # untouched by the later steps
+        assert np.array_equal(o[0], e[0]) and np.array_equal(o[2], e[2])
+        assert all(np.array_equal(o[3][k], e[3][k]) for k in e[3])
+    assert len(addrs) < 24  # released arrays' memory was reused
+
+
 def test_numpy_facade_and_errors():
     cfg = EnvConfig(domain="binary", max_width=8, max_height=8, obs_size=5)
     env = NumpyBatchEnv(cfg, 16, seed=1)
