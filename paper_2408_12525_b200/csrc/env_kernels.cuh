@@ -1259,8 +1259,21 @@ __device__ __forceinline__ void env_team_body(const Params &p, int mode) {
     }
 }
 
+// Residency target per kernel: G::MINB, except the specialised 64-row kernel
+// (c4), which runs spill-free at 96 registers (MINB 10: 277 vs 272 M
+// env-steps/s at 64 registers with 266 B of spills; its occupancy at 64 was
+// capped at 32 one-warp blocks per SM anyway). The generic 64-row kernels
+// keep 16 (at 96 registers: 65,536 envs -3%, 4,096 envs +7%).
+#ifndef LG_G64_SPEC_MINB
+#define LG_G64_SPEC_MINB 10
+#endif
+template <class G, int S>
+constexpr int team_minb() {
+    return (S != 0 && G::RPL == 2) ? LG_G64_SPEC_MINB : G::MINB;
+}
+
 template <class G, int DOM, int S = 0>
-__global__ void __launch_bounds__(64, G::MINB) env_kernel(const Params p, int mode) {
+__global__ void __launch_bounds__(64, team_minb<G, S>()) env_kernel(const Params p, int mode) {
     if constexpr (kTeamChain<G>) chain_enter(p);
     env_team_body<G, DOM, S>(p, mode);
     if constexpr (kTeamChain<G>) chain_leave(p);

@@ -1219,7 +1219,10 @@ __global__ void __maxnreg__(LG_BINARY_NREG) env_solo_kernel_binary_s(const Param
 __global__ void __maxnreg__(128) env_solo_kernel_binary_small_s(const Params p, int mode) {
     env_solo_body<0, 0, SOLO_SPEC_BINARY>(p, mode);
 }
-__global__ void __maxnreg__(128) env_solo_kernel_dungeon_s(const Params p, int mode) {
+#ifndef LG_DUNGEON_S_NREG
+#define LG_DUNGEON_S_NREG 128
+#endif
+__global__ void __maxnreg__(LG_DUNGEON_S_NREG) env_solo_kernel_dungeon_s(const Params p, int mode) {
     env_solo_body<2, 1, SOLO_SPEC_DUNGEON>(p, mode);
 }
 
