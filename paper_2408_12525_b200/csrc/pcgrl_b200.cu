@@ -1175,6 +1175,29 @@ static int launch_conv1(const uint32_t *bits, long long B, int C, int OH, int OW
     return LG_OK;
 }
 
+// conv1 tile layout for the binary observation (C = 4): row-triple tables
+static int launch_conv1_tri(const uint32_t *bits, long long B, int O, const float *w, const float *bias,
+                            void *out, int relu, cudaStream_t s) {
+    Conv1TriDiv dv;
+    fastdiv_init(dv.p, (uint32_t)(O - 2));
+    const int EB = 32;
+    const size_t tables = (size_t)3 * 216 * 24 * 2 + (size_t)9 * 16 * 20 * sizeof(float);
+    const size_t tri = ((size_t)EB * O * (O - 2) + 15) & ~(size_t)15;
+    const size_t words = ((size_t)EB * 4 * O * O + 31) / 32 + 1;
+    const size_t smem = tables + tri + words * 4;
+    auto fn = conv1_tri_kernel;
+    CU(smem_attr((const void *)fn));
+    int dev = 0, sms = 0, per = 0;
+    CU(cudaGetDevice(&dev));
+    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, LG_TRI_THREADS, smem));
+    long long grid = (long long)sms * (per > 0 ? per : 1);
+    if (grid * EB > B) grid = (B + EB - 1) / EB;
+    fn<<<(unsigned)grid, LG_TRI_THREADS, smem, s>>>(bits, B, O, w, bias, out, relu, dv);
+    CU(cudaGetLastError());
+    return LG_OK;
+}
+
 extern "C" int lg_conv1_bits(const uint32_t *bits, int64_t n_envs, int C, int OH, int OW, const float *weight,
                              const float *bias, int K, void *out, int out_bf16, int relu, int nhwc, void *stream) {
     if (!bits || !weight || !bias || !out || n_envs < 1) {
@@ -1189,6 +1212,9 @@ extern "C" int lg_conv1_bits(const uint32_t *bits, int64_t n_envs, int C, int OH
         set_err("conv1_bits tile layout (lg_policy_trunk input) needs K = 16, bfloat16 output, square windows");
         return LG_EINVAL;
     }
+    const char *cg = getenv("LG_CONV1_GENERIC");
+    if (nhwc == 2 && C == 4 && OH <= 31 && !(cg && cg[0] == '1'))  // binary's planes: row triples
+        return launch_conv1_tri(bits, (long long)n_envs, OH, weight, bias, out, relu, (cudaStream_t)stream);
     const int KC = (K + 3) / 4, KCt = KC <= 4 ? 4 : KC <= 8 ? 8 : 16;
     const size_t G = (size_t)((C + 3) / 4);
     const size_t table = G * 10 * 16 * (4 * KCt + 4) * sizeof(float);  // 9 tap tables + their sum

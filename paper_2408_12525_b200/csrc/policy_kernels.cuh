@@ -12,6 +12,7 @@
 // 1/32 of the float32 input.
 #pragma once
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 
 #include "env_kernels.cuh"
@@ -247,6 +248,178 @@ __global__ void __launch_bounds__(256) conv1_bits_kernel(const uint32_t *__restr
                         else of[k * NP] = v;
                     }
                 }
+            }
+        }
+    }
+}
+
+// Row-triple variant for the binary observation (C = 4: the one-hot tile
+// planes empty / wall / border, then the frozen plane), tile layout only (the
+// lg_policy_trunk input: K = 16, bfloat16). A cell whose tile planes are
+// one-hot has one of 6 codes (tile x frozen), so three cells of a row have
+// one of 216 and a table per kernel row dy, indexed by the triple, holds the
+// sum of that row's three taps: an output pixel is three lookups instead of
+// nine. A cell that is not one-hot (never produced by the env, but the
+// entry point takes any bits) marks its triples invalid, and those pixels
+// sum the nine tap tables of their raw 4-bit masks instead.
+struct Conv1TriDiv {
+    FastDiv p;  // P = O - 2
+};
+__device__ __forceinline__ uint32_t onehot_code(uint32_t m) {  // 4-bit cell mask -> 0..5, or 255
+    const uint32_t t = m & 7u;
+    const bool ok = t != 0 && (t & (t - 1)) == 0;
+    return ok ? (uint32_t)(__ffs((int)t) - 1) * 2u + (m >> 3) : 255u;
+}
+#ifndef LG_TRI_THREADS
+#define LG_TRI_THREADS 512
+#endif
+__global__ void __launch_bounds__(LG_TRI_THREADS) conv1_tri_kernel(const uint32_t *__restrict__ bits, long long B, int O,
+                                                        const float *__restrict__ w,
+                                                        const float *__restrict__ bias, void *out, int relu,
+                                                        const Conv1TriDiv dv) {
+    extern __shared__ __align__(16) float csm[];
+    constexpr int C = 4, K = 16, RS = K + 4, NI = 216, EB = 32;
+    // Row-triple tables in half precision, 16 channels per 48-byte row (32
+    // used: the rows land 12 banks apart): an output pixel reads 96 bytes of
+    // shared memory, not 192 -- the kernel was bound by shared-memory
+    // bandwidth. fp16 (11-bit significand) sums of three entries stay well
+    // inside the bfloat16 (8-bit) rounding of the output.
+    constexpr int RH = 24;            // halves per table row
+    __half *TRh = reinterpret_cast<__half *>(csm);  // [3][NI][RH]
+    float *T = csm + 3 * NI * RH / 2;               // [9][16][RS]: the tap tables (fallback), bias in tap 0
+    for (int i = threadIdx.x; i < 3 * NI * K; i += blockDim.x) {
+        const int k = i % K, idx = (i / K) % NI, dy = i / (K * NI);
+        float s = dy == 0 ? bias[k] : 0.0f;
+        int code = idx;
+#pragma unroll
+        for (int dx = 0; dx < 3; dx++) {
+            const int cd = code % 6, tile = cd >> 1, frz = cd & 1;
+            code /= 6;
+            s += w[((k * C + tile) * 3 + dy) * 3 + dx];
+            if (frz) s += w[((k * C + 3) * 3 + dy) * 3 + dx];
+        }
+        TRh[(dy * NI + idx) * RH + k] = __float2half_rn(s);
+    }
+    for (int i = threadIdx.x; i < 9 * 16 * K; i += blockDim.x) {
+        const int k = i % K, m = (i / K) & 15, tap = i / (16 * K);
+        float s = tap == 0 ? bias[k] : 0.0f;
+#pragma unroll
+        for (int c = 0; c < C; c++)
+            if ((m >> c) & 1) s += w[(k * C + c) * 9 + tap];
+        T[(tap * 16 + m) * RS + k] = s;
+    }
+    const int OO = O * O, PE = C * OO, P = O - 2, NP = P * P;
+    uint8_t *tri = reinterpret_cast<uint8_t *>(T + 9 * 16 * RS);  // [EB][O][P]
+    uint32_t *eb = reinterpret_cast<uint32_t *>(tri + (((size_t)EB * O * P + 15) & ~(size_t)15));
+    const int NW = (EB * PE + 31) / 32 + 1;
+    const unsigned long long total_words = ((unsigned long long)B * PE + 31) / 32;
+    for (long long env0 = (long long)blockIdx.x * EB; env0 < B; env0 += (long long)gridDim.x * EB) {
+        const int ne = B - env0 < EB ? (int)(B - env0) : EB;
+        __syncthreads();  // tables built / previous envs consumed
+        const unsigned long long g0 = (unsigned long long)env0 * PE, w0 = g0 >> 5;
+        const uint32_t sh = (uint32_t)(g0 & 31);
+        for (int i = threadIdx.x; i < NW; i += blockDim.x) {
+            const uint32_t lo = w0 + i < total_words ? bits[w0 + i] : 0u;
+            const uint32_t hi = w0 + i + 1 < total_words ? bits[w0 + i + 1] : 0u;
+            eb[i] = __funnelshift_r(lo, hi, sh);
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < ne * O; i += blockDim.x) {  // one observation row (env, y) per thread
+            const int e = i / O, y = i - e * O;
+            uint32_t r[C];
+#pragma unroll
+            for (int c = 0; c < C; c++) {
+                const int b = e * PE + c * OO + y * O;  // O <= 31: the row fits one funnel shift
+                r[c] = __funnelshift_r(eb[b >> 5], eb[(b >> 5) + 1], b & 31);
+            }
+            uint8_t *dst = tri + (size_t)i * P;
+            uint32_t c0 = 0, c1 = 0;
+            for (int x = 0; x < O; x++) {
+                const uint32_t m = ((r[0] >> x) & 1u) | ((r[1] >> x) & 1u) << 1 | ((r[2] >> x) & 1u) << 2 |
+                                   ((r[3] >> x) & 1u) << 3;
+                const uint32_t c2 = onehot_code(m);
+                if (x >= 2) dst[x - 2] = (uint8_t)((c0 | c1 | c2) > 5u ? 255u : c0 + 6u * c1 + 36u * c2);
+                c0 = c1;
+                c1 = c2;
+            }
+        }
+        __syncthreads();
+        for (int it = threadIdx.x; it < ne * NP; it += blockDim.x) {
+            int e, px;
+            if (ne == EB) {  // envs fastest: a warp's 16-byte stores fill whole core-matrix rows
+                e = it & (EB - 1);
+                px = it >> 5;
+            } else {
+                px = it / ne;
+                e = it - px * ne;
+            }
+            const int y = (int)fdiv(dv.p, (uint32_t)px), x = px - y * P;
+            const uint8_t *t0 = tri + ((size_t)e * O + y) * P + x;
+            const uint32_t i0 = t0[0], i1 = t0[P], i2 = t0[2 * P];
+            float4 acc[4];
+            if (max(i0, max(i1, i2)) < (uint32_t)NI) {
+                const uint4 *r0 = reinterpret_cast<const uint4 *>(TRh + (0 * NI + i0) * RH);
+                const uint4 *r1 = reinterpret_cast<const uint4 *>(TRh + (1 * NI + i1) * RH);
+                const uint4 *r2 = reinterpret_cast<const uint4 *>(TRh + (2 * NI + i2) * RH);
+#pragma unroll
+                for (int q = 0; q < 2; q++) {
+                    const uint4 a = r0[q], b = r1[q], c = r2[q];
+                    const uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w},
+                                   cv[4] = {c.x, c.y, c.z, c.w};
+                    float f[8];
+#pragma unroll
+                    for (int j = 0; j < 4; j++) {
+                        const __half2 h = __hadd2(__hadd2(*reinterpret_cast<const __half2 *>(&av[j]),
+                                                          *reinterpret_cast<const __half2 *>(&bv[j])),
+                                                  *reinterpret_cast<const __half2 *>(&cv[j]));
+                        const float2 v = __half22float2(h);
+                        f[2 * j] = v.x;
+                        f[2 * j + 1] = v.y;
+                    }
+                    acc[2 * q] = make_float4(f[0], f[1], f[2], f[3]);
+                    acc[2 * q + 1] = make_float4(f[4], f[5], f[6], f[7]);
+                }
+            } else {  // a cell that is not one-hot: the nine taps of the raw masks
+#pragma unroll
+                for (int q = 0; q < 4; q++) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int tap = 0; tap < 9; tap++) {
+                    const int cell = (y + tap / 3) * O + x + tap % 3;
+                    uint32_t m = 0;
+#pragma unroll
+                    for (int c = 0; c < C; c++) {
+                        const int b = e * PE + c * OO + cell;
+                        m |= ((eb[b >> 5] >> (b & 31)) & 1u) << c;
+                    }
+                    const float4 *row = reinterpret_cast<const float4 *>(T + (tap * 16 + m) * RS);
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        const float4 v = row[q];
+                        acc[q].x += v.x;
+                        acc[q].y += v.y;
+                        acc[q].z += v.z;
+                        acc[q].w += v.w;
+                    }
+                }
+            }
+            const long long env = env0 + e;
+            const int m = (int)(env & 127);
+            __nv_bfloat16 *blk = reinterpret_cast<__nv_bfloat16 *>(out) + ((size_t)(env >> 7) * NP + px) * 2048;
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                uint32_t wd[4];
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const float4 a4 = acc[2 * h + (j >> 1)];
+                    float a = (j & 1) ? a4.z : a4.x, b = (j & 1) ? a4.w : a4.y;
+                    if (relu) {
+                        a = a > 0.f ? a : 0.f;
+                        b = b > 0.f ? b : 0.f;
+                    }
+                    __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+                    wd[j] = *reinterpret_cast<uint32_t *>(&h2);
+                }
+                *reinterpret_cast<uint4 *>(blk + ((h * 16 + (m >> 3)) * 64 + (m & 7) * 8)) =
+                    make_uint4(wd[0], wd[1], wd[2], wd[3]);
             }
         }
     }

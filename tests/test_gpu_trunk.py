@@ -102,3 +102,61 @@ def test_trunk_rollout_and_refresh():
     pol.refresh()
     l1, _ = pol(bits2, n)
     assert torch.allclose(l1 - l0, torch.ones_like(l0), atol=1e-4)
+
+
+def _tiles_to_nhwc(tiles, n, P1):
+    """[tile][px][2048] UMMA core-matrix blocks -> [n, px, 16] (trunk_kernel.cuh layout)."""
+    NP = P1 * P1
+    t = tiles.float().view(-1, NP, 2, 16, 8, 8)  # tile, px, h, m>>3, m&7, channel
+    return t.permute(0, 3, 4, 1, 2, 5).reshape(-1, NP, 16)[:n]
+
+
+@pytest.mark.parametrize("kw,n", [(dict(domain="binary"), 300),
+                                  (dict(domain="binary", max_width=5, max_height=5, obs_size=5), 40),
+                                  (dict(domain="binary", max_width=12, max_height=12, obs_size=9), 1000)])
+def test_conv1_row_triple_tiles(kw, n, monkeypatch):
+    """The row-triple conv1 (C <= 2) against the float32 conv and the
+    generic table kernel (LG_CONV1_GENERIC=1), same tile layout."""
+    _no_tf32()
+    cfg = EnvConfig(**kw)
+    env = BatchEnv(cfg, n, seed=7, obs_dtype="bits")
+    bits = env.reset()
+    for t in range(4):
+        bits, _, _, _ = env.step(env.random_actions(t))
+    shp = env.observation_shape
+    model = init_policy(default_arch(shp[1], shp[0], cfg.n_actions), seed=1).cuda()
+    with torch.no_grad():
+        model.trunk[0].bias.uniform_(-0.2, 0.2)
+    pol = TrunkPolicy(model, shp)
+    tri = _tiles_to_nhwc(pol.conv1_tiles(bits, n), n, pol.P1)
+    monkeypatch.setenv("LG_CONV1_GENERIC", "1")
+    gen = _tiles_to_nhwc(pol.conv1_tiles(bits, n), n, pol.P1)
+    obs = unpack_obs(bits, n, shp)
+    c1 = model.trunk[0]
+    with torch.no_grad():
+        ref = torch.relu(torch.nn.functional.conv2d(obs, c1.weight, c1.bias))
+    ref = ref.permute(0, 2, 3, 1).reshape(n, -1, 16)
+    # fp16 row tables (policy_kernels.cuh): within a bfloat16 ulp of the
+    # float32 conv, plus 1e-3 of the largest activation for cancellation
+    scale = float(ref.abs().max())
+    assert torch.allclose(tri, gen, rtol=8e-3, atol=1e-3 * scale)
+    assert torch.allclose(tri, _bf(ref), rtol=8e-3, atol=1e-3 * scale)
+    assert float((tri - ref).abs().max()) <= 8e-3 * scale
+
+
+def test_conv1_row_triple_non_onehot_bits(monkeypatch):
+    """Arbitrary bits (cells that are not one-hot) take the nine-tap path of
+    the row-triple kernel and still equal the generic kernel."""
+    _no_tf32()
+    cfg = EnvConfig(domain="binary")
+    n = 96
+    shp = cfg.observation_shape
+    words = (n * shp[0] * shp[1] * shp[2] + 31) // 32
+    g = torch.Generator(device="cuda").manual_seed(3)
+    bits = torch.randint(-2 ** 31, 2 ** 31 - 1, (words,), dtype=torch.int32, device="cuda", generator=g)
+    model = init_policy(default_arch(shp[1], shp[0], cfg.n_actions), seed=2).cuda()
+    pol = TrunkPolicy(model, shp)
+    tri = _tiles_to_nhwc(pol.conv1_tiles(bits, n), n, pol.P1)
+    monkeypatch.setenv("LG_CONV1_GENERIC", "1")
+    gen = _tiles_to_nhwc(pol.conv1_tiles(bits, n), n, pol.P1)
+    assert torch.allclose(tri, gen, rtol=8e-3, atol=1e-6)
