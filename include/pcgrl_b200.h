@@ -231,6 +231,13 @@ int lg_conv1_bits(const uint32_t *bits_dev, int64_t n_envs, int C, int OH, int O
 int lg_policy_trunk(const void *c1_tiles, int64_t n_envs, int P1, const void *w2, const float *b2, const void *w3,
                     const float *b3, const float *wh, const float *bh, int n_actions, float *logits, float *value,
                     void *stream);
+/* lg_policy_trunk + the action draw of ppo.collect_rollout (ppo.py:125-130:
+ * Categorical(logits).sample() and log_prob) in the heads' epilogue:
+ * actions int64 [n], logp f32 [n] = log softmax(logits)[action]; the uniform
+ * of env i is a counter hash of (seed, i), so one seed per step. */
+int lg_policy_trunk_sample(const void *c1_tiles, int64_t n_envs, int P1, const void *w2, const float *b2,
+                           const void *w3, const float *b3, const float *wh, const float *bh, int n_actions,
+                           float *logits, float *value, uint64_t seed, int64_t *actions, float *logp, void *stream);
 
 /* Host SeedSequence(seed).spawn(offset+n)[offset+i] -> rng [n][6] (env.py:591-594). */
 int lg_seed_streams(uint64_t seed, int64_t offset, int64_t n, uint64_t *rng_host);

@@ -81,6 +81,8 @@ SIGNATURES = {
                                   _P]),
     "lg_seed_streams": (ctypes.c_int, [ctypes.c_uint64, _I64, _I64, _P]),
     "lg_policy_trunk": (ctypes.c_int, [_P, _I64, ctypes.c_int, _P, _P, _P, _P, _P, _P, ctypes.c_int, _P, _P, _P]),
+    "lg_policy_trunk_sample": (ctypes.c_int, [_P, _I64, ctypes.c_int, _P, _P, _P, _P, _P, _P, ctypes.c_int, _P, _P,
+                                              ctypes.c_uint64, _P, _P, _P]),
     "lg_host_threads": (ctypes.c_int, []),
     "lg_unpack_host": (ctypes.c_int, [_P, _I64, _P, ctypes.c_int]),
     "lg_conv1_bits": (ctypes.c_int, [_P, _I64, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, _P, ctypes.c_int,

@@ -1244,9 +1244,9 @@ extern "C" int lg_conv1_bits(const uint32_t *bits, int64_t n_envs, int C, int OH
 #undef LG_CONV1
 }
 
-extern "C" int lg_policy_trunk(const void *c1_tiles, int64_t n_envs, int P1, const void *w2, const float *b2,
-                               const void *w3, const float *b3, const float *wh, const float *bh, int n_actions,
-                               float *logits, float *value, void *stream) {
+static int policy_trunk(const void *c1_tiles, int64_t n_envs, int P1, const void *w2, const float *b2, const void *w3,
+                        const float *b3, const float *wh, const float *bh, int n_actions, float *logits, float *value,
+                        int64_t *actions, float *logp, uint64_t seed, void *stream) {
     if (!c1_tiles || !w2 || !b2 || !w3 || !b3 || !wh || !bh || !logits || !value || n_envs < 1) {
         set_err("policy_trunk needs every buffer and n_envs >= 1");
         return LG_EINVAL;
@@ -1276,10 +1276,32 @@ extern "C" int lg_policy_trunk(const void *c1_tiles, int64_t n_envs, int P1, con
     tp.B = n_envs;
     tp.P1 = P1;
     tp.NA = n_actions;
+    tp.actions = (long long *)actions;
+    tp.logp = logp;
+    tp.seed = seed;
     const unsigned grid = (unsigned)((n_envs + 127) / 128);
     trunk_kernel<<<grid, TK_THREADS, TK_SMEM, (cudaStream_t)stream>>>(tp);
     CU(cudaGetLastError());
     return LG_OK;
+}
+
+extern "C" int lg_policy_trunk(const void *c1_tiles, int64_t n_envs, int P1, const void *w2, const float *b2,
+                               const void *w3, const float *b3, const float *wh, const float *bh, int n_actions,
+                               float *logits, float *value, void *stream) {
+    return policy_trunk(c1_tiles, n_envs, P1, w2, b2, w3, b3, wh, bh, n_actions, logits, value, nullptr, nullptr, 0,
+                        stream);
+}
+
+extern "C" int lg_policy_trunk_sample(const void *c1_tiles, int64_t n_envs, int P1, const void *w2, const float *b2,
+                                      const void *w3, const float *b3, const float *wh, const float *bh,
+                                      int n_actions, float *logits, float *value, uint64_t seed, int64_t *actions,
+                                      float *logp, void *stream) {
+    if (!actions || !logp) {
+        set_err("policy_trunk_sample needs actions and logp buffers");
+        return LG_EINVAL;
+    }
+    return policy_trunk(c1_tiles, n_envs, P1, w2, b2, w3, b3, wh, bh, n_actions, logits, value, actions, logp, seed,
+                        stream);
 }
 
 #ifdef TK_PROF

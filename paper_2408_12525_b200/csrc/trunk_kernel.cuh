@@ -45,6 +45,8 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include "env_kernels.cuh"  // splitmix64
+
 namespace lg {
 namespace tc {
 
@@ -165,6 +167,10 @@ struct TrunkParams {
     float *value;             // [B]
     long long B;
     int P1, NA;
+    // fused sampling (lg_policy_trunk_sample): a ~ Categorical(logits) per env
+    long long *actions;       // [B] or null
+    float *logp;              // [B]: log pi(a) (ppo.py:128-130)
+    unsigned long long seed;  // counter-based draw per (seed, env)
 };
 
 #ifdef TK_PROF  // cycle accounting of the MMA issuer and one epilogue thread (tools/trunk_prof.py)
@@ -488,13 +494,46 @@ __global__ void __launch_bounds__(TK_THREADS, 1) trunk_kernel(const TrunkParams 
             }
             const long long env = tile * 128 + m;
             if (env < p.B) {
+                float lg[TK_MAXNA];
+                float mx = -INFINITY;
                 for (int o = 0; o <= p.NA; o++) {
                     const float *wr = head + o * 64;
                     float a = biash[o];
 #pragma unroll
                     for (int j = 0; j < 64; j++) a = fmaf(h[j], wr[j], a);
-                    if (o < p.NA) p.logits[env * p.NA + o] = a;
-                    else p.value[env] = a;
+                    if (o < p.NA) {
+                        p.logits[env * p.NA + o] = a;
+                        if (p.actions) {
+#pragma unroll
+                            for (int q = 0; q < TK_MAXNA; q++)
+                                if (q == o) lg[q] = a;  // register array: static indices only
+                            mx = fmaxf(mx, a);
+                        }
+                    } else {
+                        p.value[env] = a;
+                    }
+                }
+                if (p.actions) {  // Categorical(logits).sample() and its log-probability
+                    float sum = 0.f;
+#pragma unroll
+                    for (int q = 0; q < TK_MAXNA; q++)
+                        if (q < p.NA) sum += __expf(lg[q] - mx);
+                    const uint64_t x = splitmix64(p.seed * 0xD1B54A32D192ED03ULL ^ splitmix64((uint64_t)env));
+                    const float u = (float)(x >> 40) * (1.0f / 16777216.0f) * sum;
+                    float c = 0.f, la = lg[0];
+                    int a = 0;
+#pragma unroll
+                    for (int q = 0; q < TK_MAXNA; q++) {
+                        if (q < p.NA) {
+                            c += __expf(lg[q] - mx);
+                            if (c <= u && q + 1 < p.NA) {
+                                a = q + 1;
+                                la = lg[q + 1];
+                            }
+                        }
+                    }
+                    p.actions[env] = a;
+                    p.logp[env] = la - mx - __logf(sum);
                 }
             }
         }

@@ -326,6 +326,26 @@ class TrunkPolicy:
                                                p(self.b3), p(self.wh), p(self.bh), na, p(logits), p(value), stream))
         return logits, value
 
+    def sample(self, bits, n_envs: int, seed: int, actions=None, logp=None, value=None):
+        """The forward pass plus ppo.collect_rollout's action draw
+        (ppo.py:125-130: Categorical(logits).sample(), log_prob) fused into the
+        trunk kernel's heads: returns (actions int64, logp f32, value f32,
+        logits f32). Env i's uniform is a counter hash of (seed, i)."""
+        torch = _torch()
+        c1 = self.conv1_tiles(bits, n_envs)
+        na = self.model.arch.n_actions
+        dev = bits.device
+        logits = torch.empty((n_envs, na), dtype=torch.float32, device=dev)
+        value = torch.empty(n_envs, dtype=torch.float32, device=dev) if value is None else value
+        actions = torch.empty(n_envs, dtype=torch.int64, device=dev) if actions is None else actions
+        logp = torch.empty(n_envs, dtype=torch.float32, device=dev) if logp is None else logp
+        stream = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+        p = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        _lib.check(_lib.load().lg_policy_trunk_sample(
+            p(c1), int(n_envs), self.P1, p(self.w2), p(self.b2), p(self.w3), p(self.b3), p(self.wh), p(self.bh), na,
+            p(logits), p(value), int(seed) & ((1 << 64) - 1), p(actions), p(logp), stream))
+        return actions, logp, value, logits
+
 
 @dataclass
 class RolloutBatch:
@@ -355,8 +375,22 @@ def collect_rollout(policy, env, length: int, sampler, obs):
     out_values = torch.empty((length, B), dtype=torch.float32, device=dev)
     out_dones = torch.empty((length, B), dtype=torch.bool, device=dev)
     finished_sum = []
+    fused = isinstance(policy, TrunkPolicy)
+    if fused:  # the draw happens in the trunk kernel: per-step seeds from the sampler's seed, no sync
+        base = sampler.initial_seed()
+        policy._draws = getattr(policy, "_draws", 0)
     with torch.no_grad():
         for t in range(length):
+            if fused:
+                policy._draws += 1
+                seed = (base * 0x9E3779B97F4A7C15 + policy._draws) & ((1 << 64) - 1)
+                policy.sample(obs, B, seed, actions=out_actions[t], logp=out_logprobs[t], value=out_values[t])
+                out_obs[t].copy_(obs)
+                obs, reward, done, info = env.step(out_actions[t], checked=True)  # sampled: in range
+                out_rewards[t] = reward
+                out_dones[t] = done
+                finished_sum.append(info["episode_reward"])
+                continue
             logits, value = policy(obs, B) if packed else policy(obs)
             probs = torch.softmax(logits.float(), dim=-1)
             actions = torch.multinomial(probs, 1, generator=sampler).squeeze(1)

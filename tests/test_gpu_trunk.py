@@ -160,3 +160,32 @@ def test_conv1_row_triple_non_onehot_bits(monkeypatch):
     monkeypatch.setenv("LG_CONV1_GENERIC", "1")
     gen = _tiles_to_nhwc(pol.conv1_tiles(bits, n), n, pol.P1)
     assert torch.allclose(tri, gen, rtol=8e-3, atol=1e-6)
+
+
+def test_trunk_fused_sampling():
+    """lg_policy_trunk_sample: the same logits/value as lg_policy_trunk, the
+    log-probability of the drawn action, and draws distributed as
+    softmax(logits) (ppo.py:125-130)."""
+    _no_tf32()
+    cfg = EnvConfig(domain="maze", representation="turtle")  # 8 actions
+    n = 16384
+    env = BatchEnv(cfg, n, seed=1, obs_dtype="bits")
+    bits = env.reset()
+    shp = env.observation_shape
+    model = init_policy(default_arch(shp[1], shp[0], cfg.n_actions), seed=4).cuda()
+    with torch.no_grad():
+        model.policy_head.weight.mul_(20.0)
+        model.policy_head.bias.uniform_(-1.0, 1.0)
+    pol = TrunkPolicy(model, shp)
+    a, lp, v, lg = pol.sample(bits, n, seed=5)
+    l0, v0 = pol(bits, n)
+    assert torch.equal(lg, l0) and torch.equal(v, v0)
+    assert int(a.min()) >= 0 and int(a.max()) < cfg.n_actions
+    ref_lp = torch.log_softmax(lg, -1).gather(1, a[:, None]).squeeze(1)
+    assert torch.allclose(lp, ref_lp, atol=1e-4, rtol=1e-4)
+    probs = torch.softmax(lg, -1)
+    freq = torch.nn.functional.one_hot(a, cfg.n_actions).float().mean(0)
+    assert float((freq - probs.mean(0)).abs().max()) < 0.02
+    a2, _, _, _ = pol.sample(bits, n, seed=5)
+    a3, _, _, _ = pol.sample(bits, n, seed=6)
+    assert torch.equal(a, a2) and not torch.equal(a, a3)
