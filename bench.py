@@ -839,7 +839,9 @@ def main():
                          "step_kernel_ms_eager": eager_step_ms},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": K,
+            # lg_step_random: one step kernel per step; maps over 32 rows/columns
+            # (64-row lane teams, not chained) also launch random_actions_kernel
+            "gpu_launches": K * (2 if max(cfg.max_width, cfg.max_height) > 32 else 1),
             "unchained_split_launch": split,
             "timing": {"eager_ms_per_step": eager_ms / K,
                        "graph_ms_per_step": graph_ms / K if graph_ms is not None else None,
