@@ -157,6 +157,35 @@ __device__ __forceinline__ long long step_action(const Params &p, long long env,
     return p.actions[env];
 }
 
+// Episode counters (lg_step's `stats`): finished episodes add into five
+// block-shared doubles, flushed to the global counters once per block. A
+// lockstep reset step (every env of the batch finishes at once) would
+// otherwise send 5 x B double atomics to the same five addresses.
+__device__ __forceinline__ double *block_stats() {
+    __shared__ double s[5];
+    return s;
+}
+__device__ __forceinline__ bool block_stats_on(const Params &p, int mode) { return p.stats && mode == MODE_STEP; }
+__device__ __forceinline__ void block_stats_begin(const Params &p, int mode) {
+    if (!block_stats_on(p, mode)) return;
+    if (threadIdx.x < 5) block_stats()[threadIdx.x] = 0.0;
+    __syncthreads();
+}
+__device__ __forceinline__ void block_stats_add(double ep_reward, double t, double start, double fin) {
+    double *s = block_stats();
+    atomicAdd(s + 0, 1.0);
+    atomicAdd(s + 1, ep_reward);
+    atomicAdd(s + 2, t);
+    atomicAdd(s + 3, start);
+    atomicAdd(s + 4, fin);
+}
+__device__ __forceinline__ void block_stats_flush(const Params &p, int mode) {
+    if (!block_stats_on(p, mode)) return;
+    __syncthreads();
+    const double *s = block_stats();
+    if (threadIdx.x < 5 && s[0] != 0.0) atomicAdd(p.stats + threadIdx.x, s[threadIdx.x]);
+}
+
 // Chained launches. Consecutive lg_step_random launches of one env on one
 // stream are programmatic dependent launches: launch k+1 may start while
 // launch k's last wave runs. Block j of every launch steps the same envs, so
@@ -1060,9 +1089,10 @@ __device__ LG_TEAM_WRITER_ATTR void write_obs_team_nc(const Params &p, const Tea
 #ifndef LG_TEAM_EARLY_SPLIT
 #define LG_TEAM_EARLY_SPLIT 1  // eighths of an env's output stored before its recompute (specialised kernels)
 #endif
-// Chained launches and in-kernel random actions are compiled into the lane
-// teams of one row per lane only: the 64-row kernel (c4) is bound by
-// instruction fetch, and the extra code measured 277 -> 264 M env-steps/s.
+// Chained launches, in-kernel random actions and block-aggregated episode
+// counters are compiled into the lane teams of one row per lane only: the
+// 64-row kernel (c4) is bound by instruction fetch (the chain code measured
+// 277 -> 264 M env-steps/s), and it runs one env per block anyway.
 template <class G>
 constexpr bool kTeamChain = G::RPL == 1;
 
@@ -1234,11 +1264,15 @@ __device__ __forceinline__ void env_team_body(const Params &p, int mode) {
                     if (p.ep_start) p.ep_start[env] = done ? e.ep_start_loss : 0.0;
                     if (p.fin_loss) p.fin_loss[env] = done ? e.prev_loss : 0.0;
                     if (done && p.stats) {
-                        atomicAdd(p.stats + 0, 1.0);
-                        atomicAdd(p.stats + 1, e.ep_reward);
-                        atomicAdd(p.stats + 2, (double)e.t);
-                        atomicAdd(p.stats + 3, e.ep_start_loss);
-                        atomicAdd(p.stats + 4, e.prev_loss);
+                        if constexpr (kTeamChain<G>) {
+                            block_stats_add(e.ep_reward, (double)e.t, e.ep_start_loss, e.prev_loss);
+                        } else {  // 64-row teams: one env per block, the counters directly
+                            atomicAdd(p.stats + 0, 1.0);
+                            atomicAdd(p.stats + 1, e.ep_reward);
+                            atomicAdd(p.stats + 2, (double)e.t);
+                            atomicAdd(p.stats + 3, e.ep_start_loss);
+                            atomicAdd(p.stats + 4, e.prev_loss);
+                        }
                     }
                 }
                 reset_now = done && !p.no_auto_reset;
@@ -1274,9 +1308,15 @@ constexpr int team_minb() {
 
 template <class G, int DOM, int S = 0>
 __global__ void __launch_bounds__(64, team_minb<G, S>()) env_kernel(const Params p, int mode) {
-    if constexpr (kTeamChain<G>) chain_enter(p);
+    if constexpr (kTeamChain<G>) {
+        chain_enter(p);
+        block_stats_begin(p, mode);
+    }
     env_team_body<G, DOM, S>(p, mode);
-    if constexpr (kTeamChain<G>) chain_leave(p);
+    if constexpr (kTeamChain<G>) {
+        block_stats_flush(p, mode);
+        chain_leave(p);
+    }
 }
 
 }  // namespace lg

@@ -1024,13 +1024,7 @@ __device__ __forceinline__ void solo_finish(const Params &p, int mode, long long
             if (p.ep_len) p.ep_len[env] = done ? e.t : 0;
             if (p.ep_start) p.ep_start[env] = done ? e.ep_start_loss : 0.0;
             if (p.fin_loss) p.fin_loss[env] = done ? e.prev_loss : 0.0;
-            if (done && p.stats) {
-                atomicAdd(p.stats + 0, 1.0);
-                atomicAdd(p.stats + 1, e.ep_reward);
-                atomicAdd(p.stats + 2, (double)e.t);
-                atomicAdd(p.stats + 3, e.ep_start_loss);
-                atomicAdd(p.stats + 4, e.prev_loss);
-            }
+            if (done && p.stats) block_stats_add(e.ep_reward, (double)e.t, e.ep_start_loss, e.prev_loss);
             st.reset_now = done && !p.no_auto_reset;
         }
     }
@@ -1193,7 +1187,9 @@ __device__ __forceinline__ void env_solo_work(const Params &p, int mode) {
 template <int DOM, int WARP, int S = 0>
 __device__ __forceinline__ void env_solo_body(const Params &p, int mode) {
     chain_enter(p);
+    block_stats_begin(p, mode);
     env_solo_work<DOM, WARP, S>(p, mode);
+    block_stats_flush(p, mode);
     chain_leave(p);
 }
 

@@ -146,3 +146,29 @@ def test_chain_disabled_by_env(monkeypatch):
         _chain_step(a, ba, i)
         _seq_step(b, bb, i)
     _compare(a, b, ba, bb)
+
+
+@pytest.mark.parametrize("case", [0, 1, 3, 4, 5])
+def test_episode_stats_are_the_finished_episodes(case):
+    """lg_step's `stats` (block-aggregated counters, env_kernels.cuh
+    block_stats_*) equal the sums over the envs whose info reports a
+    finished episode, step after step, through lockstep resets."""
+    kw, n, steps = CASES[case]
+    cfg = EnvConfig(**kw)
+    env = BatchEnv(cfg, n, seed=9, validate=False)
+    b = _buffers(env)
+    env.reset(out=b["obs"])
+    want = torch.zeros(5, dtype=torch.float64, device="cuda")
+    for i in range(steps):
+        env.random_actions(40 + i, out=b["acts"])
+        env.step_raw(b["acts"], b["obs"], b["reward"], b["done"], b["info"], b["stats"])
+        d = b["info"]["terminal"]
+        want[0] += d.sum()
+        want[1] += b["info"]["episode_reward"][d].sum()
+        want[2] += b["info"]["episode_length"][d].double().sum()
+        want[3] += b["info"]["episode_start_loss"][d].sum()
+        want[4] += b["info"]["final_loss"][d].sum()
+    torch.cuda.synchronize()
+    assert float(want[0]) > 0
+    assert float(b["stats"][0]) == float(want[0]) and float(b["stats"][2]) == float(want[2])
+    assert torch.allclose(b["stats"], want, rtol=1e-12, atol=1e-9)
