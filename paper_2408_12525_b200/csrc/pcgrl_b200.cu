@@ -699,10 +699,15 @@ extern "C" int lg_create(const lg_config *cfg, int64_t n_envs, int64_t global_of
     p.img_words = (int)((p.PB + 31) / 32 + 1);  // + pad word for the 2-word funnel shift
 
     e->geo = pick_geo(H, W);
-    // Mid-size batches (1k..19k envs on a 16x16-or-smaller map) are one wave of
+    // Batches below 19k envs on a 16x16-or-smaller map are at most one wave of
     // latency-bound work: splitting each env over a 16-lane team shortens the
-    // per-env dependency chain (measured c2, 4096 envs: 92M vs 56M env-steps/s).
-    if (e->geo == 1 && n_envs >= 1024 && n_envs < 148LL * 4 * 32 && !getenv("LG_SOLO_MID"))
+    // per-env dependency chain (measured c2, 4,096 envs: 92 M vs 56 M
+    // env-steps/s; c1, 64 envs: 4.7 M vs 3.5 M; 16..1,000 envs +20..35%).
+    // LG_SOLO_SMALL=1 keeps them on the solo kernel (block mode).
+    const char *ss = getenv("LG_SOLO_SMALL");
+    const char *sm_ = getenv("LG_SOLO_MID");  // the round-1 name
+    const bool solo_small = (ss && ss[0] == '1') || (sm_ && sm_[0] == '1');
+    if (e->geo == 1 && n_envs < 148LL * 4 * 32 && !solo_small)
         e->geo = 16;  // lane team of 16, one row per lane (H <= 16)
     if (e->geo == 1) {
         // one env per thread; per-env shared slot (in 32-bit words): bit image +

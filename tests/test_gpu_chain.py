@@ -20,7 +20,7 @@ from paper_2408_12525_b200.env import BatchEnv  # noqa: E402
 CASES = [
     # (config, envs, steps): multi-wave solo warp mode (c5 shape), episodes end
     (dict(domain="binary", max_steps=20), 131_072 + 77, 45),
-    # solo block mode (small batch) and the dungeon spec kernel (c3 shape)
+    # small batch (lane team 16 by default) and the dungeon spec kernel (c3 shape)
     (dict(domain="binary", max_steps=7), 300, 20),
     (dict(domain="dungeon", representation="wide", randomize_shape=True, change_budget=9, max_steps=30),
      65_536, 40),
@@ -136,6 +136,12 @@ def test_chain_interleaved_with_other_calls():
             _chain_step(a, ba, 77 + i)
             _seq_step(b, bb, 77 + i)
     _compare(a, b, ba, bb)
+
+
+def test_chained_solo_block_mode(monkeypatch):
+    """Small batches default to lane teams; the solo block-mode kernel chained."""
+    monkeypatch.setenv("LG_SOLO_SMALL", "1")
+    test_chained_steps_equal_random_actions_plus_step(1)
 
 
 def test_chain_disabled_by_env(monkeypatch):

@@ -47,10 +47,11 @@ def test_golden_env_case_generic_kernels(name, monkeypatch):
 
 
 @pytest.mark.parametrize("name", SMALL_CASES)
-def test_golden_env_case_lane_team_path(name, monkeypatch):
-    """Maps <= 16x16 normally run one env per thread; force the lane-team
-    kernel so both code paths are pinned on the same fixtures."""
-    monkeypatch.setenv("LG_FORCE_TEAM", "1")
+def test_golden_env_case_solo_block_path(name, monkeypatch):
+    """Small batches on maps <= 16x16 run on 16-lane teams by default; keep
+    them on the solo kernel (block mode) so both code paths are pinned on
+    the same fixtures."""
+    monkeypatch.setenv("LG_SOLO_SMALL", "1")
     test_golden_env_case(name)
 
 
@@ -509,7 +510,7 @@ U8_CASES = [
     (dict(domain="dungeon", representation="wide", pinpoints=("player", "key", "door"),
           randomize_shape=True), 40000, {}),                              # solo warp, stream layout
     (dict(domain="binary"), 40000, {"LG_STREAM": "1"}),                   # stream layout, PE % 32 != 0
-    (dict(domain="maze", representation="turtle"), 300, {}),              # solo block mode
+    (dict(domain="maze", representation="turtle"), 300, {"LG_SOLO_SMALL": "1"}),  # solo block mode
     (dict(domain="maze", representation="turtle"), 3000, {}),             # lane-team (mid-size)
     (dict(domain="binary", max_width=64, max_height=64, obs_size=7), 500, {}),   # lane team 64
     (dict(domain="dungeon", max_width=40, max_height=20, obs_size=33), 257, {}),  # team 32, odd sizes
@@ -546,8 +547,9 @@ PACKED_CASES = [
     (dict(domain="dungeon", representation="wide", pinpoints=("player", "key", "door"),
           randomize_shape=True), 20000, {}),                              # solo warp, stream layout
     (dict(domain="binary"), 20000, {"LG_STREAM": "1"}),                   # stream layout, PE % 32 != 0
-    (dict(domain="binary"), 64, {}),                                      # c1: block mode, shared words
-    (dict(domain="maze", representation="turtle"), 300, {}),              # block mode, E * PE % 32 != 0
+    (dict(domain="binary"), 64, {"LG_SOLO_SMALL": "1"}),                  # block mode, shared words
+    (dict(domain="maze", representation="turtle"), 300, {"LG_SOLO_SMALL": "1"}),  # block mode, E * PE % 32 != 0
+    (dict(domain="binary"), 64, {}),                                      # c1: lane team 16
     (dict(domain="maze", representation="turtle"), 4096, {}),             # c2: lane team 16
     (dict(domain="binary", max_width=64, max_height=64, obs_size=7), 500, {}),   # lane team 64 (c4 shape)
     (dict(domain="dungeon", max_width=40, max_height=20, obs_size=33), 257, {}),  # team 32, odd sizes
