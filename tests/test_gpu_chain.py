@@ -178,3 +178,21 @@ def test_episode_stats_are_the_finished_episodes(case):
     assert float(want[0]) > 0
     assert float(b["stats"][0]) == float(want[0]) and float(b["stats"][2]) == float(want[2])
     assert torch.allclose(b["stats"], want, rtol=1e-12, atol=1e-9)
+
+
+@pytest.mark.parametrize("obs_dtype", ["uint8", "bits"])
+@pytest.mark.parametrize("case", [0, 1, 2, 3])
+def test_chained_steps_other_observation_formats(case, obs_dtype):
+    """uint8 planes and the packed bit stream (chained unless the stream has
+    words shared between blocks, which need a memset before each step)."""
+    kw, n, steps = CASES[case]
+    cfg = EnvConfig(**kw)
+    a = BatchEnv(cfg, n, seed=3, validate=False, obs_dtype=obs_dtype)
+    b = BatchEnv(cfg, n, seed=3, validate=False, obs_dtype=obs_dtype)
+    ba, bb = _buffers(a), _buffers(b)
+    a.reset(out=ba["obs"])
+    b.reset(out=bb["obs"])
+    for i in range(min(steps, 25)):
+        _chain_step(a, ba, 300 + i)
+        _seq_step(b, bb, 300 + i)
+    _compare(a, b, ba, bb)
