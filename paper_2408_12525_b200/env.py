@@ -225,11 +225,31 @@ class BatchEnv:
             self._h, _ptr(actions), _ptr(obs) if obs is not None else None, _ptr(reward), _ptr(done),
             ci, _ptr(stats) if stats is not None else None, _stream(self._torch, self.device)))
 
+    def _check_out(self, name, t, dtype, numel):
+        if t.device != self.device or t.dtype != dtype or not t.is_contiguous() or t.numel() != numel:
+            raise ValueError(f"{name}: expected a contiguous {dtype} tensor of {numel} elements on {self.device}, "
+                             f"got {t.dtype} {tuple(t.shape)} on {t.device}")
+
     def step_random(self, seed: int, obs, reward, done, info=None, stats=None, actions_out=None) -> None:
         """harness.bench_random_fps's loop body (harness.py:149-175) on device:
         uniform actions (the draw of ``random_actions(seed)``, recorded in
         ``actions_out``) and the step, in one call. Consecutive calls overlap
         launch to launch (include/pcgrl_b200.h lg_step_random)."""
+        t, B = self._torch, self._n
+        if not self._started:
+            raise RuntimeError("reset() the batch before stepping")
+        if obs is not None:
+            n_el = B * int(np.prod(self.observation_shape))
+            if self.obs_dtype == "bits":
+                self._check_out("obs", obs, t.int32, (n_el + 31) // 32)
+            else:
+                self._check_out("obs", obs, t.uint8 if self.obs_dtype == "uint8" else t.float32, n_el)
+        self._check_out("reward", reward, t.float64, B)
+        self._check_out("done", done, t.bool, B)
+        if actions_out is not None:
+            self._check_out("actions_out", actions_out, t.int64, B)
+        if stats is not None:
+            self._check_out("stats", stats, t.float64, 5)
         ci = None
         if info is not None:
             ci = ctypes.byref(_lib.LgInfo(*[_ptr(info[k]) if k in info else None for k in INFO_KEYS]))

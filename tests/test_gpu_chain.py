@@ -196,3 +196,20 @@ def test_chained_steps_other_observation_formats(case, obs_dtype):
         _chain_step(a, ba, 300 + i)
         _seq_step(b, bb, 300 + i)
     _compare(a, b, ba, bb)
+
+
+def test_step_random_argument_checks():
+    cfg = EnvConfig(domain="binary", max_width=8, max_height=8, obs_size=5)
+    env = BatchEnv(cfg, 40, seed=0, validate=False)
+    b = _buffers(env)
+    with pytest.raises(RuntimeError):
+        _chain_step(env, b, 0)
+    env.reset(out=b["obs"])
+    with pytest.raises(ValueError):
+        env.step_random(0, b["obs"], b["reward"].float(), b["done"])
+    with pytest.raises(ValueError):
+        env.step_random(0, b["obs"][:20], b["reward"], b["done"])
+    with pytest.raises(ValueError):
+        env.step_random(0, b["obs"], b["reward"], b["done"], actions_out=b["acts"].int())
+    _chain_step(env, b, 0)
+    assert env.errors() == 0
