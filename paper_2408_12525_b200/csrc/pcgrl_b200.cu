@@ -1267,7 +1267,8 @@ static int policy_trunk(const void *c1_tiles, int64_t n_envs, int P1, const void
             return LG_EINVAL;
         }
     NvtxRange nv("lg_policy_trunk");
-    CU(smem_attr((const void *)trunk_kernel, (int)TK_SMEM));
+    CU(smem_attr((const void *)trunk_kernel_t<false>, (int)TK_SMEM));
+    CU(smem_attr((const void *)trunk_kernel_t<true>, (int)TK_SMEM));
     TrunkParams tp;
     tp.c1 = reinterpret_cast<const __nv_bfloat16 *>(c1_tiles);
     tp.w2 = reinterpret_cast<const __nv_bfloat16 *>(w2);
@@ -1284,9 +1285,38 @@ static int policy_trunk(const void *c1_tiles, int64_t n_envs, int P1, const void
     tp.actions = (long long *)actions;
     tp.logp = logp;
     tp.seed = seed;
-    const unsigned grid = (unsigned)((n_envs + 127) / 128);
-    trunk_kernel<<<grid, TK_THREADS, TK_SMEM, (cudaStream_t)stream>>>(tp);
-    CU(cudaGetLastError());
+    // Whole waves of one tile per SM, then the tail: when it fills at most
+    // half the SMs it runs as half-tile CTA pairs (trunk_kernel_t<true>).
+    const long long tiles = (n_envs + 127) / 128;
+    int dev = 0, sms = 0;
+    CU(cudaGetDevice(&dev));
+    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int nch = (P1 - 2 + TK_CW - 1) / TK_CW;
+    long long tail = tiles % sms;
+    const char *tt = getenv("LG_TRUNK_TAIL");
+    if (nch < 2 || 2 * tail > sms || (tt && tt[0] == '0')) tail = 0;
+    const long long whole = tiles - tail;
+    tp.tile0 = 0;
+    if (whole > 0) {
+        trunk_kernel_t<false><<<(unsigned)whole, TK_THREADS, TK_SMEM, (cudaStream_t)stream>>>(tp);
+        CU(cudaGetLastError());
+    }
+    if (tail > 0) {
+        tp.tile0 = whole;
+        cudaLaunchConfig_t c = {};
+        c.gridDim = dim3((unsigned)(2 * tail));
+        c.blockDim = dim3(TK_THREADS);
+        c.dynamicSmemBytes = TK_SMEM;
+        c.stream = (cudaStream_t)stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        c.attrs = at;
+        c.numAttrs = 1;
+        CU(cudaLaunchKernelEx(&c, trunk_kernel_t<true>, tp));
+    }
     return LG_OK;
 }
 

@@ -153,6 +153,23 @@ __device__ __forceinline__ void tmem_zero32(uint32_t taddr) {
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// a float in the shared memory of CTA `rank` of the cluster (same offset as `local`)
+__device__ __forceinline__ float ld_peer_f32(const void *local, uint32_t rank) {
+    uint32_t ra;
+    float v;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(su32(local)), "r"(rank));
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(ra) : "memory");
+    return v;
+}
+
 }  // namespace tc
 
 struct TrunkParams {
@@ -166,6 +183,7 @@ struct TrunkParams {
     float *logits;            // [B][NA]
     float *value;             // [B]
     long long B;
+    long long tile0;          // first 128-env tile of this launch
     int P1, NA;
     // fused sampling (lg_policy_trunk_sample): a ~ Categorical(logits) per env
     long long *actions;       // [B] or null
@@ -230,13 +248,77 @@ __device__ __forceinline__ void conv2_row(uint32_t acc, const uint64_t (&dr)[3],
     }
 }
 
-__global__ void __launch_bounds__(TK_THREADS, 1) trunk_kernel(const TrunkParams p) {
+// bias + ReLU of the FC accumulator row, then the policy and value heads
+// (fp32), and with p.actions the action draw of ppo.py:125-130
+__device__ __forceinline__ void trunk_heads(const TrunkParams &p, const float *head, const float *bias3,
+                                            const float *biash, float (&h)[64], long long env) {
+#pragma unroll
+    for (int j = 0; j < 64; j++) {
+        const float v = h[j] + bias3[j];
+        h[j] = v > 0.f ? v : 0.f;
+    }
+    if (env >= p.B) return;
+    float lg[TK_MAXNA];
+    float mx = -INFINITY;
+    for (int o = 0; o <= p.NA; o++) {
+        const float *wr = head + o * 64;
+        float a = biash[o];
+#pragma unroll
+        for (int j = 0; j < 64; j++) a = fmaf(h[j], wr[j], a);
+        if (o < p.NA) {
+            p.logits[env * p.NA + o] = a;
+            if (p.actions) {
+#pragma unroll
+                for (int q = 0; q < TK_MAXNA; q++)
+                    if (q == o) lg[q] = a;  // register array: static indices only
+                mx = fmaxf(mx, a);
+            }
+        } else {
+            p.value[env] = a;
+        }
+    }
+    if (p.actions) {  // Categorical(logits).sample() and its log-probability
+        float sum = 0.f;
+#pragma unroll
+        for (int q = 0; q < TK_MAXNA; q++)
+            if (q < p.NA) sum += __expf(lg[q] - mx);
+        const uint64_t x = splitmix64(p.seed * 0xD1B54A32D192ED03ULL ^ splitmix64((uint64_t)env));
+        const float u = (float)(x >> 40) * (1.0f / 16777216.0f) * sum;
+        float c = 0.f, la = lg[0];
+        int a = 0;
+#pragma unroll
+        for (int q = 0; q < TK_MAXNA; q++) {
+            if (q < p.NA) {
+                c += __expf(lg[q] - mx);
+                if (c <= u && q + 1 < p.NA) {
+                    a = q + 1;
+                    la = lg[q + 1];
+                }
+            }
+        }
+        p.actions[env] = a;
+        p.logp[env] = la - mx - __logf(sum);
+    }
+}
+
+// SPLIT: launched in clusters of 2 for the tail of a launch (the tiles past
+// its last whole wave): the two CTAs of a cluster take the two halves of one
+// tile's column chunks, each accumulates its pixels' FC partial sums in its
+// own TMEM, CTA 1 hands its partial to CTA 0 through distributed shared
+// memory, and CTA 0 finishes the heads. 512 tiles (65,536 envs) on 148 SMs
+// are 3 whole waves + 68 tiles: the 68 run as 136 half-tile CTAs in one
+// wave of roughly half a tile's time instead of a fourth whole-tile wave.
+template <bool SPLIT>
+__global__ void __launch_bounds__(TK_THREADS, 1) trunk_kernel_t(const TrunkParams p) {
     extern __shared__ __align__(1024) uint8_t sm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int P1 = p.P1, P2 = P1 - 2, NP1 = P1 * P1;
-    const int nch = (P2 + TK_CW - 1) / TK_CW;
-    const int nrows = nch * P2;  // output rows over all chunks
-    const long long tile = blockIdx.x;
+    const int nch_all = (P2 + TK_CW - 1) / TK_CW;
+    const int rank = SPLIT ? (int)tc::cluster_rank() : 0;
+    const int cxa = SPLIT ? rank * ((nch_all + 1) / 2) : 0;  // this CTA's column chunks
+    const int cxb = SPLIT && rank == 0 ? (nch_all + 1) / 2 : nch_all;
+    const int nrows = (cxb - cxa) * P2;  // output rows over this CTA's chunks
+    const long long tile = p.tile0 + (SPLIT ? blockIdx.x / 2 : blockIdx.x);
     const uint32_t s0 = tc::su32(sm);
     uint64_t *bars = reinterpret_cast<uint64_t *>(sm + TK_OFF_BAR);
     const uint32_t b0 = tc::su32(bars);
@@ -283,7 +365,7 @@ __global__ void __launch_bounds__(TK_THREADS, 1) trunk_kernel(const TrunkParams 
             tc::mbar_expect_tx(BAR(W2F), 3 * 3072);
             tc::bulk_g2s(s0 + TK_OFF_W2, p.w2, 3 * 3072, BAR(W2F));
             int L = 0;
-            for (int cx = 0; cx < nch; cx++) {
+            for (int cx = cxa; cx < cxb; cx++) {
                 const int ncol = min(TK_RC, P1 - cx * TK_CW);
                 for (int r = 0; r < P1; r++, L++) {
                     const int slot = L % TK_RING;
@@ -297,7 +379,7 @@ __global__ void __launch_bounds__(TK_THREADS, 1) trunk_kernel(const TrunkParams 
         } else if (lane == 1) {
             const uint8_t *w3 = reinterpret_cast<const uint8_t *>(p.w3);
             int pix = 0;
-            for (int cx = 0; cx < nch; cx++) {
+            for (int cx = cxa; cx < cxb; cx++) {
                 const int cw = min(TK_CW, P2 - cx * TK_CW);
                 for (int y = 0; y < P2; y++)
                     for (int xl = 0; xl < cw; xl++, pix++) {
@@ -330,9 +412,9 @@ __global__ void __launch_bounds__(TK_THREADS, 1) trunk_kernel(const TrunkParams 
         const uint64_t d_w2 = tc::sdesc(s0 + TK_OFF_W2, 1536, 128);
         int Lw = 0;   // conv1 rows waited for
         int R = 0;
-        for (int cx = 0; cx < nch; cx++) {
+        for (int cx = cxa; cx < cxb; cx++) {
             const int cw = min(TK_CW, P2 - cx * TK_CW);
-            const int L0 = cx * P1;
+            const int L0 = (cx - cxa) * P1;  // ring rows this CTA streamed before chunk cx
             for (int y = 0; y < P2; y++, R++) {
                 const int ab = R % TK_EPI;
                 TKT(0);
@@ -380,7 +462,7 @@ __global__ void __launch_bounds__(TK_THREADS, 1) trunk_kernel(const TrunkParams 
         const uint64_t d_a3 = tc::sdesc(s0 + TK_OFF_A3, 2048, 128);
         const uint64_t d_w3 = tc::sdesc(s0 + TK_OFF_W3, 1024, 128);
         int pix = 0, kg0 = 0, kg1 = 0, R = 0;  // FC pixels issued; A3 blocks consumed per epilogue group
-        for (int cx = 0; cx < nch; cx++) {
+        for (int cx = cxa; cx < cxb; cx++) {
             const int cw = min(TK_CW, P2 - cx * TK_CW);
             for (int y = 0; y < P2; y++, R++) {
                 const int g = R % TK_EPI;
@@ -423,7 +505,7 @@ __global__ void __launch_bounds__(TK_THREADS, 1) trunk_kernel(const TrunkParams 
         long long eprof[4] = {0, 0, 0, 0}, e0 = clock64();
 #endif
         for (int R = grp; R < nrows; R += TK_EPI) {
-            const int cw = min(TK_CW, P2 - (R / P2) * TK_CW);
+            const int cw = min(TK_CW, P2 - (cxa + R / P2) * TK_CW);
 #ifdef TK_PROF
             long long ew = clock64();
 #endif
@@ -487,56 +569,28 @@ __global__ void __launch_bounds__(TK_THREADS, 1) trunk_kernel(const TrunkParams 
                 tc::tmem_ld32(T_D3 + lane_off + half * 32, r);
                 tc::tmem_wait_ld();
 #pragma unroll
-                for (int j = 0; j < 32; j++) {
-                    const float v = __uint_as_float(r[j]) + bias3[half * 32 + j];
-                    h[half * 32 + j] = v > 0.f ? v : 0.f;
-                }
+                for (int j = 0; j < 32; j++) h[half * 32 + j] = __uint_as_float(r[j]);
             }
-            const long long env = tile * 128 + m;
-            if (env < p.B) {
-                float lg[TK_MAXNA];
-                float mx = -INFINITY;
-                for (int o = 0; o <= p.NA; o++) {
-                    const float *wr = head + o * 64;
-                    float a = biash[o];
+            if constexpr (!SPLIT) {
+                trunk_heads(p, head, bias3, biash, h, tile * 128 + m);
+            } else {  // the partial sums go to shared memory: [64][128] floats in the (idle) ring
+                float *xb = reinterpret_cast<float *>(sm + TK_OFF_RING);
 #pragma unroll
-                    for (int j = 0; j < 64; j++) a = fmaf(h[j], wr[j], a);
-                    if (o < p.NA) {
-                        p.logits[env * p.NA + o] = a;
-                        if (p.actions) {
-#pragma unroll
-                            for (int q = 0; q < TK_MAXNA; q++)
-                                if (q == o) lg[q] = a;  // register array: static indices only
-                            mx = fmaxf(mx, a);
-                        }
-                    } else {
-                        p.value[env] = a;
-                    }
-                }
-                if (p.actions) {  // Categorical(logits).sample() and its log-probability
-                    float sum = 0.f;
-#pragma unroll
-                    for (int q = 0; q < TK_MAXNA; q++)
-                        if (q < p.NA) sum += __expf(lg[q] - mx);
-                    const uint64_t x = splitmix64(p.seed * 0xD1B54A32D192ED03ULL ^ splitmix64((uint64_t)env));
-                    const float u = (float)(x >> 40) * (1.0f / 16777216.0f) * sum;
-                    float c = 0.f, la = lg[0];
-                    int a = 0;
-#pragma unroll
-                    for (int q = 0; q < TK_MAXNA; q++) {
-                        if (q < p.NA) {
-                            c += __expf(lg[q] - mx);
-                            if (c <= u && q + 1 < p.NA) {
-                                a = q + 1;
-                                la = lg[q + 1];
-                            }
-                        }
-                    }
-                    p.actions[env] = a;
-                    p.logp[env] = la - mx - __logf(sum);
-                }
+                for (int j = 0; j < 64; j++) xb[j * 128 + m] = h[j];
             }
         }
+    }
+    if constexpr (SPLIT) {
+        tc::cluster_sync();  // both partials are in shared memory
+        if (rank == 0 && warp >= 2 && warp < 6) {  // epilogue group 0 of CTA 0: sum, bias, ReLU, heads
+            const int m = (warp & 3) * 32 + lane;
+            const float *xb = reinterpret_cast<const float *>(sm + TK_OFF_RING);
+            float h[64];
+#pragma unroll
+            for (int j = 0; j < 64; j++) h[j] = xb[j * 128 + m] + tc::ld_peer_f32(xb + j * 128 + m, 1);
+            trunk_heads(p, head, bias3, biash, h, tile * 128 + m);
+        }
+        tc::cluster_sync();  // CTA 0 has read CTA 1's shared memory
     }
     tc::tc_before();
     __syncthreads();

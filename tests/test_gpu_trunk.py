@@ -189,3 +189,33 @@ def test_trunk_fused_sampling():
     a2, _, _, _ = pol.sample(bits, n, seed=5)
     a3, _, _, _ = pol.sample(bits, n, seed=6)
     assert torch.equal(a, a2) and not torch.equal(a, a3)
+
+
+@pytest.mark.parametrize("n", [300, 128 * 158 + 5])
+def test_trunk_tail_split_pairs(n, monkeypatch):
+    """The tiles past the last whole wave run as half-tile CTA pairs (FC
+    partials summed through DSMEM): the same logits/value as whole tiles
+    (LG_TRUNK_TAIL=0) up to fp32 summation order, and the torch reference."""
+    _no_tf32()
+    cfg = EnvConfig(domain="binary")
+    env = BatchEnv(cfg, n, seed=2, obs_dtype="bits")
+    bits = env.reset()
+    bits, _, _, _ = env.step(env.random_actions(1))
+    shp = env.observation_shape
+    model = init_policy(default_arch(shp[1], shp[0], cfg.n_actions), seed=3).cuda()
+    with torch.no_grad():
+        model.policy_head.weight.mul_(50.0)
+        model.trunk[5].bias.uniform_(-0.1, 0.1)
+    pol = TrunkPolicy(model, shp)
+    lg, v = pol(bits, n)
+    monkeypatch.setenv("LG_TRUNK_TAIL", "0")
+    lg0, v0 = pol(bits, n)
+    for a, b in ((lg, lg0), (v, v0)):
+        scale = float(b.abs().max())
+        assert float((a - b).abs().max()) <= 1e-4 * scale + 1e-5  # fp32 sums of ~23k terms, reordered
+    obs = unpack_obs(bits, n, shp)
+    with torch.no_grad():
+        el, ev = emulated(model, obs)
+    for got, emu in ((lg, el), (v, ev)):
+        scale = float(emu.abs().max())
+        assert float((got - emu).abs().max()) <= 3e-3 * scale + 1e-5
