@@ -394,10 +394,10 @@ def main():
         if ep_len in times:
             steady = statistics.median(v for k, v in times.items() if k % ep_len)
             t_reset = times[ep_len]
-            boundary = {"step": ep_len, "reset_step_ms": t_reset, "steady_step_ms": steady,
-                        "amortized_value": global_b * ep_len / (((ep_len - 1) * steady + t_reset) / 1e3),
-                        "note": "every env of the lockstep batch auto-resets on step 3*h*w; "
-                                "amortized = one episode cycle of L-1 steady steps + the reset step"}
+            boundary = {"step": ep_len, "reset_step_ms": t_reset, "steady_step_ms_events": steady,
+                        "note": "every env of the lockstep batch auto-resets on step 3*h*w; both timed with "
+                                "per-step events during the burn-in (which break the launch chain); "
+                                "amortized = one episode cycle of L-1 steps at the timed rate + the reset step"}
     t0_step = args.warmup + burn
     if world > 1:
         dist.barrier()
@@ -498,6 +498,9 @@ def main():
     if errs:
         raise SystemExit(f"device error flags {errs}")
     value = global_b * K / (elapsed_ms / 1e3)
+    if boundary:
+        L, steady_ms = boundary["step"], elapsed_ms / K
+        boundary["amortized_value"] = global_b * L / (((L - 1) * steady_ms + boundary["reset_step_ms"]) / 1e3)
 
     obs_shape = env.observation_shape
     team = env._desc.team
