@@ -554,7 +554,8 @@ def main():
         n_el = B * int(np.prod(env.observation_shape))
         # the library packs when there are no control planes and the float32
         # observation is >= 2 MB (below that the plain copy has lower latency)
-        use_packed = packed and not cfg.controllable and n_el * 4 >= (2 << 20)
+        # (below that only into pageable arrays: the fresh-array run)
+        use_packed = packed and not cfg.controllable and (n_el * 4 >= (2 << 20) or fresh)
         obs_d2h = (n_el + 31) // 32 * 4 if use_packed else n_el * (1 if obs_dtype == "uint8" else 4)
         d2h = obs_d2h + B * (8 + 1 + 1 + 8 + 8 + 8 + 8)
         out = {"value": global_b * n_steps / dt, "unit": UNIT,

@@ -381,6 +381,10 @@ struct lg_env {
     unsigned char *d_done = nullptr, *d_term = nullptr;
     double *d_er = nullptr, *d_es = nullptr, *d_fl = nullptr;
     long long *d_el = nullptr;
+    // the per-env outputs above are one device block [rew|er|es|fl|el|done|term]
+    // (d_small); small batches copy it to the host in one transfer (h_small)
+    void *d_small = nullptr;
+    uint8_t *h_small = nullptr;
     // packed observation transfer (lg_step_host): device bit stream, pinned
     // host copy, one event per copied chunk
     uint32_t *d_bits = nullptr;
@@ -843,11 +847,12 @@ extern "C" int lg_destroy(lg_env *e) {
     DeviceGuard dg(e->device);
     Params &p = e->base;
     void *ptrs[] = {p.rows, p.hot, p.mv, p.lossv, p.rs, p.ri, p.rb, p.mseed, p.err, p.aux,
-                    e->d_act, e->d_obs, e->d_rew, e->d_done, e->d_term, e->d_er, e->d_es, e->d_fl, e->d_el,
+                    e->d_act, e->d_obs, e->d_small,
                     e->d_bits, e->tickets, e->act_scratch};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     if (e->h_bits) cudaFreeHost(e->h_bits);
+    if (e->h_small) cudaFreeHost(e->h_small);
     for (cudaEvent_t ev : e->chunk_ev) cudaEventDestroy(ev);
     delete e;
     return LG_OK;
@@ -882,14 +887,22 @@ static int check_obs_ptr(const void *obs) {
 
 // Packed transfer is used when every observation element is a 0/1 plane
 // element (no control planes); LG_HOST_EXPAND=0 forces the float32 copy.
-static bool packed_ok(const lg_env *e) {
+static bool packed_ok(const lg_env *e, const void *dst) {
     if (e->cfg.n_ctrl > 0) return false;
     const char *v = getenv("LG_HOST_EXPAND");
     if (v) return v[0] != '0';
     // below ~2 MB of float32 observations the copy is latency, not bandwidth:
-    // the plain copy wins (c1, 64 envs: 0.61 vs 0.58 M env-steps/s)
+    // into page-locked memory the plain copy wins (c1, 64 envs: 0.61 vs
+    // 0.58 M env-steps/s); into pageable memory the driver stages it through
+    // its own buffer (c1: 0.29 M), and the packed stream + host expansion wins
     const size_t n = (size_t)e->B * e->C * e->OH * e->OW;
-    return n * 4 >= ((size_t)2 << 20);
+    if (n * 4 >= ((size_t)2 << 20)) return true;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, dst) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return a.type != cudaMemoryTypeHost;
 }
 
 // Some stream words are shared by two blocks (or lane teams): they are
@@ -1044,29 +1057,38 @@ extern "C" int lg_step_host(lg_env *e, const int64_t *actions_host, void *obs_ho
     const size_t n_elems = B * (size_t)e->C * e->OH * e->OW;
     size_t obs_bytes = n_elems * (e->base.obs_u8 ? 1 : sizeof(float));
     const bool dev_bits = e->base.obs_bits;  // the env's own format is the packed stream
-    const bool packed = obs_host && (dev_bits || packed_ok(e));
+    const bool packed = obs_host && (dev_bits || packed_ok(e, obs_host));
     // Staging buffers are allocated into locals and committed to the env only
     // when every allocation succeeded, so a failed call leaves no half-set
     // state behind for the next one to launch into.
+    // small batches: the per-env outputs come back in one transfer (each
+    // cudaMemcpyAsync costs microseconds of latency; c1 has 8 of them)
+    const size_t small_bytes = B * (5 * 8 + 2);
+    const bool one_copy = small_bytes <= ((size_t)1 << 20);
     if (!e->d_act) {
-        void *q[8] = {};
-        const size_t sz[8] = {B * 8, B * 8, B, B, B * 8, B * 8, B * 8, B * 8};
-        cudaError_t err = cudaSuccess;
-        for (int i = 0; i < 8 && err == cudaSuccess; i++) err = cudaMalloc(&q[i], sz[i]);
+        void *act = nullptr, *blk = nullptr;
+        uint8_t *hs = nullptr;
+        cudaError_t err = cudaMalloc(&act, B * 8);
+        if (err == cudaSuccess) err = cudaMalloc(&blk, small_bytes);
+        if (err == cudaSuccess && one_copy) err = cudaHostAlloc((void **)&hs, small_bytes, cudaHostAllocDefault);
         if (err != cudaSuccess) {
-            for (void *x : q)
-                if (x) cudaFree(x);
+            if (act) cudaFree(act);
+            if (blk) cudaFree(blk);
+            if (hs) cudaFreeHost(hs);
             set_err("CUDA allocation failed: %s", cudaGetErrorString(err));
             return LG_ECUDA;
         }
-        e->d_act = (long long *)q[0];
-        e->d_rew = (double *)q[1];
-        e->d_done = (unsigned char *)q[2];
-        e->d_term = (unsigned char *)q[3];
-        e->d_er = (double *)q[4];
-        e->d_es = (double *)q[5];
-        e->d_fl = (double *)q[6];
-        e->d_el = (long long *)q[7];
+        uint8_t *b = reinterpret_cast<uint8_t *>(blk);
+        e->d_act = (long long *)act;
+        e->d_small = blk;
+        e->h_small = hs;
+        e->d_rew = (double *)(b);
+        e->d_er = (double *)(b + B * 8);
+        e->d_es = (double *)(b + B * 16);
+        e->d_fl = (double *)(b + B * 24);
+        e->d_el = (long long *)(b + B * 32);
+        e->d_done = b + B * 40;
+        e->d_term = b + B * 41;
     }
     if (packed && !e->d_bits) {
         const size_t bits_bytes = ((n_elems + 31) / 32) * 4;
@@ -1116,9 +1138,13 @@ extern "C" int lg_step_host(lg_env *e, const int64_t *actions_host, void *obs_ho
     } else if (obs_host) {
         CU(cudaMemcpyAsync(obs_host, e->d_obs, obs_bytes, cudaMemcpyDeviceToHost, s));
     }
-    CU(cudaMemcpyAsync(reward_host, e->d_rew, B * 8, cudaMemcpyDeviceToHost, s));
-    CU(cudaMemcpyAsync(done_host, e->d_done, B, cudaMemcpyDeviceToHost, s));
-    if (info_host) {
+    if (one_copy && e->h_small) {
+        CU(cudaMemcpyAsync(e->h_small, e->d_small, small_bytes, cudaMemcpyDeviceToHost, s));
+    } else {
+        CU(cudaMemcpyAsync(reward_host, e->d_rew, B * 8, cudaMemcpyDeviceToHost, s));
+        CU(cudaMemcpyAsync(done_host, e->d_done, B, cudaMemcpyDeviceToHost, s));
+    }
+    if (info_host && !(one_copy && e->h_small)) {
         if (info_host->terminal) CU(cudaMemcpyAsync(info_host->terminal, e->d_term, B, cudaMemcpyDeviceToHost, s));
         if (info_host->episode_reward)
             CU(cudaMemcpyAsync(info_host->episode_reward, e->d_er, B * 8, cudaMemcpyDeviceToHost, s));
@@ -1129,6 +1155,18 @@ extern "C" int lg_step_host(lg_env *e, const int64_t *actions_host, void *obs_ho
         if (info_host->final_loss)
             CU(cudaMemcpyAsync(info_host->final_loss, e->d_fl, B * 8, cudaMemcpyDeviceToHost, s));
     }
+    auto scatter_small = [&]() {  // the one-copy block into the caller's arrays
+        if (!(one_copy && e->h_small)) return;
+        const uint8_t *h = e->h_small;
+        memcpy(reward_host, h, B * 8);
+        memcpy(done_host, h + B * 40, B);
+        if (!info_host) return;
+        if (info_host->episode_reward) memcpy(info_host->episode_reward, h + B * 8, B * 8);
+        if (info_host->episode_start_loss) memcpy(info_host->episode_start_loss, h + B * 16, B * 8);
+        if (info_host->final_loss) memcpy(info_host->final_loss, h + B * 24, B * 8);
+        if (info_host->episode_length) memcpy(info_host->episode_length, h + B * 32, B * 8);
+        if (info_host->terminal) memcpy(info_host->terminal, h + B * 41, B);
+    };
     if (packed && !dev_bits) {
         ChunkPoll cp{e, false};
         lg_host::expand_bits(e->h_bits, obs_host, e->base.obs_u8 ? 1 : 0, n_elems, e->chunk_bytes, chunk_ready,
@@ -1138,9 +1176,11 @@ extern "C" int lg_step_host(lg_env *e, const int64_t *actions_host, void *obs_ho
             set_err("CUDA error while copying the packed observations");
             return LG_ECUDA;
         }
+        scatter_small();
         return LG_OK;
     }
     CU(cudaStreamSynchronize(s));
+    scatter_small();
     return LG_OK;
 }
 

@@ -468,8 +468,12 @@ class _HostPool:
         if len(lst) < self.keep:
             lst.append(block)
 
+    SMALL = 1 << 18  # below this, np.empty is cheaper than a lease (no page faults to save)
+
     def take(self, shape, dtype) -> np.ndarray:
         import weakref
+        if int(np.prod(shape)) * np.dtype(dtype).itemsize < self.SMALL:
+            return np.empty(shape, dtype)
         key = (tuple(shape), np.dtype(dtype).str)
         lst = self.free.get(key)
         block = lst.pop() if lst else np.empty(shape, dtype)
