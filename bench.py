@@ -534,8 +534,9 @@ def main():
         t0 = time.perf_counter()
         nenv.step(a0)  # sizes the timed loop
         per = time.perf_counter() - t0
-        # at least e2e_steps steps and ~0.3 s of them (small batches are microseconds per step)
-        n_steps = max(args.e2e_steps, min(500, int(0.5 / max(per, 1e-6))))
+        # at least e2e_steps steps and ~1.5 s of them (host-memory-bound: one
+        # short sample is noisy; small batches are microseconds per step)
+        n_steps = max(args.e2e_steps, min(2000, int(1.5 / max(per, 1e-6))))
         if fresh and per > 0.5:
             n_steps = 3
         if world > 1:
