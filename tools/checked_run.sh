@@ -5,4 +5,4 @@
 #   nvcc ... -DLG_CHECKS -o variants/checked.so; bash tools/checked_run.sh
 export LG_LIB_PATH=variants/checked.so
 timeout 600 python tools/sanitize_cases.py > gpurun_out/checked_cases.log 2>&1; echo "cases rc=$?"; tail -2 gpurun_out/checked_cases.log
-timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_full_size.py tests/test_gpu_reference_semantics.py -m gpu -q > gpurun_out/checked_tests.log 2>&1; echo "tests rc=$?"; tail -2 gpurun_out/checked_tests.log
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_full_size.py tests/test_gpu_reference_semantics.py tests/test_gpu_chain.py tests/test_gpu_trunk.py -m gpu -q > gpurun_out/checked_tests.log 2>&1; echo "tests rc=$?"; tail -2 gpurun_out/checked_tests.log
