@@ -213,3 +213,33 @@ def test_step_random_argument_checks():
         env.step_random(0, b["obs"], b["reward"], b["done"], actions_out=b["acts"].int())
     _chain_step(env, b, 0)
     assert env.errors() == 0
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_chained_random_config_fuzz(seed):
+    """Random configs (test_gpu_parity._random_config) and batch sizes that
+    reach every kernel family: the chained path equals the unchained one."""
+    from tests.test_gpu_parity import _random_config
+    rng = np.random.default_rng(7000 + seed)
+    cfg = _random_config(rng)
+    n = int(rng.choice([37, 300, 4096 + 3, 20000, 40001]))
+    try:
+        a = BatchEnv(cfg, n, seed=seed, validate=False)
+        b = BatchEnv(cfg, n, seed=seed, validate=False)
+    except ValueError:
+        pytest.skip("config rejected on device (limits)")
+    ba, bb = _buffers(a), _buffers(b)
+    a.reset(out=ba["obs"])
+    b.reset(out=bb["obs"])
+    if a.errors() or b.errors():
+        pytest.skip("reset flagged (pinpoints do not fit)")
+    for i in range(30):
+        _chain_step(a, ba, 50 + i)
+        _seq_step(b, bb, 50 + i)
+    torch.cuda.synchronize()
+    for k in ("obs", "reward", "done", "acts"):
+        assert torch.equal(ba[k], bb[k]), k
+    for k in ba["info"]:
+        assert torch.equal(ba["info"][k], bb["info"][k]), k
+    _same_state(a.state_dict(), b.state_dict())
+    assert a.errors() == b.errors()
