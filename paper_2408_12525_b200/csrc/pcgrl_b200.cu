@@ -723,7 +723,9 @@ extern "C" int lg_create(const lg_config *cfg, int64_t n_envs, int64_t global_of
         p.env_smem = slot;
         e->team = 1;
         const char *tb = getenv("LG_SOLO_THREADS");
-        int warp_threads = tb ? atoi(tb) : 64;
+        // dungeon: 4-warp blocks (c3 steady state with the chained launches
+        // 593 -> 608 M env-steps/s over 3 runs each); binary: 2 (equal either way)
+        int warp_threads = tb ? atoi(tb) : (cfg->domain == 2 ? 128 : 64);
         if (warp_threads != 32 && warp_threads != 64 && warp_threads != 128) warp_threads = 64;
         if (n_envs >= 148LL * 4 * 32) {  // >= 4 warps per SM: each warp writes its own 32 envs
             e->threads = warp_threads;
