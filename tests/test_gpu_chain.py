@@ -243,3 +243,19 @@ def test_chained_random_config_fuzz(seed):
         assert torch.equal(ba["info"][k], bb["info"][k]), k
     _same_state(a.state_dict(), b.state_dict())
     assert a.errors() == b.errors()
+
+
+@pytest.mark.parametrize("n", [1, 300, 20000])
+def test_chained_steps_without_observations(n):
+    """obs=None (no observation written), down to a single env."""
+    cfg = EnvConfig(domain="maze", representation="turtle", max_steps=9)
+    a, b, ba, bb = _pair(dict(domain="maze", representation="turtle", max_steps=9), n)
+    for i in range(20):
+        a.step_random(900 + i, None, ba["reward"], ba["done"], ba["info"], ba["stats"], actions_out=ba["acts"])
+        b.random_actions(900 + i, out=bb["acts"])
+        b.step_raw(bb["acts"], None, bb["reward"], bb["done"], bb["info"], bb["stats"])
+    torch.cuda.synchronize()
+    for k in ("reward", "done", "acts"):
+        assert torch.equal(ba[k], bb[k]), k
+    _same_state(a.state_dict(), b.state_dict())
+    assert cfg.n_actions == 8
