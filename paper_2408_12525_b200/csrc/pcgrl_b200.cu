@@ -781,9 +781,11 @@ extern "C" int lg_create(const lg_config *cfg, int64_t n_envs, int64_t global_of
     if (e->geo != 1) {
         e->team = e->geo == 16 ? 16 : 32;
         const char *tt = getenv("LG_TEAM_THREADS");
-        // 64x64 maps: one env (one warp) per block, so a block's slot frees as
-        // soon as its env is done (recompute times vary); c4 92M vs 87M env-steps/s
-        e->threads = tt ? atoi(tt) : (e->geo == 64 ? 32 : 64);
+        // one-warp blocks, so a block's slot frees as soon as its envs are done
+        // (recompute times vary): 64x64 maps, one env per block (c4 92 M vs
+        // 87 M env-steps/s); 16-lane teams, two envs per block (c1 +5%, c2 +3%
+        // with the chained launches); 32-row teams keep two warps
+        e->threads = tt ? atoi(tt) : (e->geo == 32 ? 64 : 32);
         if (e->threads != 32 && e->threads != 64 && e->threads != 128 && e->threads != 256) e->threads = 64;
         e->E = e->threads / e->team;
         int rows = e->geo == 16 ? 16 : e->geo == 32 ? 32 : 64;
