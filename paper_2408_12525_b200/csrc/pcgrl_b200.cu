@@ -1229,7 +1229,7 @@ static int launch_conv1_tri(const uint32_t *bits, long long B, int O, const floa
                             void *out, int relu, cudaStream_t s) {
     Conv1TriDiv dv;
     fastdiv_init(dv.p, (uint32_t)(O - 2));
-    const int EB = 32;
+    const int EB = LG_TRI_EB;
     const size_t tables = (size_t)3 * 216 * 24 * 2 + (size_t)9 * 16 * 20 * sizeof(float);
     const size_t tri = ((size_t)EB * O * (O - 2) + 15) & ~(size_t)15;
     const size_t words = ((size_t)EB * 4 * O * O + 31) / 32 + 1;

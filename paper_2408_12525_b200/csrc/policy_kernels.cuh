@@ -273,12 +273,15 @@ __device__ __forceinline__ uint32_t onehot_code(uint32_t m) {  // 4-bit cell mas
 #ifndef LG_TRI_THREADS
 #define LG_TRI_THREADS 512
 #endif
+#ifndef LG_TRI_EB
+#define LG_TRI_EB 32  // envs per block iteration (a power of two, <= 32)
+#endif
 __global__ void __launch_bounds__(LG_TRI_THREADS) conv1_tri_kernel(const uint32_t *__restrict__ bits, long long B, int O,
                                                         const float *__restrict__ w,
                                                         const float *__restrict__ bias, void *out, int relu,
                                                         const Conv1TriDiv dv) {
     extern __shared__ __align__(16) float csm[];
-    constexpr int C = 4, K = 16, RS = K + 4, NI = 216, EB = 32;
+    constexpr int C = 4, K = 16, RS = K + 4, NI = 216, EB = LG_TRI_EB;
     // Row-triple tables in half precision, 16 channels per 48-byte row (32
     // used: the rows land 12 banks apart): an output pixel reads 96 bytes of
     // shared memory, not 192 -- the kernel was bound by shared-memory
@@ -348,7 +351,7 @@ __global__ void __launch_bounds__(LG_TRI_THREADS) conv1_tri_kernel(const uint32_
             int e, px;
             if (ne == EB) {  // envs fastest: a warp's 16-byte stores fill whole core-matrix rows
                 e = it & (EB - 1);
-                px = it >> 5;
+                px = it / EB;
             } else {
                 px = it / ne;
                 e = it - px * ne;
