@@ -152,6 +152,15 @@ __device__ __forceinline__ void tmem_zero32(uint32_t taddr) {
         : "memory");
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// 16 registers -> 16 consecutive columns of this warp's 32 lanes
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+        "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
 
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
@@ -211,20 +220,25 @@ constexpr int TK_RING = 4;                    // conv1 rows in shared memory
 #endif
 constexpr int TK_W3 = TK_W3_SLOTS;            // FC weight blocks in flight (released in pairs)
 constexpr int TK_EPI = 2;                     // epilogue warp groups (output row R -> group R % 2)
-constexpr int TK_A3G = TK_A3_SLOTS;           // conv2 activation blocks (FC A operand) per group
+#ifndef TK_A3_TMEM
+#define TK_A3_TMEM 0  // extra FC A-operand slots per group kept in TMEM (16 columns each, TS MMAs)
+#endif
+constexpr int TK_A3S = TK_A3_SLOTS;           // conv2 activation blocks in shared memory per group
+constexpr int TK_A3G = TK_A3_SLOTS + TK_A3_TMEM;  // activation slots (FC A operand) per group
 constexpr int TK_THREADS = 64 + 128 * TK_EPI + 32;  // + the FC issuer warp
 constexpr int TK_MAXNA = 16;
 constexpr uint32_t TK_BLK = 4096;             // one 128 x 16 bf16 block
 // TMEM columns: one conv2 accumulator row (CW pixels x 32 channels) per epilogue group + FC accumulator
 constexpr uint32_t TK_T_ACC = 0;
 constexpr uint32_t TK_T_D3 = TK_T_ACC + TK_EPI * TK_CW * 32;  // 448
-static_assert(TK_T_D3 + 64 <= 512, "TMEM budget");
+constexpr uint32_t TK_T_A3 = TK_T_D3 + 64;                      // TMEM activation slots
+static_assert(TK_T_A3 + TK_EPI * TK_A3_TMEM * 16 <= 512, "TMEM budget");
 static_assert(TK_CW <= 7, "conv2_row dispatch covers chunk widths 1..7");
 constexpr uint32_t TK_OFF_RING = 0;
 constexpr uint32_t TK_OFF_W2 = TK_OFF_RING + TK_RING * TK_RC * TK_BLK;  // 147456: 3 x [96 x 16] bf16
 constexpr uint32_t TK_OFF_W3 = TK_OFF_W2 + 3 * 3072;
 constexpr uint32_t TK_OFF_A3 = TK_OFF_W3 + TK_W3 * 4096;
-constexpr uint32_t TK_OFF_HEAD = TK_OFF_A3 + TK_EPI * TK_A3G * 8192;
+constexpr uint32_t TK_OFF_HEAD = TK_OFF_A3 + TK_EPI * TK_A3S * 8192;
 constexpr uint32_t TK_OFF_BIAS = TK_OFF_HEAD + (TK_MAXNA + 1) * 64 * 4;
 constexpr uint32_t TK_OFF_BAR = (TK_OFF_BIAS + (32 + 64 + TK_MAXNA + 1) * 4 + 7) & ~7u;  // 8-byte aligned
 constexpr int TK_NBAR = 2 * TK_RING + TK_W3 + TK_W3 / 2 + 2 * TK_EPI + 2 * TK_EPI * TK_A3G + 2;
@@ -468,15 +482,22 @@ __global__ void __launch_bounds__(TK_THREADS, 1) trunk_kernel_t(const TrunkParam
                 const int g = R % TK_EPI;
                 int &kg = g ? kg1 : kg0;
                 for (int j = 0; j < cw; j++, pix++, kg++) {  // D3 += relu(conv2)(pixel) x W3(pixel)
-                    const int a = g * TK_A3G + kg % TK_A3G, w = pix % TK_W3;
+                    const int sl = kg % TK_A3G, a = g * TK_A3G + sl, w = pix % TK_W3;
                     tc::mbar_wait(BAR(A3F + a), (uint32_t)((kg / TK_A3G) & 1));
                     tc::mbar_wait(BAR(W3F + w), (uint32_t)((pix / TK_W3) & 1));
                     tc::tc_after();
                     if (tc::elect_one()) {
-                        tc::mma_bf16(T_D3, d_a3 + ((uint32_t)a * 8192u >> 4), d_w3 + ((uint32_t)w * 4096u >> 4), ID3,
-                                     pix > 0 ? 1u : 0u);
-                        tc::mma_bf16(T_D3, d_a3 + (((uint32_t)a * 8192u + 4096u) >> 4),
-                                     d_w3 + (((uint32_t)w * 4096u + 2048u) >> 4), ID3, 1u);
+                        if (TK_A3_TMEM == 0 || sl < TK_A3S) {  // A from shared memory
+                            const uint32_t as = (uint32_t)(g * TK_A3S + sl) * 8192u;
+                            tc::mma_bf16(T_D3, d_a3 + (as >> 4), d_w3 + ((uint32_t)w * 4096u >> 4), ID3,
+                                         pix > 0 ? 1u : 0u);
+                            tc::mma_bf16(T_D3, d_a3 + ((as + 4096u) >> 4), d_w3 + (((uint32_t)w * 4096u + 2048u) >> 4),
+                                         ID3, 1u);
+                        } else {  // A from TMEM: 16 columns, channels (2c, 2c + 1) in column c
+                            const uint32_t at = tmem + TK_T_A3 + 16u * (uint32_t)(g * TK_A3_TMEM + sl - TK_A3S);
+                            tc::mma_bf16_ts(T_D3, at, d_w3 + ((uint32_t)w * 4096u >> 4), ID3, pix > 0 ? 1u : 0u);
+                            tc::mma_bf16_ts(T_D3, at + 8u, d_w3 + (((uint32_t)w * 4096u + 2048u) >> 4), ID3, 1u);
+                        }
                         tc::mma_commit(BAR(A3E + a));
                         if (w & 1) tc::mma_commit(BAR(W3E + w / 2));
                     }
@@ -520,7 +541,7 @@ __global__ void __launch_bounds__(TK_THREADS, 1) trunk_kernel_t(const TrunkParam
                 tc::tmem_ld32(acc + 32u * j, r);
                 tc::tmem_wait_ld();
                 tc::tmem_zero32(acc + 32u * j);
-                const int a = grp * TK_A3G + k % TK_A3G;
+                const int sl = k % TK_A3G, a = grp * TK_A3G + sl;
 #ifdef TK_PROF
                 long long ea = clock64();
 #endif
@@ -528,7 +549,25 @@ __global__ void __launch_bounds__(TK_THREADS, 1) trunk_kernel_t(const TrunkParam
 #ifdef TK_PROF
                 eprof[1] += clock64() - ea;
 #endif
-                uint8_t *a3 = sm + TK_OFF_A3 + a * 8192u;
+                if (TK_A3_TMEM > 0 && sl >= TK_A3S) {  // TMEM slot: bf16 pairs, one column per two channels
+                    uint32_t wd[16];
+#pragma unroll
+                    for (int c2 = 0; c2 < 16; c2++) {
+                        float x0 = __uint_as_float(r[2 * c2]) + b2r[2 * c2];
+                        float x1 = __uint_as_float(r[2 * c2 + 1]) + b2r[2 * c2 + 1];
+                        x0 = x0 > 0.f ? x0 : 0.f;
+                        x1 = x1 > 0.f ? x1 : 0.f;
+                        __nv_bfloat162 h2 = __floats2bfloat162_rn(x0, x1);
+                        wd[c2] = *reinterpret_cast<uint32_t *>(&h2);
+                    }
+                    tc::tmem_st16(tmem + lane_off + TK_T_A3 + 16u * (uint32_t)(grp * TK_A3_TMEM + sl - TK_A3S), wd);
+                    tc::tmem_wait_st();
+                    tc::tc_before();
+                    tc::mbar_arrive(BAR(A3F + a));
+                    __syncwarp();
+                    continue;
+                }
+                uint8_t *a3 = sm + TK_OFF_A3 + (uint32_t)(grp * TK_A3S + sl) * 8192u;
 #pragma unroll
                 for (int kc = 0; kc < 4; kc++) {  // 8 channels -> one 16-byte core-matrix row
                     uint32_t wd[4];
